@@ -1,0 +1,123 @@
+"""SDRT residual in Appendix-B matrix form + classical RK4 (oracle; test infrastructure only).
+
+State layout: U has shape (N_sol, N_V, K): the Appendix-B state matrix
+U^(u) = N_sol x N_V|Omega_e| (PAPER.md Eq. state_matrices l.2835-2843).
+
+Residual, step by step in the paper's order (§2.1 l.268-350, App. B l.2855-2925):
+  1. U_ext = M0 U ;  U_u = M12 U ;  U_int = P U_u                 Eqs. l.2860-2865
+  2. (viscous) per face point C = (1/2-beta) u_L + (1/2+beta) u_R l.282-291
+     Q~ = M16 C + M15 U_int                                     l.2877-2880
+     Q = J^-T Q~ (per solution point)                           l.299-302
+     Q_ext = M5 Q ; Q_u = M18 Q                                 l.2882-2900
+  3. F~_u[d] = (detJ J^-1 f(U_u, Q_u))_d ; F~_int = M19.P2 F~_u  Eq. normal_transformed_flux l.305-311
+  4. per face point: common flux F(u_L, u_R, q_L, q_R, n_L), computed ONCE per face
+     point; D~_L = +s_L F, D~_R = -s_R F, s = detJ |J^-T n~|      l.312-340 (O9, O28)
+  5. R~ = M14 D~ + M13 F~_int                                    Eq. residual_sdrt_matrices l.2919-2925
+  6. dU/dt = -R~ / detJ                                          l.347-350
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import physics as phys
+from .operators import build_operators
+
+
+class Residual:
+    def __init__(self, mesh, ph):
+        self.mesh = mesh
+        self.ph = ph
+        self.ops = build_operators(mesh.etype, mesh.p)
+        o, m = self.ops, mesh
+        D = o.nd
+        # per external point reference normal and metric scale
+        fn = o.ext_normal                                         # N_ext x D
+        jn = np.einsum("kji,sj->ski", m.Jinv, fn)                 # J^-T n~  [s, k, i]
+        nrm = np.linalg.norm(jn, axis=2)                          # N_ext x K
+        self.s = m.detJ[None, :] * nrm                            # N_ext x K
+        self.nphys = jn / nrm[..., None]                          # N_ext x K x D
+        # face-point lists (flattened over faces x face points)
+        nfp = o.nfp
+        F = m.face_elem.shape[0]
+        self.fL = np.repeat(m.face_elem[:, 0].astype(np.int64), nfp)
+        self.fR = np.repeat(m.face_elem[:, 1].astype(np.int64), nfp)
+        q = np.tile(np.arange(nfp), F)
+        self.pL = m.face_lface[:, 0].astype(np.int64).repeat(nfp) * nfp + q
+        self.pR = m.face_lface[:, 1].astype(np.int64).repeat(nfp) * nfp + m.face_perm.astype(np.int64).reshape(-1)
+        self.nL = self.nphys[self.pL, self.fL].T                  # D x (F.nfp)
+
+    # ---------------------------------------------------------------- helpers
+    def _face_scatter(self, valL, valR, shape):
+        out = np.zeros(shape)
+        out[self.pL, :, self.fL] = valL
+        out[self.pR, :, self.fR] = valR
+        return out
+
+    def gradient(self, U):
+        """Physical gradient Q (D, N_sol, N_V, K) of the conserved variables (step 2)."""
+        o, m, ph = self.ops, self.mesh, self.ph
+        nsol, NV, K = U.shape
+        D = o.nd
+        Uf = U.reshape(nsol, NV * K)
+        Uext = (o.M0 @ Uf).reshape(o.next, NV, K)
+        Uu = (o.M12 @ Uf).reshape(o.nu, NV, K)
+        uL = Uext[self.pL, :, self.fL]                            # (F.nfp, NV)
+        uR = Uext[self.pR, :, self.fR]
+        Cf = phys.common_value(ph, uL, uR)
+        C = self._face_scatter(Cf, Cf, (o.next, NV, K))
+        Uint = (o.P @ Uu.reshape(o.nu, NV * K))
+        Qt = o.M16 @ C.reshape(o.next, NV * K) + o.M15 @ Uint      # (D.nsol, NV.K)
+        Qt = Qt.reshape(D, nsol, NV, K)
+        return np.einsum("kji,jsak->isak", m.Jinv, Qt)            # q_i = sum_j Jinv[j,i] q~_j
+
+    def __call__(self, U):
+        o, m, ph = self.ops, self.mesh, self.ph
+        nsol, NV, K = U.shape
+        D = o.nd
+        Uf = U.reshape(nsol, NV * K)
+        Uext = (o.M0 @ Uf).reshape(o.next, NV, K)
+        Uu = (o.M12 @ Uf).reshape(o.nu, NV, K)
+        Qext = Qu = None
+        if ph.viscous:
+            Q = self.gradient(U)
+            Qext = np.stack([(o.M0 @ Q[d].reshape(nsol, NV * K)).reshape(o.next, NV, K)
+                             for d in range(D)])
+            Qu = np.stack([(o.M12 @ Q[d].reshape(nsol, NV * K)).reshape(o.nu, NV, K)
+                           for d in range(D)])
+        # step 3: transformed flux at unique internal points
+        f = phys.flux(ph, np.moveaxis(Uu, 1, 0), None if Qu is None else np.moveaxis(Qu, 2, 1))
+        # f: (D, NV, nu, K);  f~_d = detJ sum_j Jinv[d, j] f_j
+        ft = np.einsum("k,kdj,jauk->duak", m.detJ, m.Jinv, f)      # (D, nu, NV, K)
+        Fint = o.M19P2 @ ft.reshape(D * o.nu, NV * K)              # (N_int, NV.K)
+        # step 4: common flux once per face point
+        uL = Uext[self.pL, :, self.fL].T                           # (NV, F.nfp)
+        uR = Uext[self.pR, :, self.fR].T
+        qL = qR = None
+        if ph.viscous:
+            qL = np.stack([Qext[d][self.pL, :, self.fL].T for d in range(D)])
+            qR = np.stack([Qext[d][self.pR, :, self.fR].T for d in range(D)])
+        Fc = phys.common_flux(ph, uL, uR, qL, qR, self.nL)         # (NV, F.nfp)
+        Dt = self._face_scatter((self.s[self.pL, self.fL] * Fc).T,
+                                (-self.s[self.pR, self.fR] * Fc).T, (o.next, NV, K))
+        # step 5-6
+        R = o.M14 @ Dt.reshape(o.next, NV * K) + o.M13 @ Fint
+        return (-R.reshape(nsol, NV, K)) / m.detJ[None, None, :]
+
+    def face_common_flux(self, U):
+        """Per-face-point common flux F (NV, F.nfp) for the antisymmetry check (O28)."""
+        raise NotImplementedError
+
+
+def rk4_step(L, u, dt):
+    """Classical RK4, c = (0, 1/2, 1/2, 1), b = (1/6, 1/3, 1/3, 1/6) (reading O22)."""
+    k1 = L(u)
+    k2 = L(u + 0.5 * dt * k1)
+    k3 = L(u + 0.5 * dt * k2)
+    k4 = L(u + dt * k3)
+    return u + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+
+def integrate(L, u, dt, nsteps):
+    for _ in range(nsteps):
+        u = rk4_step(L, u, dt)
+    return u
