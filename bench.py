@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""SDRT residual / RK4 throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl sdrt|reference]
+
+A "step" is one classical-RK4 step (4 residual stages, every §8(a) row) of the
+configuration's full mesh.  value = N_sol * N_V * K_elems * 4 * steps (summed over
+ranks) / max-over-ranks device time / 1e9  [GDOF-stage/s]  (1/PM of PAPER.md
+Eq. performance_per_iter_measure l.2942-2951 with N_RK = 4).
+
+N > 1 (torchrun, one rank per GPU): weak scaling, each rank advances its own copy
+of the configuration's periodic mesh (replicas; the NCCL halo path is DESIGN.md
+"next").  --impl reference times the CPU oracle (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from dataclasses import replace
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from sdrt_inputs import CONFIGS, initial_state  # noqa: E402
+
+METRIC = "SDRT residual GDOF-stage/s (fp64)"
+# reference-arm sample size (patterns per axis) so K steps of the oracle take ~1 s each
+REF_SUBBOX = {"c1": 8, "c2": 40, "c3": 6, "c4": 8, "c5": 4}
+UNIT = "GDOF-stage/s"
+WORKLOADS = {
+    "c1": "c1: 2D linear advection, quad p=2, 8^2 periodic",
+    "c2": "c2: 2D isentropic Euler vortex, tri p=3, 40^2x2",
+    "c3": "c3: 3D linear advection-diffusion, hex p=4, 24^3",
+    "c4": "c4: 3D Taylor-Green vortex NS, hex p=3, 32^3 (Re=1600, Ma=0.1)",
+    "c5": "c5: 3D Taylor-Green vortex NS, tet p=3, 48^3x6",
+}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def dims(cfg):
+    D = cfg.nd
+    p = cfg.p
+    if cfg.etype == "quad":
+        ns, ne, nu = (p + 1) ** 2, 4 * (p + 1), 2 * p * (p + 1)
+    elif cfg.etype == "hex":
+        ns, ne, nu = (p + 1) ** 3, 6 * (p + 1) ** 2, 3 * p * (p + 1) ** 2
+    elif cfg.etype == "tri":
+        ns, ne, nu = (p + 1) * (p + 2) // 2, 3 * (p + 1), p * (p + 1) // 2
+    else:
+        ns, ne, nu = (p + 1) * (p + 2) * (p + 3) // 6, 2 * (p + 1) * (p + 2), p * (p + 1) * (p + 2) // 6
+    return D, ns, ne, nu
+
+
+def kernel_bytes(cfg, K):
+    """Algorithmic bytes per launch of each kernel of the v1 path (each input array
+    read once, each output written once; fp64)."""
+    D, ns, ne, nu = dims(cfg)
+    V = cfg.nvars
+    b = 8 * V * K
+    return {
+        "interp_ext(M0)": b * (ns + ne),
+        "interp_int(M12)": b * (ns + nu),
+        "common_value": b * (2 * ne + ne),
+        "gradient(M16|M15P)": b * (ne + nu + D * ns),
+        "metric_grad": b * 2 * D * ns,
+        "grad_interp_ext(M5)": b * D * (ns + ne),
+        "grad_interp_int(M18)": b * D * (ns + nu),
+        "int_flux": b * (nu + (D * nu if cfg.eq in ("ns", "linadvdiff") else 0) + D * nu),
+        "face_flux": b * (2 * ne + (2 * D * ne if cfg.eq in ("ns", "linadvdiff") else 0) + ne),
+        "divergence(M14|M13M19P2)": b * (ne + D * nu + ns),
+        "rk_update": b * ns * 4.25,
+    }
+
+
+def stage_model_bytes(cfg):
+    """SURVEY.md §8(d) algorithmic bytes per DOF-stage (element-local data flow)."""
+    D, ns, ne, nu = dims(cfg)
+    V = cfg.nvars
+    b = 4 * ns * V + 2 * ne * V
+    if cfg.eq in ("ns", "linadvdiff"):
+        ndq = D if cfg.eq == "ns" else 1
+        X = ndq * ne * V * (1 if abs(cfg.beta) == 0.5 else 2)
+        b += ne * V + X
+    return 8.0 * b / (ns * V)
+
+
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.strip().split(",") for l in open(self.f.name) if l.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def threads_used():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_stage_rate(cfg, nstages, warm=0, N=None):
+    """Time the CPU oracle: nstages residual evaluations + RK axpys on the full mesh,
+    or on an N^D-pattern periodic sub-box with the same h (bounded sample)."""
+    from oracle.mesh import build_mesh
+    from oracle.physics import Physics
+    from oracle.residual import Residual
+    if N is not None and N < cfg.N:
+        hi = tuple(l + (h - l) * N / cfg.N for l, h in zip(cfg.lo, cfg.hi))
+        cfg = replace(cfg, N=N, hi=hi)
+    m = build_mesh(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi)
+    R = Residual(m, Physics(cfg.eq, cfg.nd, **cfg.physics_kwargs()))
+    U = initial_state(cfg, m.sol_coords())
+    dof = U.size
+    for _ in range(warm):
+        U = U + 0.0 * R(U)
+    t0 = time.perf_counter()
+    u = U
+    for s in range(nstages):
+        k = R(u)
+        u = U + (0.5 * cfg.dt) * k
+    t = time.perf_counter() - t0
+    return dof * nstages / t / 1e9, t, dof
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    nsub = min(cfg.N, REF_SUBBOX.get(cfg.name, cfg.N))
+    val, t, dof = oracle_stage_rate(cfg, args.steps, warm=args.warmup, N=nsub)
+    cores = threads_used()
+    sample = (f"each step = 1 RK stage (residual + RK axpy) of the {cfg.name} workload on a "
+              f"{nsub}^{cfg.nd}-pattern periodic sub-box with the same h, p and physics ({dof} DOF); "
+              f"{args.warmup} untimed stages first")
+    out = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": WORKLOADS[cfg.name], "elements": cfg.K,
+                                           "dof": dof, "device": "host cpu"},
+           "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="sdrt", choices=["sdrt", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2105_08632_b200.build import build
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.barrier()
+    from paper_2105_08632_b200.solver import Solver
+
+    S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, **cfg.physics_kwargs())
+    U0 = initial_state(cfg, S.sol_coords())
+    U = S.to_device(U0)
+    nsol, nv, Kp = S.shape
+    K = S.K
+    dof = nsol * nv * K
+    stream = torch.cuda.current_stream(dev)
+
+    # ---------------------------------------------------------------- warm-up
+    S.rk_step(U, cfg.dt, args.warmup)
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    time.sleep(0.3)
+
+    # ---------------------------------------------------------------- timed region
+    S.set_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    launches = 0
+    for _ in range(args.steps):
+        S.rk_step(U, cfg.dt, 1)
+        launches += S.last_launches()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ktimes = S.kernel_times()
+    S.set_timing(False)
+    # repeat once more without per-kernel events for a clean clock record window
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        S.rk_step(U, cfg.dt, 1)
+    e3.record(stream)
+    torch.cuda.synchronize(dev)
+    ms_clean = e2.elapsed_time(e3)
+    clk = clocks.stop()
+    finite = bool(torch.isfinite(U[:, :, :K]).all().item())
+
+    t = torch.tensor([ms, ms_clean], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max, ms_clean_max = float(t[0]), float(t[1])
+    total_dof_stages = dof * 4 * args.steps * world
+    value = total_dof_stages / (ms_max * 1e-3) / 1e9
+
+    # ---------------------------------------------------------------- e2e (host buffers)
+    pin = torch.empty(S.shape, dtype=torch.float64).pin_memory()
+    pin.copy_(U.cpu())
+    outp = torch.empty_like(pin).pin_memory()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(args.steps):
+        U.copy_(pin, non_blocking=True)
+        S.rk_step(U, cfg.dt, 1)
+        outp.copy_(U, non_blocking=True)
+    a1.record(stream)
+    torch.cuda.synchronize(dev)
+    te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_val = total_dof_stages / (float(te[0]) * 1e-3) / 1e9
+    state_bytes = U.numel() * 8
+
+    # ---------------------------------------------------------------- roofline
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs")
+    peak_note = "MEASURED_PEAKS.json hbm_gbs" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
+    hbm = hbm or 6650.0
+    kb = kernel_bytes(cfg, K)
+    dom, dom_ms, dom_n = None, -1.0, 0
+    for nm, (tms, cnt) in ktimes.items():
+        if tms > dom_ms:
+            dom, dom_ms, dom_n = nm, tms, cnt
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(dom)
+    achieved = kb[dom] / (dom_ms / dom_n * 1e-3) / 1e9 if dom else None
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm if achieved else None, "traffic": traffic,
+            "bytes_per_launch": kb.get(dom), "avg_launch_ms": dom_ms / dom_n if dom else None,
+            "peak_source": peak_note,
+            "step_share": dom_ms / ms if dom else None}
+    model_b = stage_model_bytes(cfg)
+    stage_roof = {"model_bytes_per_dof_stage": model_b,
+                  "achieved_gbs": model_b * dof * 4 * args.steps / (ms_clean_max * 1e-3) / 1e9,
+                  "frac_of_hbm": model_b * dof * 4 * args.steps / (ms_clean_max * 1e-3) / 1e9 / hbm,
+                  "ceiling_gdof_stage_s": hbm / model_b}
+
+    # ---------------------------------------------------------------- cpu baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, tt, _ = oracle_stage_rate(cfg, 1)
+            cpu = {"value": v, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
+                   "sample": f"1 RK stage (residual + RK axpy) of the full {cfg.name} mesh, "
+                             f"{tt:.1f} s of CPU time"}
+        except Exception as ex:  # report, do not fail the bench
+            cpu = {"value": None, "unit": UNIT, "cores": threads_used(), "kind": "oracle",
+                   "sample": f"failed: {ex!r}"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": WORKLOADS[cfg.name], "elements_per_gpu": K, "dof_per_gpu": dof,
+                          "p": cfg.p, "dt": cfg.dt, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                          "l2": "working set > L2 (state 3 registers + traces >> 126 MB); no flush needed"
+                          if dof * 8 * 3 > 126e6 else "working set fits L2 (small config)"},
+               "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,
+               "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                       "d2h_bytes_per_step": state_bytes},
+               "gpu_launches": launches, "clocks": clk, "kernel_ms": {k: v[0] for k, v in ktimes.items()},
+               "ms_per_step_no_events": ms_clean_max / args.steps, "state_finite": finite}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

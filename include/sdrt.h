@@ -1,0 +1,146 @@
+/*
+ * sdrt.h — C ABI of the B200-native SDRT residual / RK4 library (libsdrt.so).
+ *
+ * Spectral Difference Raviart-Thomas (SDRT), arXiv 2105.08632:
+ *   semi-discrete residual dU/dt = -J^-1 (div~ f~)  ....... §2.1, l.268-350
+ *   matrix form R~ = M14 D~ + M13 M19 P2 F~ ................ App. B, l.2828-2925
+ *   explicit Runge-Kutta (classical RK4) ................... l.351, l.1124
+ *
+ * Conventions
+ *   - All entry points return sdrt_status (0 = OK). On failure sdrt_last_error()
+ *     returns a thread-local message. No exception crosses the ABI.
+ *   - Opaque handles are library-owned host objects freed by their _destroy.
+ *   - ALL device memory is caller-owned (plain device pointers). The library never
+ *     calls cudaMalloc: the context lives in one caller-provided workspace of
+ *     sdrt_ctx_workspace_bytes() bytes (256-byte aligned).
+ *   - Streams are cudaStream_t passed as void*. Calls enqueue asynchronously.
+ *   - State layout (every fp64 state-like array): row-major [row][alpha*K_pad + n]
+ *     = [N_sol][N_V][K_pad], point-major, then variable, element fastest. This is
+ *     App. B's state matrix U^(u) (N_sol x N_V|Omega_e|, l.2835-2843). Columns
+ *     n >= K (padding) are ignored on input and left unspecified on output.
+ *   - Element order: pattern (i,j[,k]) x fastest, then subcell s; id = pattern*N_p+s
+ *     (DESIGN.md "Mesh"); reference point orders: DESIGN.md "Ordering".
+ */
+#ifndef SDRT_H
+#define SDRT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDRT_ABI_VERSION 1
+
+typedef enum {
+  SDRT_OK = 0,
+  SDRT_E_INVALID_ARG = -1,
+  SDRT_E_UNSUPPORTED = -2,
+  SDRT_E_ILL_CONDITIONED = -3,
+  SDRT_E_CUDA = -4,
+  SDRT_E_NCCL = -5,
+  SDRT_E_WORKSPACE = -6,
+  SDRT_E_DIVERGED = -7,
+  SDRT_E_INTERNAL = -8
+} sdrt_status;
+
+/* element types (App. A); N_p = 1, 2, 1, 6 sub-cells per pattern (l.499) */
+typedef enum { SDRT_QUAD = 0, SDRT_TRI = 1, SDRT_HEX = 2, SDRT_TET = 3 } sdrt_etype;
+typedef enum { SDRT_SCHEME_SDRT = 0 } sdrt_scheme;
+/* equations: linear advection, linear advection-diffusion (l.1658), Euler
+ * (l.1909-1935), compressible Navier-Stokes (l.2012-2030) */
+typedef enum { SDRT_EQ_LINADV = 0, SDRT_EQ_LINADVDIFF = 1, SDRT_EQ_EULER = 2, SDRT_EQ_NS = 3 } sdrt_eq;
+
+typedef struct {
+  int eq;          /* sdrt_eq */
+  double c[3];     /* advection velocity (linear equations) */
+  double mu;       /* diffusivity (lin.) / dynamic viscosity (NS) */
+  double gamma;    /* ratio of specific heats (Euler/NS) */
+  double Pr;       /* Prandtl number (NS) */
+  double beta;     /* LDG common-value parameter, Eq. common_var_for_grad l.290 */
+  double eta;      /* LDG penalty, l.332-334 */
+} sdrt_physics;
+
+typedef struct sdrt_mesh sdrt_mesh;
+typedef struct sdrt_operators sdrt_operators;
+typedef struct sdrt_ctx sdrt_ctx;
+
+typedef struct {
+  int etype, p, nd;
+  int nsol, next, nint, nu, nfaces, nfp;
+  int nsub;            /* N_p */
+  int N[3];            /* local patterns per axis (this rank) */
+  int Nglobal[3];      /* global patterns per axis */
+  int offset[3];       /* first global pattern index of this rank */
+  int64_t K;           /* local elements */
+  int64_t K_pad;       /* K rounded up to a multiple of 32 */
+  int64_t n_faces;     /* local face count (faces whose left element is local) */
+} sdrt_mesh_info_t;
+
+int sdrt_abi_version(void);
+const char* sdrt_last_error(void);
+
+/* Uniform mesh of N[0] x N[1] (x N[2]) patterns on the box [lo, hi], each pattern
+ * split into N_p sub-cells. periodic[d] must be 1 (only
+ * periodic meshes are supported by this hot path). N[d] >= 3.
+ * Multi-rank: the pattern grid is block-partitioned by pgrid (pgrid[d] divides
+ * N[d]); rank r owns block (r % pg0, (r / pg0) % pg1, r / (pg0 pg1)).
+ * Single rank: rank = 0, nranks = 1, pgrid = NULL.
+ * Errors: SDRT_E_INVALID_ARG (bad sizes), SDRT_E_UNSUPPORTED (etype/p). */
+sdrt_status sdrt_mesh_create(int etype, int p, const int N[3], const double lo[3], const double hi[3],
+                             const int periodic[3], int rank, int nranks, const int pgrid[3],
+                             sdrt_mesh** out);
+sdrt_status sdrt_mesh_info(const sdrt_mesh* m, sdrt_mesh_info_t* out);
+/* Face list of the (local) mesh, faces sorted by (left element, left local face)
+ * (reading O14: left = element whose outward unit normal has its first non-zero
+ * component positive).  face_elem[F][2] = (left, right) element ids (global ids
+ * for multi-rank), face_lface[F][2] local face ids, face_perm[F][nfp] = right's
+ * local face-point index matching the left's point q, is_left[K][nfaces].
+ * Any pointer may be NULL. Host memory, caller-owned. */
+sdrt_status sdrt_mesh_export_maps(const sdrt_mesh* m, int32_t* face_elem, int8_t* face_lface,
+                                  int16_t* face_perm, uint8_t* is_left);
+/* Physical coordinates of the solution points: x[N_sol][D][K] (host). */
+sdrt_status sdrt_mesh_sol_coords(const sdrt_mesh* m, double* x);
+/* Per-element det J (host, [K]), used for conservation sums. */
+sdrt_status sdrt_mesh_detj(const sdrt_mesh* m, double* detj);
+void sdrt_mesh_destroy(sdrt_mesh* m);
+
+/* Appendix-B operators for (etype, p), built in __float128 and rounded once.
+ * Errors: SDRT_E_UNSUPPORTED, SDRT_E_ILL_CONDITIONED (cond(V^f) > 1e12). */
+sdrt_status sdrt_operators_build(int etype, int p, int scheme, sdrt_operators** out);
+/* name in {"M0","M12","M13","M14","M15","M16","P","M19P2","w","xsol","xext","xu"};
+ * dst == NULL queries the shape. Row-major doubles, host memory. */
+sdrt_status sdrt_operators_get(const sdrt_operators* o, const char* name, double* dst, int* rows,
+                               int* cols);
+void sdrt_operators_destroy(sdrt_operators* o);
+
+/* Device workspace size for a context (bytes). */
+size_t sdrt_ctx_workspace_bytes(const sdrt_mesh* m, const sdrt_operators* o, const sdrt_physics* ph);
+/* Create a context over caller-owned device workspace d_ws (>= the size above).
+ * Uploads operators and geometry tables on `stream`. The mesh and operators may be
+ * destroyed afterwards. Errors: SDRT_E_WORKSPACE, SDRT_E_CUDA, SDRT_E_INVALID_ARG. */
+sdrt_status sdrt_ctx_create(const sdrt_mesh* m, const sdrt_operators* o, const sdrt_physics* ph,
+                            void* d_ws, size_t ws_bytes, void* stream, sdrt_ctx** out);
+/* dU/dt = -J^-1 R~ for the device state d_U -> d_dUdt (both [N_sol][N_V][K_pad]). */
+sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* stream);
+/* nsteps classical RK4 steps of size dt, in place on d_U. check_every > 0 syncs the
+ * stream every check_every steps and returns SDRT_E_DIVERGED (message names the
+ * first non-finite / non-physical element and step) if the state went bad. */
+sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream);
+/* Per-kernel device timing (CUDA events recorded on the launching stream around each
+ * kernel) for measurement: enable, run, then read per-kernel totals.  names receives
+ * max_tags NUL-terminated strings of 64 bytes each (may be NULL); ms/counts get the
+ * summed device milliseconds and launch counts per kernel; *ntags the count used.
+ * Reading synchronises on the recorded events and resets the accumulators. */
+sdrt_status sdrt_ctx_set_timing(sdrt_ctx* c, int enable);
+sdrt_status sdrt_ctx_kernel_times(sdrt_ctx* c, int max_tags, char* names, double* ms, int64_t* counts,
+                                  int* ntags);
+/* Number of kernel launches enqueued by the last sdrt_residual / sdrt_rk_step call. */
+int64_t sdrt_ctx_last_launches(const sdrt_ctx* c);
+void sdrt_ctx_destroy(sdrt_ctx* c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDRT_H */

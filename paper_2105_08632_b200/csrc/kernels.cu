@@ -1,0 +1,711 @@
+// SDRT residual + classical RK4 on sm_100a (fp64) and the device-side C ABI.
+//
+// Residual per stage, §2.1 l.268-350 in App. B matrix form l.2855-2925:
+//   U_ext = M0 U, U_u = M12 U                                   (interp kernels)
+//   [viscous] C = (1/2-b) u_L + (1/2+b) u_R at face points      (k_common_value)
+//             Q~ = [M16 | M15 P] [C; U_u], Q = J^-T Q~           (apply + k_metric_grad)
+//             Q_ext = M5 Q, Q_u = M18 Q                          (apply on [s][d][v][n])
+//   F~_u = detJ J^-1 f(U_u, Q_u)                                (k_int_flux)
+//   D~ = +/- s F(u_L, u_R, q_L, q_R, n_L), once per face point   (k_face_flux, canonical L/R)
+//   R~ = [M14 | M13 M19 P2] [D~; F~_u]                           (apply)
+//   dU/dt = -R~/detJ, fused with the RK4 register update        (k_rk)
+// Layouts (element fastest, K_pad columns):  U, R [N_sol][N_V][Kp];  U_ext [N_ext][N_V][Kp];
+// Xg = [C; U_u] [(N_ext+N_u)][N_V][Kp];  Q [N_sol][D][N_V][Kp];  Q_ext [N_ext][D][N_V][Kp];
+// Q_u [N_u][D][N_V][Kp];  Xd = [D~; F~_u] [(N_ext + D N_u)][N_V][Kp].
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "capi_internal.h"
+#include "ctx.h"
+
+namespace sdrt {
+
+#define CUDA_OK(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t err_ = (x);                                                               \
+    if (err_ != cudaSuccess)                                                              \
+      throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(err_) + " at " \
+                               #x);                                                       \
+  } while (0)
+
+// ------------------------------------------------------------------------ kernels
+// Y[r][j] = sum_c M[r][c] X[c][j]  for j in [0, W)  (one row chunk per blockIdx.y)
+__global__ void __launch_bounds__(256) k_apply(OpDev M, const double* __restrict__ X,
+                                               double* __restrict__ Y, int64_t W) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int ch = blockIdx.y;
+  if (j >= W) return;
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+  const int b = M.chunk_ptr[ch], e = M.chunk_ptr[ch + 1];
+  for (int k = b; k < e; ++k) {
+    const double x = X[(int64_t)__ldg(M.col + k) * W + j];
+    const double* v = M.val + (int64_t)k * RB;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = fma(__ldg(v + r), x, acc[r]);
+  }
+  const int r0 = ch * RB;
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+    if (r0 + r < M.rows) Y[(int64_t)(r0 + r) * W + j] = acc[r];
+}
+
+// neighbour of local element n across local face f: element id and its face
+__device__ __forceinline__ int64_t nbr_elem(const GeomDev& g, int64_t n, int s, int f) {
+  int64_t pat = n / g.nsub;
+  int c[3] = {0, 0, 0};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (d < g.nd) {
+      c[d] = (int)(pat % g.Nloc[d]);
+      pat /= g.Nloc[d];
+    }
+  }
+  int64_t id = 0, mul = 1;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (d < g.nd) {
+      int cc = c[d] + g.off[s][f][d];
+      if (cc < 0) cc += g.Nloc[d];
+      if (cc >= g.Nloc[d]) cc -= g.Nloc[d];
+      id += mul * cc;
+      mul *= g.Nloc[d];
+    }
+  }
+  return id * g.nsub + g.nshape[s][f];
+}
+
+// C at external points: (1/2-b) u_L + (1/2+b) u_R, written into Xg rows [0, N_ext)
+template <int NV>
+__global__ void __launch_bounds__(256) k_common_value(GeomDev g, PhysDev ph, const double* __restrict__ Uext,
+                                                      double* __restrict__ Xg) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.y;
+  if (n >= g.K) return;
+  const int s = (int)(n % g.nsub);
+  const int f = e / g.nfp, q = e % g.nfp;
+  const int64_t m = nbr_elem(g, n, s, f);
+  const int e2 = g.nface[s][f] * g.nfp + g.perm[s][f][q];
+  const bool left = g.left[s][f];
+  const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
+#pragma unroll
+  for (int a = 0; a < NV; ++a) {
+    const double mine = Uext[((int64_t)e * NV + a) * g.Kp + n];
+    const double other = Uext[((int64_t)e2 * NV + a) * g.Kp + m];
+    const double uL = left ? mine : other, uR = left ? other : mine;
+    Xg[((int64_t)e * NV + a) * g.Kp + n] = wl * uL + wr * uR;
+  }
+}
+
+// Q = J^-T Q~ in place on [s][d][v][n]
+template <int D, int NV>
+__global__ void __launch_bounds__(256) k_metric_grad(GeomDev g, double* __restrict__ Q, int nsol) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int sp = blockIdx.y;
+  if (n >= g.K) return;
+  const int s = (int)(n % g.nsub);
+#pragma unroll
+  for (int a = 0; a < NV; ++a) {
+    double qt[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) qt[d] = Q[(((int64_t)sp * D + d) * NV + a) * g.Kp + n];
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < D; ++j) v = fma(g.Jinv[s][j * 3 + i], qt[j], v);
+      Q[(((int64_t)sp * D + i) * NV + a) * g.Kp + n] = v;
+    }
+  }
+}
+
+// F~_u[d][u] = (detJ J^-1 f(u, q))_d  into Xd rows [N_ext + d N_u + u]
+template <int EQ, int D>
+__global__ void __launch_bounds__(256) k_int_flux(GeomDev g, PhysDev ph, const double* __restrict__ Uu,
+                                                  const double* __restrict__ Qu, double* __restrict__ Xd,
+                                                  int nu, int next) {
+  using P = Phys<EQ, D>;
+  constexpr int NV = P::NV;
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int u = blockIdx.y;
+  if (n >= g.K) return;
+  const int s = (int)(n % g.nsub);
+  double uu[NV], qq[D * NV];
+#pragma unroll
+  for (int a = 0; a < NV; ++a) uu[a] = Uu[((int64_t)u * NV + a) * g.Kp + n];
+  if constexpr (P::VISC) {
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int a = 0; a < NV; ++a) qq[d * NV + a] = Qu[(((int64_t)u * D + d) * NV + a) * g.Kp + n];
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    double w[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) w[j] = g.detJ[s] * g.Jinv[s][d * 3 + j];
+    double f[NV];
+    P::conv_dir(ph, uu, w, f);
+    if constexpr (P::VISC) {
+      double fv[NV];
+      P::visc_dir(ph, uu, qq, w, fv);
+#pragma unroll
+      for (int a = 0; a < NV; ++a) f[a] += fv[a];
+    }
+#pragma unroll
+    for (int a = 0; a < NV; ++a) Xd[(((int64_t)next + d * nu + u) * NV + a) * g.Kp + n] = f[a];
+  }
+}
+
+// D~ at external points: common flux with canonical (left, right) order
+template <int EQ, int D>
+__global__ void __launch_bounds__(256) k_face_flux(GeomDev g, PhysDev ph, const ExtMetric* __restrict__ xm,
+                                                   const double* __restrict__ Uext,
+                                                   const double* __restrict__ Qext, double* __restrict__ Xd) {
+  using P = Phys<EQ, D>;
+  constexpr int NV = P::NV;
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.y;
+  if (n >= g.K) return;
+  const int s = (int)(n % g.nsub);
+  const int f = e / g.nfp, q = e % g.nfp;
+  const int64_t m = nbr_elem(g, n, s, f);
+  const int e2 = g.nface[s][f] * g.nfp + g.perm[s][f][q];
+  const bool left = g.left[s][f];
+  double um[NV], uo[NV], qm[D * NV], qo[D * NV];
+#pragma unroll
+  for (int a = 0; a < NV; ++a) {
+    um[a] = Uext[((int64_t)e * NV + a) * g.Kp + n];
+    uo[a] = Uext[((int64_t)e2 * NV + a) * g.Kp + m];
+  }
+  if constexpr (P::VISC) {
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int a = 0; a < NV; ++a) {
+        qm[d * NV + a] = Qext[(((int64_t)e * D + d) * NV + a) * g.Kp + n];
+        qo[d * NV + a] = Qext[(((int64_t)e2 * D + d) * NV + a) * g.Kp + m];
+      }
+  }
+  const ExtMetric mt = xm[s * g.next + e];
+  const double nl[3] = {mt.n0, mt.n1, mt.n2};
+  double F[NV];
+  if (left) P::common_flux(ph, um, uo, qm, qo, nl, F);
+  else P::common_flux(ph, uo, um, qo, qm, nl, F);
+  const double sc = left ? mt.s : -mt.s;
+#pragma unroll
+  for (int a = 0; a < NV; ++a) Xd[((int64_t)e * NV + a) * g.Kp + n] = sc * F[a];
+}
+
+// k = -R~/detJ ; mode 0: out = k ; RK4 stage update otherwise (3-register form):
+//  stage 0: ACC = U + dt/6 k, Us = U + dt/2 k     stage 1: ACC += dt/3 k, Us = U + dt/2 k
+//  stage 2: ACC += dt/3 k, Us = U + dt k           stage 3: U = ACC + dt/6 k
+__global__ void __launch_bounds__(256) k_rk(GeomDev g, const double* __restrict__ R, int rows, int stage,
+                                            double dt, double* __restrict__ out, double* __restrict__ U,
+                                            double* __restrict__ Us, double* __restrict__ ACC) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  if (n >= g.K || r >= rows) return;
+  const int s = (int)(n % g.nsub);
+  const int64_t i = (int64_t)r * g.Kp + n;
+  const double k = -R[i] / g.detJ[s];
+  switch (stage) {
+    case -1: out[i] = k; break;
+    case 0: {
+      const double u = U[i];
+      ACC[i] = fma(dt / 6.0, k, u);
+      Us[i] = fma(0.5 * dt, k, u);
+    } break;
+    case 1: {
+      ACC[i] = fma(dt / 3.0, k, ACC[i]);
+      Us[i] = fma(0.5 * dt, k, U[i]);
+    } break;
+    case 2: {
+      ACC[i] = fma(dt / 3.0, k, ACC[i]);
+      Us[i] = fma(dt, k, U[i]);
+    } break;
+    default: U[i] = fma(dt / 6.0, k, ACC[i]); break;
+  }
+}
+
+// divergence check: first element with a non-finite value (or rho/p <= 0)
+template <int EQ, int D>
+__global__ void k_check(GeomDev g, PhysDev ph, const double* __restrict__ U, int nsol,
+                        unsigned long long* bad) {
+  using P = Phys<EQ, D>;
+  constexpr int NV = P::NV;
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= g.K) return;
+  for (int sp = 0; sp < nsol; ++sp) {
+    double u[NV];
+    bool ok = true;
+    for (int a = 0; a < NV; ++a) {
+      u[a] = U[((int64_t)sp * NV + a) * g.Kp + n];
+      ok = ok && isfinite(u[a]);
+    }
+    if constexpr (NV > 1) {
+      double kin = 0.0;
+      for (int d = 0; d < D; ++d) kin += u[1 + d] * u[1 + d];
+      const double p = (ph.gamma - 1.0) * (u[D + 1] - 0.5 * kin / u[0]);
+      ok = ok && u[0] > 0.0 && p > 0.0;
+    }
+    if (!ok) {
+      atomicMin(bad, (unsigned long long)n);
+      return;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------ host side
+struct OpHost {
+  std::vector<int> ptr, col;
+  std::vector<double> val;
+  int rows, cols, nchunks;
+};
+
+static OpHost pack(const Mat& M) {
+  OpHost o;
+  o.rows = M.rows;
+  o.cols = M.cols;
+  o.nchunks = (M.rows + RB - 1) / RB;
+  o.ptr.push_back(0);
+  for (int ch = 0; ch < o.nchunks; ++ch) {
+    for (int c = 0; c < M.cols; ++c) {
+      bool nz = false;
+      for (int r = ch * RB; r < std::min(M.rows, (ch + 1) * RB); ++r) nz = nz || M(r, c) != 0.0;
+      if (!nz) continue;
+      o.col.push_back(c);
+      for (int r = ch * RB; r < (ch + 1) * RB; ++r) o.val.push_back(r < M.rows ? M(r, c) : 0.0);
+    }
+    o.ptr.push_back((int)o.col.size());
+  }
+  return o;
+}
+
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+struct Plan {
+  size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
+      off_bad, total;
+  size_t ops_bytes;
+};
+
+static void build_ops(const Operators& O, int D, Mat ops[5]) {
+  const RefElement& r = O.ref;
+  int ns = r.nsol;
+  ops[0] = O.M0;
+  ops[1] = O.M12;
+  // gradient G[(s,d)][ [C (next) ; U_u (nu)] ]
+  Mat G(ns * D, r.next + r.nu);
+  for (int s = 0; s < ns; ++s)
+    for (int d = 0; d < D; ++d) {
+      for (int e = 0; e < r.next; ++e) G(s * D + d, e) = O.M16(d * ns + s, e);
+      for (int i = 0; i < r.nint; ++i) {
+        double v = O.M15(d * ns + s, i);
+        if (v != 0.0) G(s * D + d, r.next + r.int_u[i]) += v;
+      }
+    }
+  ops[2] = G;
+  // divergence Dv[s][ [D~ (next) ; F~_u (D nu, [d][u])] ]
+  Mat Dv(ns, r.next + D * r.nu);
+  for (int s = 0; s < ns; ++s) {
+    for (int e = 0; e < r.next; ++e) Dv(s, e) = O.M14(s, e);
+    for (int i = 0; i < r.nint; ++i) {
+      double v = O.M13(s, i);
+      if (v != 0.0) Dv(s, r.next + r.int_dir[i] * r.nu + r.int_u[i]) += v;
+    }
+  }
+  ops[3] = Dv;
+}
+
+}  // namespace sdrt
+
+using namespace sdrt;
+
+enum KTag { T_M0 = 0, T_M12, T_CV, T_GRAD, T_METRIC, T_QEXT, T_QU, T_IFLUX, T_FFLUX, T_DIV, T_RK, T_NTAGS };
+static const char* KTAG_NAMES[T_NTAGS] = {"interp_ext(M0)", "interp_int(M12)", "common_value", "gradient(M16|M15P)",
+                                          "metric_grad", "grad_interp_ext(M5)", "grad_interp_int(M18)",
+                                          "int_flux", "face_flux", "divergence(M14|M13M19P2)", "rk_update"};
+
+struct sdrt_ctx {
+  bool timing = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  GeomDev g;
+  PhysDev ph;
+  int eq, nd, nv, nsol, next, nu, nint;
+  bool visc;
+  double *Uext, *Xg, *Q, *Qext, *Qu, *Xd, *R, *Us, *ACC;
+  ExtMetric* xm;
+  unsigned long long* bad;
+  OpDev op[4];
+  int64_t launches = 0;
+};
+
+static int nvars(int eq, int D) { return (eq == SDRT_EQ_LINADV || eq == SDRT_EQ_LINADVDIFF) ? 1 : D + 2; }
+
+static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph, std::vector<OpHost>* packed) {
+  const RefElement& r = O.ref;
+  int D = m.nd, NV = nvars(ph->eq, D);
+  bool visc = ph->eq == SDRT_EQ_LINADVDIFF || ph->eq == SDRT_EQ_NS;
+  size_t col = (size_t)NV * m.K_pad * sizeof(double);
+  Plan p;
+  size_t o = 0;
+  p.off_uext = o; o += align256(r.next * col);
+  p.off_xg = o; o += align256((r.next + r.nu) * col);
+  p.off_q = o; o += visc ? align256((size_t)r.nsol * D * col) : 0;
+  p.off_qext = o; o += visc ? align256((size_t)r.next * D * col) : 0;
+  p.off_qu = o; o += visc ? align256((size_t)r.nu * D * col) : 0;
+  p.off_xd = o; o += align256((r.next + (size_t)D * r.nu) * col);
+  p.off_r = o; o += align256((size_t)r.nsol * col);
+  p.off_us = o; o += align256((size_t)r.nsol * col);
+  p.off_acc = o; o += align256((size_t)r.nsol * col);
+  Mat ops[5];
+  build_ops(O, D, ops);
+  size_t ob = 0;
+  std::vector<OpHost> pk;
+  for (int i = 0; i < 4; ++i) {
+    pk.push_back(pack(ops[i]));
+    ob += align256(pk.back().ptr.size() * sizeof(int)) + align256(pk.back().col.size() * sizeof(int) + 4) +
+          align256(pk.back().val.size() * sizeof(double) + 8);
+  }
+  p.off_ops = o; o += ob;
+  p.ops_bytes = ob;
+  p.off_xm = o; o += align256((size_t)m.nsub * r.next * sizeof(ExtMetric));
+  p.off_bad = o; o += 256;
+  p.total = o;
+  if (packed) *packed = pk;
+  return p;
+}
+
+extern "C" {
+
+size_t sdrt_ctx_workspace_bytes(const sdrt_mesh* m, const sdrt_operators* o, const sdrt_physics* ph) {
+  if (!m || !o || !ph) return 0;
+  try {
+    return make_plan(m->m, o->o, ph, nullptr).total;
+  } catch (...) {
+    return 0;
+  }
+}
+
+sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const sdrt_physics* ph, void* d_ws,
+                            size_t ws_bytes, void* stream, sdrt_ctx** out) {
+  if (!mm || !oo || !ph || !out || !d_ws) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  const Mesh& m = mm->m;
+  const Operators& O = oo->o;
+  if (m.etype != O.ref.etype || m.p != O.ref.p) {
+    set_error("mesh and operators disagree on element type / degree");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (ph->eq < 0 || ph->eq > 3) {
+    set_error("unknown equation");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (m.nranks != 1) {
+    set_error("multi-rank contexts are created with sdrt_ctx_create on a rank-local mesh; halo exchange "
+              "is not enabled in this build");
+    return SDRT_E_UNSUPPORTED;
+  }
+  SDRT_TRY({
+    std::vector<OpHost> pk;
+    Plan p = make_plan(m, O, ph, &pk);
+    if (ws_bytes < p.total || ((uintptr_t)d_ws % 256)) {
+      set_error("workspace too small or not 256-byte aligned");
+      return SDRT_E_WORKSPACE;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    char* base = (char*)d_ws;
+    auto* c = new sdrt_ctx;
+    const RefElement& r = O.ref;
+    c->eq = ph->eq;
+    c->nd = m.nd;
+    c->nv = nvars(ph->eq, m.nd);
+    c->nsol = r.nsol;
+    c->next = r.next;
+    c->nu = r.nu;
+    c->nint = r.nint;
+    c->visc = ph->eq == SDRT_EQ_LINADVDIFF || ph->eq == SDRT_EQ_NS;
+    c->Uext = (double*)(base + p.off_uext);
+    c->Xg = (double*)(base + p.off_xg);
+    c->Q = (double*)(base + p.off_q);
+    c->Qext = (double*)(base + p.off_qext);
+    c->Qu = (double*)(base + p.off_qu);
+    c->Xd = (double*)(base + p.off_xd);
+    c->R = (double*)(base + p.off_r);
+    c->Us = (double*)(base + p.off_us);
+    c->ACC = (double*)(base + p.off_acc);
+    c->xm = (ExtMetric*)(base + p.off_xm);
+    c->bad = (unsigned long long*)(base + p.off_bad);
+    // operators
+    size_t o = p.off_ops;
+    for (int i = 0; i < 4; ++i) {
+      OpHost& h = pk[i];
+      int* dptr = (int*)(base + o);
+      CUDA_OK(cudaMemcpyAsync(dptr, h.ptr.data(), h.ptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      o += align256(h.ptr.size() * sizeof(int));
+      int* dcol = (int*)(base + o);
+      if (!h.col.empty())
+        CUDA_OK(cudaMemcpyAsync(dcol, h.col.data(), h.col.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      o += align256(h.col.size() * sizeof(int) + 4);
+      double* dval = (double*)(base + o);
+      if (!h.val.empty())
+        CUDA_OK(cudaMemcpyAsync(dval, h.val.data(), h.val.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      o += align256(h.val.size() * sizeof(double) + 8);
+      c->op[i] = OpDev{h.rows, h.cols, h.nchunks, dptr, dcol, dval};
+    }
+    // geometry
+    GeomDev& g = c->g;
+    std::memset(&g, 0, sizeof(g));
+    g.nd = m.nd;
+    g.nsub = m.nsub;
+    g.nfaces = r.nfaces;
+    g.nfp = r.nfp;
+    g.next = r.next;
+    for (int d = 0; d < 3; ++d) {
+      g.Nloc[d] = m.Nloc[d];
+      g.Nglob[d] = m.Nglob[d];
+      g.offset[d] = m.offset[d];
+    }
+    g.K = m.K;
+    g.Kp = m.K_pad;
+    for (int s = 0; s < m.nsub; ++s) {
+      g.detJ[s] = m.detJ[s];
+      for (int k = 0; k < 9; ++k) g.Jinv[s][k] = m.Jinv[s][k];
+      for (int f = 0; f < r.nfaces; ++f) {
+        const FaceLink& L = m.link[s * r.nfaces + f];
+        for (int d = 0; d < 3; ++d) g.off[s][f][d] = (int8_t)L.off[d];
+        g.nshape[s][f] = (int8_t)L.nshape;
+        g.nface[s][f] = (int8_t)L.nface;
+        g.left[s][f] = (int8_t)L.left;
+        for (int q = 0; q < r.nfp; ++q) g.perm[s][f][q] = (int8_t)L.perm[q];
+      }
+    }
+    std::vector<ExtMetric> xm(m.nsub * r.next);
+    for (int i = 0; i < m.nsub * r.next; ++i)
+      xm[i] = ExtMetric{m.sscale[i], m.nleft[i][0], m.nleft[i][1], m.nleft[i][2]};
+    CUDA_OK(cudaMemcpyAsync(c->xm, xm.data(), xm.size() * sizeof(ExtMetric), cudaMemcpyHostToDevice, st));
+    // zero the intermediate buffers (padding columns stay finite)
+    CUDA_OK(cudaMemsetAsync(base, 0, p.off_ops, st));
+    c->ph = PhysDev{{ph->c[0], ph->c[1], ph->c[2]}, ph->mu, ph->gamma, ph->Pr, ph->beta, ph->eta};
+    CUDA_OK(cudaStreamSynchronize(st));  // host vectors go out of scope
+    *out = c;
+    return SDRT_OK;
+  })
+}
+
+void sdrt_ctx_destroy(sdrt_ctx* c) {
+  if (!c) return;
+  for (auto e : c->pool) cudaEventDestroy(e);
+  delete c;
+}
+
+sdrt_status sdrt_ctx_set_timing(sdrt_ctx* c, int enable) {
+  if (!c) {
+    set_error("null ctx");
+    return SDRT_E_INVALID_ARG;
+  }
+  c->timing = enable != 0;
+  c->ev.clear();
+  c->pool_used = 0;
+  return SDRT_OK;
+}
+
+sdrt_status sdrt_ctx_kernel_times(sdrt_ctx* c, int max_tags, char* names, double* ms, int64_t* counts,
+                                  int* ntags) {
+  if (!c || !ms || !counts || !ntags) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    for (auto& e : c->ev) CUDA_OK(cudaEventSynchronize(e.second.second));
+    int n = std::min(max_tags, (int)T_NTAGS);
+    for (int t = 0; t < n; ++t) {
+      ms[t] = 0.0;
+      counts[t] = 0;
+      if (names) {
+        std::strncpy(names + 64 * t, KTAG_NAMES[t], 63);
+        names[64 * t + 63] = 0;
+      }
+    }
+    for (auto& e : c->ev) {
+      float v = 0.f;
+      CUDA_OK(cudaEventElapsedTime(&v, e.second.first, e.second.second));
+      if (e.first < n) {
+        ms[e.first] += v;
+        counts[e.first] += 1;
+      }
+    }
+    *ntags = n;
+    c->ev.clear();
+    c->pool_used = 0;
+    return SDRT_OK;
+  })
+}
+int64_t sdrt_ctx_last_launches(const sdrt_ctx* c) { return c ? c->launches : -1; }
+
+}  // extern "C"
+
+namespace sdrt {
+
+static cudaEvent_t get_event(sdrt_ctx* c) {
+  if (c->pool_used == c->pool.size()) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreate(&e));
+    c->pool.push_back(e);
+  }
+  return c->pool[c->pool_used++];
+}
+
+// RAII marker: records a start/stop event pair around one launch when timing is on
+struct Mark {
+  sdrt_ctx* c;
+  cudaStream_t st;
+  int tag;
+  cudaEvent_t a = nullptr;
+  Mark(sdrt_ctx* c_, cudaStream_t st_, int tag_) : c(c_), st(st_), tag(tag_) {
+    if (c->timing) {
+      a = get_event(c);
+      CUDA_OK(cudaEventRecord(a, st));
+    }
+    c->launches++;
+  }
+  ~Mark() {
+    if (c->timing) {
+      cudaEvent_t b = get_event(c);
+      cudaEventRecord(b, st);
+      c->ev.push_back({tag, {a, b}});
+    }
+  }
+};
+
+static void apply(sdrt_ctx* c, int tag, const OpDev& M, const double* X, double* Y, int64_t W, cudaStream_t st) {
+  dim3 grid((unsigned)((W + 255) / 256), (unsigned)M.nchunks);
+  Mark mk(c, st, tag);
+  k_apply<<<grid, 256, 0, st>>>(M, X, Y, W);
+}
+
+template <int EQ, int D>
+static void residual_impl(sdrt_ctx* c, const double* U, int stage, double dt, double* out, double* Ubase,
+                          cudaStream_t st) {
+  constexpr int NV = Phys<EQ, D>::NV;
+  const GeomDev& g = c->g;
+  const int64_t W = (int64_t)NV * g.Kp;
+  const unsigned gx = (unsigned)((g.K + 255) / 256);
+  apply(c, T_M0, c->op[0], U, c->Uext, W, st);                                  // U_ext = M0 U
+  apply(c, T_M12, c->op[1], U, c->Xg + (size_t)c->next * W, W, st);             // U_u = M12 U
+  if constexpr (Phys<EQ, D>::VISC) {
+    {
+      Mark mk(c, st, T_CV);
+      k_common_value<NV><<<dim3(gx, c->next), 256, 0, st>>>(g, c->ph, c->Uext, c->Xg);
+    }
+    apply(c, T_GRAD, c->op[2], c->Xg, c->Q, W, st);                             // Q~ = G [C; U_u]
+    {
+      Mark mk(c, st, T_METRIC);
+      k_metric_grad<D, NV><<<dim3(gx, c->nsol), 256, 0, st>>>(g, c->Q, c->nsol);
+    }
+    apply(c, T_QEXT, c->op[0], c->Q, c->Qext, (int64_t)D * W, st);              // Q_ext = M5 Q
+    apply(c, T_QU, c->op[1], c->Q, c->Qu, (int64_t)D * W, st);                  // Q_u = M18 Q
+  }
+  {
+    Mark mk(c, st, T_IFLUX);
+    k_int_flux<EQ, D><<<dim3(gx, c->nu), 256, 0, st>>>(g, c->ph, c->Xg + (size_t)c->next * W, c->Qu, c->Xd,
+                                                        c->nu, c->next);
+  }
+  {
+    Mark mk(c, st, T_FFLUX);
+    k_face_flux<EQ, D><<<dim3(gx, c->next), 256, 0, st>>>(g, c->ph, c->xm, c->Uext, c->Qext, c->Xd);
+  }
+  apply(c, T_DIV, c->op[3], c->Xd, c->R, W, st);                                 // R~ = Dv [D~; F~_u]
+  {
+    Mark mk(c, st, T_RK);
+    k_rk<<<dim3(gx, c->nsol * NV), 256, 0, st>>>(g, c->R, c->nsol * NV, stage, dt, out, Ubase, c->Us, c->ACC);
+  }
+}
+
+template <int EQ, int D>
+static bool check_impl(sdrt_ctx* c, const double* U, cudaStream_t st, int64_t* bad_elem) {
+  unsigned long long init = ~0ull, host = 0;
+  CUDA_OK(cudaMemcpyAsync(c->bad, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  k_check<EQ, D><<<(unsigned)((c->g.K + 255) / 256), 256, 0, st>>>(c->g, c->ph, U, c->nsol, c->bad);
+  CUDA_OK(cudaMemcpyAsync(&host, c->bad, sizeof(host), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  *bad_elem = host == ~0ull ? -1 : (int64_t)host;
+  return host == ~0ull;
+}
+
+typedef void (*ResFn)(sdrt_ctx*, const double*, int, double, double*, double*, cudaStream_t);
+typedef bool (*ChkFn)(sdrt_ctx*, const double*, cudaStream_t, int64_t*);
+
+static ResFn pick_res(int eq, int D) {
+#define CASE(E, DD) \
+  if (eq == E && D == DD) return residual_impl<E, DD>;
+  CASE(0, 2) CASE(0, 3) CASE(1, 2) CASE(1, 3) CASE(2, 2) CASE(2, 3) CASE(3, 2) CASE(3, 3)
+#undef CASE
+  return nullptr;
+}
+static ChkFn pick_chk(int eq, int D) {
+#define CASE(E, DD) \
+  if (eq == E && D == DD) return check_impl<E, DD>;
+  CASE(0, 2) CASE(0, 3) CASE(1, 2) CASE(1, 3) CASE(2, 2) CASE(2, 3) CASE(3, 2) CASE(3, 3)
+#undef CASE
+  return nullptr;
+}
+
+}  // namespace sdrt
+
+extern "C" {
+
+sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* stream) {
+  if (!c || !d_U || !d_dUdt) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    pick_res(c->eq, c->nd)(c, d_U, -1, 0.0, d_dUdt, nullptr, st);
+    CUDA_OK(cudaGetLastError());
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream) {
+  if (!c || !d_U || nsteps < 0) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    ResFn res = pick_res(c->eq, c->nd);
+    for (int step = 0; step < nsteps; ++step) {
+      for (int s = 0; s < 4; ++s) res(c, s == 0 ? d_U : c->Us, s, dt, nullptr, d_U, st);
+      CUDA_OK(cudaGetLastError());
+      if (check_every > 0 && (step + 1) % check_every == 0) {
+        int64_t bad;
+        if (!pick_chk(c->eq, c->nd)(c, d_U, st, &bad)) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "diverged: element %lld non-finite or non-physical after step %d",
+                   (long long)bad, step + 1);
+          set_error(buf);
+          return SDRT_E_DIVERGED;
+        }
+      }
+    }
+    return SDRT_OK;
+  })
+}
+
+}  // extern "C"

@@ -1,0 +1,45 @@
+// Uniform periodic pattern meshes (host).  PAPER.md §2 l.145-172, §3 l.497-519.
+#pragma once
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "refel.h"
+
+namespace sdrt {
+
+// Neighbour link of local face f of sub-cell shape s (translation invariant).
+struct FaceLink {
+  int off[3];          // neighbour pattern offset
+  int nshape, nface;   // neighbour sub-cell shape and its local face
+  int left;            // 1 if this side is the LEFT element (reading O14)
+  std::vector<int> perm;  // my face point q -> neighbour face point index
+};
+
+struct Mesh {
+  int etype, p, nd, nsub;
+  int Nloc[3], Nglob[3], offset[3];
+  int rank, nranks, pgrid[3];
+  double lo[3], hi[3], h[3];
+  int64_t K, K_pad;
+  RefElement ref;
+  // per shape
+  std::vector<std::array<double, 9>> J, Jinv;   // row-major D x D (padded to 3x3)
+  std::vector<double> detJ;
+  std::vector<std::array<double, 3>> P0;        // unit-cube position of the image of V0
+  // per (shape, face)
+  std::vector<FaceLink> link;                   // [s * nfaces + f]
+  // per (shape, ext point)
+  std::vector<double> sscale;                   // detJ |J^-T n~|
+  std::vector<std::array<double, 3>> nleft;     // canonical (left element's) unit normal
+
+  int64_t pattern_of(int64_t e) const { return e / nsub; }
+  // global pattern coords of local element e
+  void gcoords(int64_t e, int c[3]) const;
+  int64_t global_id(int64_t e) const;
+};
+
+Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const double hi[3], int rank,
+                int nranks, const int pgrid[3]);
+
+}  // namespace sdrt

@@ -1,0 +1,93 @@
+"""Solver: owns a mesh, operators and a device context over torch-allocated memory.
+
+Plumbing only: torch provides the device workspace, state tensors and streams;
+every step of the residual / RK4 path runs in libsdrt.so's kernels.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import sdrt
+
+
+class Solver:
+    def __init__(self, etype, p, N, lo, hi, eq, device="cuda", rank=0, nranks=1, pgrid=None, **phys):
+        D = 2 if etype in ("quad", "tri") else 3
+        Nl = list(N) if np.ndim(N) else [int(N)] * D
+        self.mesh = sdrt.mesh_create(etype, p, Nl, lo, hi, rank=rank, nranks=nranks, pgrid=pgrid)
+        self.ops = sdrt.operators_build(etype, p)
+        self.info = sdrt.mesh_info(self.mesh)
+        self.phys = sdrt.physics(eq, **phys)
+        self.nv = 1 if eq in ("linadv", "linadvdiff") else D + 2
+        self.device = torch.device(device)
+        nbytes = sdrt.ctx_workspace_bytes(self.mesh, self.ops, self.phys)
+        if nbytes == 0:
+            raise RuntimeError("workspace query failed: " + sdrt.last_error())
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=self.device)
+        base = self.ws.data_ptr()
+        self._ws_ptr = (base + 255) // 256 * 256
+        self._ws_bytes = nbytes
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.ctx = sdrt.ctx_create(self.mesh, self.ops, self.phys, self._ws_ptr, nbytes, stream)
+
+    @property
+    def shape(self):
+        return (self.info["nsol"], self.nv, self.info["K_pad"])
+
+    @property
+    def K(self):
+        return self.info["K"]
+
+    def sol_coords(self):
+        return sdrt.mesh_sol_coords(self.mesh)
+
+    def to_device(self, U_np):
+        """(N_sol, N_V, K) numpy -> padded device tensor (N_sol, N_V, K_pad)."""
+        U = torch.zeros(self.shape, dtype=torch.float64, device=self.device)
+        U[:, :, : self.K] = torch.from_numpy(np.ascontiguousarray(U_np))
+        return U
+
+    def to_host(self, U):
+        return U[:, :, : self.K].cpu().numpy()
+
+    def residual(self, U, out=None):
+        out = torch.empty_like(U) if out is None else out
+        sdrt.residual(self.ctx, U.data_ptr(), out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        return out
+
+    def rk_step(self, U, dt, nsteps=1, check_every=0):
+        sdrt.rk_step(self.ctx, U.data_ptr(), dt, nsteps, check_every,
+                     torch.cuda.current_stream(self.device).cuda_stream)
+        return U
+
+    def set_timing(self, enable):
+        sdrt.ctx_set_timing(self.ctx, enable)
+
+    def kernel_times(self):
+        return sdrt.ctx_kernel_times(self.ctx)
+
+    def last_launches(self):
+        return sdrt.ctx_last_launches(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            sdrt.ctx_destroy(self.ctx)
+            self.ctx = None
+        if getattr(self, "mesh", None):
+            sdrt.mesh_destroy(self.mesh)
+            self.mesh = None
+        if getattr(self, "ops", None):
+            sdrt.operators_destroy(self.ops)
+            self.ops = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def from_config(cfg, device="cuda", N=None):
+    return Solver(cfg.etype, cfg.p, cfg.N if N is None else N, cfg.lo, cfg.hi, cfg.eq, device=device,
+                  **cfg.physics_kwargs())

@@ -1,0 +1,99 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance (north_star, reading O25): per variable alpha,
+    e_alpha = max |U_gpu - U_oracle| / max |U_oracle|  <=  1e-11.
+Inputs are seeded (sdrt_inputs); the oracle and the product receive the same arrays.
+"""
+import numpy as np
+import pytest
+
+from sdrt_inputs import CONFIGS, initial_state, random_state, scaled
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+
+
+def _rel(a, b):
+    """max over variables of max|a-b| / max|b| for arrays (N_sol, N_V, K)."""
+    num = np.abs(a - b).max(axis=(0, 2))
+    den = np.maximum(np.abs(b).max(axis=(0, 2)), 1e-300)
+    return float((num / den).max())
+
+
+def _pair(cfg, N):
+    from oracle.mesh import build_mesh
+    from oracle.physics import Physics
+    from oracle.residual import Residual
+    from paper_2105_08632_b200.solver import Solver
+    D = cfg.nd
+    Nt = tuple(N) if isinstance(N, (tuple, list)) else (N,) * D
+    m = build_mesh(cfg.etype, cfg.p, Nt, cfg.lo, cfg.hi)
+    R = Residual(m, Physics(cfg.eq, D, **cfg.physics_kwargs()))
+    S = Solver(cfg.etype, cfg.p, list(Nt), cfg.lo, cfg.hi, cfg.eq, device="cuda", **cfg.physics_kwargs())
+    return m, R, S
+
+
+RES_CASES = [("c1", 5), ("c1", (3, 7)), ("c2", 5), ("c3", 3), ("c4", (3, 4, 5)), ("c5", 3)]
+
+
+@pytest.mark.parametrize("name,N", RES_CASES)
+@pytest.mark.parametrize("state", ["random", "ic"])
+def test_residual_parity(name, N, state):
+    cfg = CONFIGS[name]
+    m, R, S = _pair(cfg, N)
+    nsol = R.ops.nsol
+    if state == "random":
+        U = random_state(cfg, nsol, m.K, seed=7, amp=0.3)
+    else:
+        U = initial_state(cfg, m.sol_coords())
+    ref = R(U)
+    got = S.to_host(S.residual(S.to_device(U)))
+    torch.cuda.synchronize()
+    assert np.isfinite(got).all()
+    assert _rel(got, ref) <= TOL, _rel(got, ref)
+    assert S.last_launches() > 0
+
+
+RK_CASES = [("c1", 8, 100), ("c2", 6, 40), ("c3", 3, 10), ("c4", 4, 10), ("c5", 3, 4)]
+
+
+@pytest.mark.parametrize("name,N,steps", RK_CASES)
+def test_rk4_parity(name, N, steps):
+    from oracle.residual import integrate
+    cfg = CONFIGS[name]
+    m, R, S = _pair(cfg, N)
+    U0 = initial_state(cfg, m.sol_coords())
+    ref = integrate(R, U0, cfg.dt, steps)
+    Ud = S.to_device(U0)
+    S.rk_step(Ud, cfg.dt, steps, check_every=steps)
+    got = S.to_host(Ud)
+    assert _rel(got, ref) <= TOL, _rel(got, ref)
+
+
+@pytest.mark.parametrize("name,steps", [("c1", 100), ("c4", 1)])
+def test_full_size_parity(name, steps):
+    """BASELINE.json full sizes in the bench launch configuration (c1: the full
+    100-step run; c4: 32^3 hexes p=3, one RK4 step compared element-wise)."""
+    from oracle.residual import integrate
+    cfg = CONFIGS[name]
+    m, R, S = _pair(cfg, cfg.N)
+    U0 = initial_state(cfg, m.sol_coords())
+    ref = integrate(R, U0, cfg.dt, steps)
+    Ud = S.to_device(U0)
+    S.rk_step(Ud, cfg.dt, steps)
+    got = S.to_host(Ud)
+    assert _rel(got, ref) <= TOL, _rel(got, ref)
+
+
+def test_divergence_is_reported():
+    from paper_2105_08632_b200 import sdrt
+    cfg = CONFIGS["c2"]
+    m, R, S = _pair(cfg, 4)
+    U = initial_state(cfg, m.sol_coords())
+    U[:, 0, 5] = -1.0          # negative density in element 5
+    Ud = S.to_device(U)
+    with pytest.raises(sdrt.SdrtError) as e:
+        S.rk_step(Ud, 0.0, 1, check_every=1)
+    assert e.value.code == -7 and "element" in str(e.value)
