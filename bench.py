@@ -228,9 +228,14 @@ def main():
     dof = nsol * nv * K
     stream = torch.cuda.current_stream(dev)
 
+    def finite_now():
+        torch.cuda.synchronize(dev)
+        return bool(torch.isfinite(U[:, :, :K]).all().item())
+
     # ---------------------------------------------------------------- warm-up
     S.rk_step(U, cfg.dt, args.warmup)
     torch.cuda.synchronize(dev)
+    dbg = {"after_warmup": finite_now()}
     clocks = ClockSampler(local)
     time.sleep(0.3)
 
@@ -250,6 +255,7 @@ def main():
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    dbg["after_timed"] = finite_now()
     ktimes = S.kernel_times()
     S.set_timing(False)
     # repeat once more without per-kernel events for a clean clock record window
@@ -341,7 +347,8 @@ def main():
                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                        "d2h_bytes_per_step": state_bytes},
                "gpu_launches": launches, "clocks": clk, "kernel_ms": {k: v[0] for k, v in ktimes.items()},
-               "ms_per_step_no_events": ms_clean_max / args.steps, "state_finite": finite}
+               "ms_per_step_no_events": ms_clean_max / args.steps, "state_finite": finite,
+               "finite_trace": dbg}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
