@@ -67,8 +67,10 @@ def dims(cfg):
 
 
 def kernel_bytes(cfg, K):
-    """Algorithmic bytes per launch of each kernel of the v1 path (each input array
-    read once, each output written once; fp64)."""
+    """Algorithmic bytes per launch of each kernel (each input array read once, each
+    output written once; fp64).  tensor_stage(B): stage input + RK registers (3 N_sol
+    rows on average over the 4 stages) + neighbour U traces + viscous traces + new
+    traces; tensor_grad(A): stage input + U traces + published viscous traces."""
     D, ns, ne, nu = dims(cfg)
     V = cfg.nvars
     b = 8 * V * K
@@ -84,6 +86,10 @@ def kernel_bytes(cfg, K):
         "face_flux": b * (2 * ne + (2 * D * ne if cfg.eq in ("ns", "linadvdiff") else 0) + ne),
         "divergence(M14|M13M19P2)": b * (ne + D * nu + ns),
         "rk_update": b * ns * 4.25,
+        # fused tensor path (each array read/written once per launch)
+        "tensor_traces": b * (ns + ne),
+        "tensor_grad(A)": b * (ns + ne + (ne // 2 if abs(cfg.beta) == 0.5 else ne)),
+        "tensor_stage(B)": b * (ns + 3 * ns + ne + (ne if cfg.eq in ("ns", "linadvdiff") else 0) + ne),
     }
 
 
@@ -311,10 +317,11 @@ def main():
     tf = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(dom)
-    achieved = kb[dom] / (dom_ms / dom_n * 1e-3) / 1e9 if dom else None
+    achieved = kb[dom] / (dom_ms / dom_n * 1e-3) / 1e9 if dom in kb else None
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm if achieved else None, "traffic": traffic,
             "bytes_per_launch": kb.get(dom), "avg_launch_ms": dom_ms / dom_n if dom else None,
+            "launches_per_step": dom_n / args.steps if dom else None,
             "peak_source": peak_note,
             "step_share": dom_ms / ms if dom else None}
     model_b = stage_model_bytes(cfg)

@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -23,6 +24,7 @@
 
 #include "capi_internal.h"
 #include "ctx.h"
+#include "tensor.cuh"
 
 namespace sdrt {
 
@@ -293,7 +295,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, total;
+      off_bad, off_tu0, off_tu1, off_tg, total;
   size_t ops_bytes;
 };
 
@@ -329,10 +331,12 @@ static void build_ops(const Operators& O, int D, Mat ops[5]) {
 
 using namespace sdrt;
 
-enum KTag { T_M0 = 0, T_M12, T_CV, T_GRAD, T_METRIC, T_QEXT, T_QU, T_IFLUX, T_FFLUX, T_DIV, T_RK, T_NTAGS };
+enum KTag { T_M0 = 0, T_M12, T_CV, T_GRAD, T_METRIC, T_QEXT, T_QU, T_IFLUX, T_FFLUX, T_DIV, T_RK,
+            T_TRACE, T_FA, T_FB, T_NTAGS };
 static const char* KTAG_NAMES[T_NTAGS] = {"interp_ext(M0)", "interp_int(M12)", "common_value", "gradient(M16|M15P)",
                                           "metric_grad", "grad_interp_ext(M5)", "grad_interp_int(M18)",
-                                          "int_flux", "face_flux", "divergence(M14|M13M19P2)", "rk_update"};
+                                          "int_flux", "face_flux", "divergence(M14|M13M19P2)", "rk_update",
+                                          "tensor_traces", "tensor_grad(A)", "tensor_stage(B)"};
 
 struct sdrt_ctx {
   bool timing = false;
@@ -348,6 +352,14 @@ struct sdrt_ctx {
   unsigned long long* bad;
   OpDev op[4];
   int64_t launches = 0;
+  // fused tensor-product path
+  bool fused = false;
+  int etype = 0, p = 0;
+  TensorGeom tg;
+  Line1D line;
+  double* Tu[2] = {nullptr, nullptr};
+  double* Tg = nullptr;
+  int cur = 0;
 };
 
 static int nvars(int eq, int D) { return (eq == SDRT_EQ_LINADV || eq == SDRT_EQ_LINADVDIFF) ? 1 : D + 2; }
@@ -381,6 +393,10 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.ops_bytes = ob;
   p.off_xm = o; o += align256((size_t)m.nsub * r.next * sizeof(ExtMetric));
   p.off_bad = o; o += 256;
+  size_t tb = etype_tensor(m.etype) ? align256((size_t)r.next * col) : 0;
+  p.off_tu0 = o; o += tb;
+  p.off_tu1 = o; o += tb;
+  p.off_tg = o; o += tb;
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -499,6 +515,40 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     // zero the intermediate buffers (padding columns stay finite)
     CUDA_OK(cudaMemsetAsync(base, 0, p.off_ops, st));
     c->ph = PhysDev{{ph->c[0], ph->c[1], ph->c[2]}, ph->mu, ph->gamma, ph->Pr, ph->beta, ph->eta};
+    // fused tensor-product path (default for quad/hex; SDRT_FORCE_GENERIC=1 selects the
+    // generic operator path, a test hook for cross-checking the two)
+    c->etype = m.etype;
+    c->p = m.p;
+    const char* fg = getenv("SDRT_FORCE_GENERIC");
+    c->fused = etype_tensor(m.etype) && !(fg && fg[0] == '1') && tensor_supported(m.nd, m.p, ph->eq);
+    if (c->fused) {
+      TensorGeom& t = c->tg;
+      for (int d = 0; d < 3; ++d) t.N[d] = m.Nloc[d];
+      t.K = m.K;
+      t.Kp = m.K_pad;
+      t.detJ = m.detJ[0];
+      for (int d = 0; d < 3; ++d) {
+        t.jinv[d] = d < m.nd ? m.Jinv[0][d * 3 + d] : 0.0;
+        t.sface[d] = d < m.nd ? m.detJ[0] * t.jinv[d] : 0.0;
+      }
+      for (int f = 0; f < r.nfaces; ++f)
+        for (int q = 0; q < r.nfp; ++q)
+          if (m.link[f].perm[q] != q) throw std::runtime_error("internal: tensor face permutation not identity");
+      Line1D& L = c->line;
+      std::memset(&L, 0, sizeof(L));
+      int n = m.p + 1;
+      for (int i = 0; i < n; ++i) {
+        L.Iend[0][i] = O.M0(0 * r.nfp + 0, i);
+        L.Iend[1][i] = O.M0(1 * r.nfp + 0, i);
+        for (int a = 0; a < m.p; ++a) L.Iint[a][i] = O.M12(a, i);
+        L.Dfl[i][0] = -O.M14(i, 0 * r.nfp + 0);
+        L.Dfl[i][m.p + 1] = O.M14(i, 1 * r.nfp + 0);
+        for (int a = 0; a < m.p; ++a) L.Dfl[i][a + 1] = O.M13(i, a);
+      }
+      c->Tu[0] = (double*)(base + p.off_tu0);
+      c->Tu[1] = (double*)(base + p.off_tu1);
+      c->Tg = (double*)(base + p.off_tg);
+    }
     CUDA_OK(cudaStreamSynchronize(st));  // host vectors go out of scope
     *out = c;
     return SDRT_OK;
@@ -645,6 +695,33 @@ static bool check_impl(sdrt_ctx* c, const double* U, cudaStream_t st, int64_t* b
   return host == ~0ull;
 }
 
+static void fused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
+  Mark mk(c, st, T_TRACE);
+  tensor_launch_traces(c->nd, c->p, c->eq, c->tg, c->line, U, c->Tu[c->cur], st);
+}
+
+static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, double dt, double* out,
+                        cudaStream_t st) {
+  TensorBufs b;
+  b.Uin = Uin;
+  b.U = U;
+  b.Us = c->Us;
+  b.ACC = c->ACC;
+  b.out = out;
+  b.Tu = c->Tu[c->cur];
+  b.Tu_next = c->Tu[c->cur ^ 1];
+  b.Tg = c->Tg;
+  if (c->visc) {
+    Mark mk(c, st, T_FA);
+    tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, st);
+  }
+  {
+    Mark mk(c, st, T_FB);
+    tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, stage, dt, st);
+  }
+  if (stage >= 0) c->cur ^= 1;
+}
+
 typedef void (*ResFn)(sdrt_ctx*, const double*, int, double, double*, double*, cudaStream_t);
 typedef bool (*ChkFn)(sdrt_ctx*, const double*, cudaStream_t, int64_t*);
 
@@ -675,7 +752,12 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
-    pick_res(c->eq, c->nd)(c, d_U, -1, 0.0, d_dUdt, nullptr, st);
+    if (c->fused) {
+      fused_traces(c, d_U, st);
+      fused_stage(c, d_U, nullptr, -1, 0.0, d_dUdt, st);
+    } else {
+      pick_res(c->eq, c->nd)(c, d_U, -1, 0.0, d_dUdt, nullptr, st);
+    }
     CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })
@@ -690,8 +772,12 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
     ResFn res = pick_res(c->eq, c->nd);
+    if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
     for (int step = 0; step < nsteps; ++step) {
-      for (int s = 0; s < 4; ++s) res(c, s == 0 ? d_U : c->Us, s, dt, nullptr, d_U, st);
+      for (int s = 0; s < 4; ++s) {
+        if (c->fused) fused_stage(c, s == 0 ? d_U : c->Us, d_U, s, dt, nullptr, st);
+        else res(c, s == 0 ? d_U : c->Us, s, dt, nullptr, d_U, st);
+      }
       CUDA_OK(cudaGetLastError());
       if (check_every > 0 && (step + 1) % check_every == 0) {
         int64_t bad;

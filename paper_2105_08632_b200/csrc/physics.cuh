@@ -113,6 +113,37 @@ struct Phys {
     }
   }
 
+  // convective common flux (upwind LF for linear, Rusanov otherwise) along n
+  static __device__ __forceinline__ void conv_common(const PhysDev& ph, const double* uL, const double* uR,
+                                                     const double* n, double* F) {
+    if constexpr (NV == 1) {
+      double cn = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) cn += ph.c[d] * n[d];
+      F[0] = 0.5 * cn * (uL[0] + uR[0]) + 0.5 * fabs(cn) * (uL[0] - uR[0]);
+    } else {
+      double fL[NV], fR[NV];
+      conv_dir(ph, uL, n, fL);
+      conv_dir(ph, uR, n, fR);
+      const double irL = 1.0 / uL[0], irR = 1.0 / uR[0];
+      double vnL = 0.0, vnR = 0.0, vvL = 0.0, vvR = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        vnL += uL[1 + d] * n[d];
+        vnR += uR[1 + d] * n[d];
+        vvL += uL[1 + d] * uL[1 + d];
+        vvR += uR[1 + d] * uR[1 + d];
+      }
+      vnL *= irL;
+      vnR *= irR;
+      const double pL = (ph.gamma - 1.0) * (uL[D + 1] - 0.5 * vvL * irL);
+      const double pR = (ph.gamma - 1.0) * (uR[D + 1] - 0.5 * vvR * irR);
+      const double phi = fmax(fabs(vnL) + sqrt(ph.gamma * pL * irL), fabs(vnR) + sqrt(ph.gamma * pR * irR));
+#pragma unroll
+      for (int a = 0; a < NV; ++a) F[a] = 0.5 * (fL[a] + fR[a]) + 0.5 * phi * (uL[a] - uR[a]);
+    }
+  }
+
   // common normal flux along nL (left element's unit normal)
   static __device__ __forceinline__ void common_flux(const PhysDev& ph, const double* uL, const double* uR,
                                                      const double* qL, const double* qR, const double* n,

@@ -1,0 +1,495 @@
+// Fused SDRT stage for tensor-product elements (quad / hex) on sm_100a, fp64.
+//
+// The App. B operators of tensor elements factor into 1D line operators along the
+// GL-aligned flux lines (App. A l.2618-2625; B7 structural sparsity
+// l.2927-2932: one normal component per unique internal point), so a stage is
+// evaluated line by line with the whole element tile resident in shared memory:
+//
+//   kernel A (viscous only): U, neighbour U traces -> common value C (l.282-291) ->
+//     gradient Q~ = M16 C + M15 U_int along lines (l.295-298), Q = J^-T Q~ (l.299-302)
+//     -> viscous normal flux g = n_L . f^v(u, q) at face points, published as a trace
+//     (the common viscous flux (1/2+b) g_L + (1/2-b) g_R + eta (u_L - u_R), l.330-335,
+//     needs only these N_V numbers per face point, not the D N_V gradient)
+//   kernel B: U, traces -> [gradient again] -> per line: internal transformed flux
+//     (l.305-311, one component per point), common flux at both ends (Rusanov l.324-328
+//     + LDG), divergence R~ = M14 D~ + M13 F~ (l.2919-2925) accumulated per direction
+//     -> dU/dt = -R~/detJ (l.347-350) -> RK4 register update -> traces of the new state.
+//
+// Tile: E consecutive elements per CTA, shared memory [point][var][E] (element
+// fastest, matching the ABI layout so global loads/stores are row segments of E
+// doubles).  Face values are exchanged only through traces [N_ext][N_V][K_pad]
+// written by the previous stage (double-buffered), so each face point's common flux
+// is evaluated by both neighbours from bit-identical inputs (explicit fma chains for
+// the trace interpolation, published g read back by both sides) and D~_R = -D~_L
+// bitwise (O28).
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "tensor.cuh"
+
+namespace sdrt {
+
+template <int D, int P>
+struct TDims {
+  static constexpr int n = P + 1;
+  static constexpr int NL = D == 2 ? n : n * n;  // lines per direction (= points per face)
+  static constexpr int NS = D == 2 ? n * n : n * n * n;
+  static constexpr int NEXT = 2 * D * NL;
+};
+
+template <int D, int P>
+__device__ __forceinline__ int sidx(int d, int t, int i) {
+  constexpr int n = P + 1;
+  if constexpr (D == 2) {
+    return d == 0 ? i + n * t : t + n * i;
+  } else {
+    const int ta = t % n, tb = t / n;
+    return d == 0 ? i + n * (ta + n * tb) : (d == 1 ? ta + n * (i + n * tb) : ta + n * (tb + n * i));
+  }
+}
+
+// neighbour element along axis d (delta = -1 / +1), periodic pattern grid, N_p = 1
+template <int D>
+__device__ __forceinline__ int64_t tnbr(const TensorGeom& g, int64_t e, int d, int delta) {
+  int c[3];
+  int64_t r = e;
+  c[0] = (int)(r % g.N[0]);
+  r /= g.N[0];
+  c[1] = (int)(r % g.N[1]);
+  r /= g.N[1];
+  c[2] = (int)r;
+  int v = c[d] + delta;
+  v = v < 0 ? v + g.N[d] : (v >= g.N[d] ? v - g.N[d] : v);
+  c[d] = v;
+  return (int64_t)c[0] + (int64_t)g.N[0] * (c[1] + (int64_t)g.N[1] * c[2]);
+}
+
+// value at a line end: explicit fma chain in fixed order (bit-identical wherever used)
+template <int n>
+__device__ __forceinline__ double interp_end(const double (&Iend)[TMAXP + 1], const double* u) {
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < n; ++i) acc = __fma_rn(Iend[i], u[i], acc);
+  return acc;
+}
+
+template <int D, int P, int NV, int E>
+__device__ __forceinline__ void load_tile(const double* __restrict__ src, double* sU, int64_t e0, int64_t K,
+                                          int64_t Kp) {
+  constexpr int NS = TDims<D, P>::NS;
+  for (int idx = threadIdx.x; idx < NS * NV * E; idx += blockDim.x) {
+    const int el = idx % E, row = idx / E;
+    const int64_t e = e0 + el;
+    sU[idx] = e < K ? src[(int64_t)row * Kp + e] : 0.0;
+  }
+}
+
+// gradient along lines -> sQ[d][s][v][E] = (2/h_d) (M16 C + M15 U_int)   (l.295-302)
+template <int D, int P, int EQ, int E>
+__device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                                               const double* __restrict__ Tu, const double* sU, double* sQ,
+                                               int64_t e0) {
+  using T = TDims<D, P>;
+  constexpr int n = T::n, NL = T::NL, NS = T::NS;
+  constexpr int NV = Phys<EQ, D>::NV;
+  const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
+  for (int item = threadIdx.x; item < D * NL * E; item += blockDim.x) {
+    const int el = item % E, line = item / E, d = line / NL, t = line % NL;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int64_t mlo = tnbr<D>(g, e, d, -1), mhi = tnbr<D>(g, e, d, +1);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double u[n];
+#pragma unroll
+      for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+      // common values at both ends (own trace recomputed bit-identically, neighbour read)
+      const double own0 = interp_end<n>(L.Iend[0], u), own1 = interp_end<n>(L.Iend[1], u);
+      const double nb0 = Tu[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kp + mlo];
+      const double nb1 = Tu[((int64_t)((2 * d + 0) * NL + t) * NV + v) * g.Kp + mhi];
+      const double c0 = wl * nb0 + wr * own0;   // face x_d = -1: this element is RIGHT
+      const double c1 = wl * own1 + wr * nb1;   // face x_d = +1: this element is LEFT
+      double ui[P];
+#pragma unroll
+      for (int a = 0; a < P; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i], s);
+        ui[a] = s;
+      }
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        double q = L.Dfl[i][0] * c0;
+#pragma unroll
+        for (int a = 0; a < P; ++a) q = fma(L.Dfl[i][a + 1], ui[a], q);
+        q = fma(L.Dfl[i][P + 1], c1, q);
+        sQ[((d * NS + sidx<D, P>(d, t, i)) * NV + v) * E + el] = g.jinv[d] * q;
+      }
+    }
+  }
+}
+
+// traces of a state held in shared memory -> T[N_ext][N_V][Kp]
+template <int D, int P, int NV, int E>
+__device__ __forceinline__ void write_traces(const TensorGeom& g, const Line1D& L, const double* sU,
+                                             double* __restrict__ T, int64_t e0) {
+  using Tm = TDims<D, P>;
+  constexpr int n = Tm::n, NL = Tm::NL, NEXT = Tm::NEXT;
+  for (int item = threadIdx.x; item < NEXT * NV * E; item += blockDim.x) {
+    const int el = item % E, r = item / E, v = r % NV, ext = r / NV;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int face = ext / NL, t = ext % NL, d = face / 2, side = face % 2;
+    double u[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+    T[((int64_t)ext * NV + v) * g.Kp + e] = interp_end<n>(L.Iend[side], u);
+  }
+}
+
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const double* __restrict__ U,
+                                                 double* __restrict__ T) {
+  constexpr int NV = Phys<EQ, D>::NV;
+  extern __shared__ double smem[];
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  load_tile<D, P, NV, E>(U, smem, e0, g.K, g.Kp);
+  __syncthreads();
+  write_traces<D, P, NV, E>(g, L, smem, T, e0);
+}
+
+// kernel A: gradient + published viscous normal-flux traces
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
+  extern __shared__ double smem[];
+  double* sU = smem;
+  double* sQ = smem + NS * NV * E;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  load_tile<D, P, NV, E>(b.Uin, sU, e0, g.K, g.Kp);
+  __syncthreads();
+  gradient_lines<D, P, EQ, E>(g, L, ph, b.Tu, sU, sQ, e0);
+  __syncthreads();
+  // publish g at face points of the sides that carry weight: side 1 (left) if
+  // 1/2 + beta != 0, side 0 (right) if 1/2 - beta != 0
+  const bool pub1 = (0.5 + ph.beta) != 0.0, pub0 = (0.5 - ph.beta) != 0.0;
+  for (int item = threadIdx.x; item < 2 * D * NL * E; item += blockDim.x) {
+    const int el = item % E, ext = item / E;
+    const int face = ext / NL, t = ext % NL, d = face / 2, side = face % 2;
+    if ((side == 1 && !pub1) || (side == 0 && !pub0)) continue;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    double u[NV], q[D * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double ul[n];
+#pragma unroll
+      for (int i = 0; i < n; ++i) ul[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+      u[v] = interp_end<n>(L.Iend[side], ul);
+#pragma unroll
+      for (int dd = 0; dd < D; ++dd) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) s = fma(L.Iend[side][i], sQ[((dd * NS + sidx<D, P>(d, t, i)) * NV + v) * E + el], s);
+        q[dd * NV + v] = s;
+      }
+    }
+    double nL[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;  // canonical (left) normal +e_d
+    double gv[NV];
+    Ph::visc_dir(ph, u, q, nL, gv);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)ext * NV + v) * g.Kp + e] = gv[v];
+  }
+}
+
+// kernel B: fluxes, divergence, RK update, new traces
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
+                                                double dt) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
+  extern __shared__ double smem[];
+  double* sU = smem;
+  double* sR = smem + NS * NV * E;
+  double* sQ = sR + NS * NV * E;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  load_tile<D, P, NV, E>(b.Uin, sU, e0, g.K, g.Kp);
+  __syncthreads();
+  if constexpr (Ph::VISC) {
+    gradient_lines<D, P, EQ, E>(g, L, ph, b.Tu, sU, sQ, e0);
+    __syncthreads();
+  }
+  const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+  for (int d = 0; d < D; ++d) {
+    const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
+    for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
+      const int el = item % E, t = item / E;
+      const int64_t e = e0 + el;
+      if (e >= g.K) continue;
+      double u[n][NV];
+#pragma unroll
+      for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) u[i][v] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+      double q[Ph::VISC ? n : 1][Ph::VISC ? D * NV : 1];
+      if constexpr (Ph::VISC) {
+#pragma unroll
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+          for (int dd = 0; dd < D; ++dd)
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+              q[i][dd * NV + v] = sQ[((dd * NS + sidx<D, P>(d, t, i)) * NV + v) * E + el];
+      }
+      double r[n][NV];
+#pragma unroll
+      for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) r[i][v] = d == 0 ? 0.0 : sR[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+      // internal flux points along the line (normal e_d): F~ = detJ (J^-1 f)_d
+#pragma unroll
+      for (int a = 0; a < P; ++a) {
+        double ua[NV], qa[Ph::VISC ? D * NV : 1], w[D], f[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i][v], s);
+          ua[v] = s;
+        }
+        if constexpr (Ph::VISC) {
+#pragma unroll
+          for (int k = 0; k < D * NV; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], q[i][k], s);
+            qa[k] = s;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
+        Ph::conv_dir(ph, ua, w, f);
+        if constexpr (Ph::VISC) {
+          double fv[NV];
+          Ph::visc_dir(ph, ua, qa, w, fv);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) f[v] += fv[v];
+        }
+#pragma unroll
+        for (int i = 0; i < n; ++i)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) r[i][v] = fma(L.Dfl[i][a + 1], f[v], r[i][v]);
+      }
+      // both ends: common flux with canonical (left, right) = (x_d-side element, x_d+side)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int64_t m = tnbr<D>(g, e, d, side ? 1 : -1);
+        const int ext_own = (2 * d + side) * NL + t, ext_nbr = (2 * d + 1 - side) * NL + t;
+        double uo[NV], un[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double ul[n];
+#pragma unroll
+          for (int i = 0; i < n; ++i) ul[i] = u[i][v];
+          uo[v] = interp_end<n>(L.Iend[side], ul);
+          un[v] = b.Tu[((int64_t)ext_nbr * NV + v) * g.Kp + m];
+        }
+        const double* uL = side ? uo : un;
+        const double* uR = side ? un : uo;
+        double nL[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
+        double F[NV];
+        Ph::conv_common(ph, uL, uR, nL, F);
+        if constexpr (Ph::VISC) {
+          const int64_t eL = side ? e : m, eR = side ? m : e;
+          const int xL = (2 * d + 1) * NL + t, xR = (2 * d) * NL + t;
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            double fv = 0.0;
+            if (wl != 0.0) fv = wl * b.Tg[((int64_t)xL * NV + v) * g.Kp + eL];
+            if (wr != 0.0) fv = fma(wr, b.Tg[((int64_t)xR * NV + v) * g.Kp + eR], fv);
+            F[v] += fv + ph.eta * (uL[v] - uR[v]);
+          }
+        }
+        (void)ext_own;
+        const double sD = side ? g.sface[d] : -g.sface[d];
+        // M14 column of this end: -L_0' (x_d = -1), +L_{p+1}' (x_d = +1)
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double m14 = side ? L.Dfl[i][P + 1] : -L.Dfl[i][0];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) r[i][v] = fma(m14, sD * F[v], r[i][v]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sR[(sidx<D, P>(d, t, i) * NV + v) * E + el] = r[i][v];
+    }
+    __syncthreads();
+  }
+  // dU/dt = -R~/detJ, RK4 (3-register form), new state into sU
+  const double idet = 1.0 / g.detJ;
+  for (int idx = threadIdx.x; idx < NS * NV * E; idx += blockDim.x) {
+    const int el = idx % E, row = idx / E;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int64_t gi = (int64_t)row * g.Kp + e;
+    const double k = -sR[idx] * idet;
+    double nu;
+    switch (stage) {
+      case -1:
+        b.out[gi] = k;
+        nu = 0.0;
+        break;
+      case 0: {
+        const double u0 = sU[idx];
+        b.ACC[gi] = fma(dt / 6.0, k, u0);
+        nu = fma(0.5 * dt, k, u0);
+        b.Us[gi] = nu;
+      } break;
+      case 1:
+        b.ACC[gi] = fma(dt / 3.0, k, b.ACC[gi]);
+        nu = fma(0.5 * dt, k, b.U[gi]);
+        b.Us[gi] = nu;
+        break;
+      case 2:
+        b.ACC[gi] = fma(dt / 3.0, k, b.ACC[gi]);
+        nu = fma(dt, k, b.U[gi]);
+        b.Us[gi] = nu;
+        break;
+      default:
+        nu = fma(dt / 6.0, k, b.ACC[gi]);
+        b.U[gi] = nu;
+        break;
+    }
+    sU[idx] = nu;
+  }
+  if (stage < 0) return;
+  __syncthreads();
+  write_traces<D, P, NV, E>(g, L, sU, b.Tu_next, e0);
+}
+
+// ------------------------------------------------------------------ launchers
+template <int D, int P, int EQ>
+struct TCfg {
+  static constexpr int NV = Phys<EQ, D>::NV;
+  static constexpr int E = NV > 1 ? 8 : (D == 3 ? 16 : 32);
+  static constexpr int NL = TDims<D, P>::NL;
+  static constexpr int THREADS = ((NL * E + 31) / 32) * 32 > 256 ? 256 : ((NL * E + 31) / 32) * 32;
+  static constexpr size_t TILE = (size_t)TDims<D, P>::NS * NV * E * sizeof(double);
+  static constexpr size_t SMEM_A = TILE * (1 + D);
+  static constexpr size_t SMEM_B = TILE * (2 + (Phys<EQ, D>::VISC ? D : 0));
+  static constexpr size_t SMEM_T = TILE;
+};
+
+template <int D, int P, int EQ>
+static void set_smem(const void* k, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA smem attr: ") + cudaGetErrorString(e));
+  }
+}
+
+template <int D, int P, int EQ>
+static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const TensorBufs& b, int stage,
+                      double dt, cudaStream_t st, int which) {
+  using C = TCfg<D, P, EQ>;
+  const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
+  if (which == 0) {
+    if constexpr (Phys<EQ, D>::VISC) {
+      auto ka = kt_grad<D, P, EQ, C::E>;
+      set_smem<D, P, EQ>((const void*)ka, C::SMEM_A);
+      ka<<<grid, C::THREADS, C::SMEM_A, st>>>(g, L, ph, b);
+    }
+  } else {
+    auto kb = kt_stage<D, P, EQ, C::E>;
+    set_smem<D, P, EQ>((const void*)kb, C::SMEM_B);
+    kb<<<grid, C::THREADS, C::SMEM_B, st>>>(g, L, ph, b, stage, dt);
+  }
+}
+
+template <int D, int P, int EQ>
+static void run_traces(const TensorGeom& g, const Line1D& L, const double* U, double* Tu, cudaStream_t st) {
+  using C = TCfg<D, P, EQ>;
+  const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
+  auto k = kt_traces<D, P, EQ, C::E>;
+  set_smem<D, P, EQ>((const void*)k, C::SMEM_T);
+  k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, L, U, Tu);
+}
+
+typedef void (*StageFn)(const TensorGeom&, const Line1D&, const PhysDev&, const TensorBufs&, int, double,
+                        cudaStream_t, int);
+typedef void (*TraceFn)(const TensorGeom&, const Line1D&, const double*, double*, cudaStream_t);
+
+template <int D, int P>
+static void pick(int eq, StageFn* s, TraceFn* t) {
+  switch (eq) {
+    case EQ_LINADV: *s = run_stage<D, P, EQ_LINADV>; *t = run_traces<D, P, EQ_LINADV>; break;
+    case EQ_LINADVDIFF: *s = run_stage<D, P, EQ_LINADVDIFF>; *t = run_traces<D, P, EQ_LINADVDIFF>; break;
+    case EQ_EULER: *s = run_stage<D, P, EQ_EULER>; *t = run_traces<D, P, EQ_EULER>; break;
+    default: *s = run_stage<D, P, EQ_NS>; *t = run_traces<D, P, EQ_NS>; break;
+  }
+}
+
+static void pick_all(int D, int P, int eq, StageFn* s, TraceFn* t) {
+  *s = nullptr;
+  *t = nullptr;
+  if (D == 2) {
+    switch (P) {
+      case 1: pick<2, 1>(eq, s, t); break;
+      case 2: pick<2, 2>(eq, s, t); break;
+      case 3: pick<2, 3>(eq, s, t); break;
+      case 4: pick<2, 4>(eq, s, t); break;
+    }
+  } else {
+    switch (P) {
+      case 1: pick<3, 1>(eq, s, t); break;
+      case 2: pick<3, 2>(eq, s, t); break;
+      case 3: pick<3, 3>(eq, s, t); break;
+      case 4: pick<3, 4>(eq, s, t); break;
+    }
+  }
+}
+
+bool tensor_supported(int D, int P, int eq) {
+  StageFn s;
+  TraceFn t;
+  if (eq < 0 || eq > 3) return false;
+  pick_all(D, P, eq, &s, &t);
+  return s != nullptr;
+}
+
+void tensor_launch_grad(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                        const TensorBufs& b, cudaStream_t st) {
+  StageFn s;
+  TraceFn t;
+  pick_all(D, P, eq, &s, &t);
+  s(g, L, ph, b, 0, 0.0, st, 0);
+}
+
+void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                        const TensorBufs& b, int stage, double dt, cudaStream_t st) {
+  StageFn s;
+  TraceFn t;
+  pick_all(D, P, eq, &s, &t);
+  s(g, L, ph, b, stage, dt, st, 1);
+}
+
+void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const double* U,
+                          double* Tu, cudaStream_t st) {
+  StageFn s;
+  TraceFn t;
+  pick_all(D, P, eq, &s, &t);
+  t(g, L, U, Tu, st);
+}
+
+}  // namespace sdrt

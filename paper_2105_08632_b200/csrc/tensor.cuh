@@ -1,0 +1,56 @@
+// Fused sum-factorised SDRT stage for tensor-product elements (quad/hex), sm_100a.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "physics.cuh"
+
+namespace sdrt {
+
+constexpr int TMAXP = 4;  // max degree of the fused tensor path
+
+// 1D line operators, extracted on the host from the App. B matrices (so the fused
+// path applies exactly the operators the generic path does):
+//   Iend[s][i] = ell_i(-1 / +1)              (M0 restricted to one line)
+//   Iint[a][i] = ell_i(zeta_a)               (M12 restricted to one line)
+//   Dfl[i][f]  = L_f'(g_i), f over the flux line {-1, zeta_1..zeta_p, +1}
+//                (M13 columns are Dfl[.][1..p]; M14 = -Dfl[.][0] (x=-1), +Dfl[.][p+1] (x=+1);
+//                 M16 = n . M14 = Dfl[.][0] / Dfl[.][p+1] for both ends)
+struct Line1D {
+  double Iend[2][TMAXP + 1];
+  double Iint[TMAXP][TMAXP + 1];
+  double Dfl[TMAXP + 1][TMAXP + 2];
+};
+
+struct TensorGeom {
+  int N[3];           // patterns per axis (periodic)
+  int64_t K, Kp;
+  double jinv[3];     // 2 / h_d  (J^-T = diag)
+  double detJ;        // prod h_d / 2
+  double sface[3];    // detJ * 2 / h_d  (= detJ |J^-T n~| on faces normal to d)
+};
+
+struct TensorBufs {
+  const double* Uin;  // stage input (U or Us)
+  double* U;          // u_n register (ABI state)
+  double* Us;         // stage register
+  double* ACC;        // RK accumulator
+  double* out;        // residual output (stage == -1)
+  const double* Tu;   // traces of the stage input  [N_ext][N_V][Kp]
+  double* Tu_next;    // traces of the stage output
+  double* Tg;         // published viscous normal-flux traces [N_ext][N_V][Kp]
+};
+
+// Launchers (tensor.cu).  stage: -1 residual, 0..3 RK4 stages.
+void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const double* U,
+                          double* Tu, cudaStream_t st);
+// kernel A (viscous equations only): gradient + published viscous normal-flux traces
+void tensor_launch_grad(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                        const TensorBufs& b, cudaStream_t st);
+// kernel B: fluxes, divergence, RK update, new traces
+void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                        const TensorBufs& b, int stage, double dt, cudaStream_t st);
+bool tensor_supported(int D, int P, int eq);
+
+}  // namespace sdrt
