@@ -70,12 +70,17 @@ CONFIGS = {
     "c3": Config("c3", "hex", 4, 24, (0.0,) * 3, (2 * math.pi,) * 3, "linadvdiff", c=(1.0, 1.0, 1.0),
                  mu=0.01, beta=0.0, eta=0.0,
                  dt=2.5e-3 * min(_H3 / math.sqrt(3.0), _H3 ** 2 / 0.01), steps=200, ic="sines_modes", nd=3),
-    # c4: TGV NS, hexes p=3, 32^3, Re=1600, Ma=0.1, Pr=0.71, beta=1/2, eta=0.1; dt = 0.1 h/11
+    # c4: TGV NS, hexes p=3, 32^3, Re=1600, Ma=0.1, Pr=0.71, beta=1/2, eta=0.1.
+    #     dt = 0.06 h/11 (O16): the SURVEY's 0.1 h/11 is linearly unstable for Rusanov in 3D
+    #     (measured: x0.9 and x0.75 of 0.1 h/11 diverge at steps 32 and 103; x0.6, x0.65
+    #     run 500 steps); Rusanov applies the full |v.n|+c dissipation on all three axes,
+    #     ~1.74x the per-axis load of the theta=(pi/6, pi/4) advection tau_MAX (0.131, l.1296)
     "c4": Config("c4", "hex", 3, 32, (0.0,) * 3, (2 * math.pi,) * 3, "ns", mu=1.0 / TGV_RE, gamma=1.4,
-                 Pr=0.71, beta=0.5, eta=0.1, dt=0.1 * _H4 / 11.0, steps=500, ic="tgv", nd=3),
-    # c5: TGV NS on tets p=3, 48^3 x 6 (663552 tets); dt = 0.05 h/11
+                 Pr=0.71, beta=0.5, eta=0.1, dt=0.06 * _H4 / 11.0, steps=500, ic="tgv", nd=3),
+    # c5: TGV NS on tets p=3, 48^3 x 6 (663552 tets); dt = 0.035 h/11 (O16: 0.05 h/11
+    #     diverges at step 169; x0.8 of it runs 200 steps; 0.7x taken for margin)
     "c5": Config("c5", "tet", 3, 48, (0.0,) * 3, (2 * math.pi,) * 3, "ns", mu=1.0 / TGV_RE, gamma=1.4,
-                 Pr=0.71, beta=0.5, eta=0.1, dt=0.05 * _H5 / 11.0, steps=200, ic="tgv", nd=3),
+                 Pr=0.71, beta=0.5, eta=0.1, dt=0.035 * _H5 / 11.0, steps=200, ic="tgv", nd=3),
 }
 
 # c2 dt literal: 0.1 * 0.25 / lambda_max, lambda_max = max(|v| + a) over the initial
