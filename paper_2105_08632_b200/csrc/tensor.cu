@@ -75,15 +75,52 @@ __device__ __forceinline__ double interp_end(const double (&Iend)[TMAXP + 1], co
   return acc;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Tile load [row][E] <- src[row][e0 .. e0+E): 16-byte cp.async (LDGSTS), all in
+// flight at once.  Rows have K_pad >= e0 + E columns (ABI), so no guards are needed;
+// padding columns are loaded but never used.
 template <int D, int P, int NV, int E>
 __device__ __forceinline__ void load_tile(const double* __restrict__ src, double* sU, int64_t e0, int64_t K,
                                           int64_t Kp) {
   constexpr int NS = TDims<D, P>::NS;
-  for (int idx = threadIdx.x; idx < NS * NV * E; idx += blockDim.x) {
-    const int el = idx % E, row = idx / E;
-    const int64_t e = e0 + el;
-    sU[idx] = e < K ? src[(int64_t)row * Kp + e] : 0.0;
+  constexpr int CH = E / 2;  // 16-byte chunks per row
+  (void)K;
+  for (int idx = threadIdx.x; idx < NS * NV * CH; idx += blockDim.x) {
+    const int c = idx % CH, row = idx / CH;
+    const double* g = src + (int64_t)row * Kp + e0 + 2 * c;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sU + row * E + 2 * c);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g));
   }
+  asm volatile("cp.async.commit_group;");
+}
+
+__device__ __forceinline__ void wait_tile() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// L2 prefetch of the rows [N_ext][N_V] of a trace array seen by a tile's face
+// neighbours (and optionally of the tile itself)
+template <int D, int P, int NV, int E>
+__device__ __forceinline__ void prefetch_traces(const TensorGeom& g, const double* __restrict__ T, int64_t e0,
+                                                bool own) {
+  using Tm = TDims<D, P>;
+  constexpr int NL = Tm::NL;
+  for (int item = threadIdx.x; item < 2 * D * NL * NV; item += blockDim.x) {
+    const int v = item % NV, ext = item / NV;
+    const int face = ext / NL, d = face / 2, side = face % 2;
+    // the neighbour across face (d, side) reads its opposite face (d, 1-side)
+    const int ext_n = (2 * d + 1 - side) * NL + ext % NL;
+    const int64_t m = tnbr<D>(g, e0, d, side ? 1 : -1);
+    prefetch_l2(T + ((int64_t)ext_n * NV + v) * g.Kp + m);
+    if (own) prefetch_l2(T + ((int64_t)ext * NV + v) * g.Kp + e0);
+  }
+}
+
+template <int D, int P, int NV, int E>
+__device__ __forceinline__ void prefetch_rows(const double* __restrict__ A, int64_t e0, int64_t Kp) {
+  constexpr int NS = TDims<D, P>::NS;
+  for (int row = threadIdx.x; row < NS * NV; row += blockDim.x) prefetch_l2(A + (int64_t)row * Kp + e0);
 }
 
 // gradient along lines -> sQ[d][s][v][E] = (2/h_d) (M16 C + M15 U_int)   (l.295-302)
@@ -95,8 +132,10 @@ __device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D
   constexpr int n = T::n, NL = T::NL, NS = T::NS;
   constexpr int NV = Phys<EQ, D>::NV;
   const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
-  for (int item = threadIdx.x; item < D * NL * E; item += blockDim.x) {
-    const int el = item % E, line = item / E, d = line / NL, t = line % NL;
+#pragma unroll
+  for (int d = 0; d < D; ++d)
+  for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
+    const int el = item % E, t = item / E;
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
     const int64_t mlo = tnbr<D>(g, e, d, -1), mhi = tnbr<D>(g, e, d, +1);
@@ -137,15 +176,20 @@ __device__ __forceinline__ void write_traces(const TensorGeom& g, const Line1D& 
                                              double* __restrict__ T, int64_t e0) {
   using Tm = TDims<D, P>;
   constexpr int n = Tm::n, NL = Tm::NL, NEXT = Tm::NEXT;
-  for (int item = threadIdx.x; item < NEXT * NV * E; item += blockDim.x) {
-    const int el = item % E, r = item / E, v = r % NV, ext = r / NV;
-    const int64_t e = e0 + el;
-    if (e >= g.K) continue;
-    const int face = ext / NL, t = ext % NL, d = face / 2, side = face % 2;
-    double u[n];
+  (void)NEXT;
 #pragma unroll
-    for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
-    T[((int64_t)ext * NV + v) * g.Kp + e] = interp_end<n>(L.Iend[side], u);
+  for (int face = 0; face < 2 * D; ++face) {
+    const int d = face / 2, side = face % 2;
+    for (int item = threadIdx.x; item < NL * NV * E; item += blockDim.x) {
+      const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+      const int64_t e = e0 + el;
+      if (e >= g.K) continue;
+      const int ext = face * NL + t;
+      double u[n];
+#pragma unroll
+      for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+      T[((int64_t)ext * NV + v) * g.Kp + e] = interp_end<n>(L.Iend[side], u);
+    }
   }
 }
 
@@ -156,6 +200,7 @@ __global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const d
   extern __shared__ double smem[];
   const int64_t e0 = (int64_t)blockIdx.x * E;
   load_tile<D, P, NV, E>(U, smem, e0, g.K, g.Kp);
+  wait_tile();
   __syncthreads();
   write_traces<D, P, NV, E>(g, L, smem, T, e0);
 }
@@ -171,15 +216,19 @@ __global__ void __launch_bounds__(256) kt_grad(TensorGeom g, Line1D L, PhysDev p
   double* sQ = smem + NS * NV * E;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   load_tile<D, P, NV, E>(b.Uin, sU, e0, g.K, g.Kp);
+  prefetch_traces<D, P, NV, E>(g, b.Tu, e0, false);
+  wait_tile();
   __syncthreads();
   gradient_lines<D, P, EQ, E>(g, L, ph, b.Tu, sU, sQ, e0);
   __syncthreads();
   // publish g at face points of the sides that carry weight: side 1 (left) if
   // 1/2 + beta != 0, side 0 (right) if 1/2 - beta != 0
   const bool pub1 = (0.5 + ph.beta) != 0.0, pub0 = (0.5 - ph.beta) != 0.0;
-  for (int item = threadIdx.x; item < 2 * D * NL * E; item += blockDim.x) {
-    const int el = item % E, ext = item / E;
-    const int face = ext / NL, t = ext % NL, d = face / 2, side = face % 2;
+#pragma unroll
+  for (int face = 0; face < 2 * D; ++face)
+  for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
+    const int el = item % E, t = item / E;
+    const int d = face / 2, side = face % 2, ext = face * NL + t;
     if ((side == 1 && !pub1) || (side == 0 && !pub0)) continue;
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
@@ -221,12 +270,20 @@ __global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev 
   double* sQ = sR + NS * NV * E;
   const int64_t e0 = (int64_t)blockIdx.x * E;
   load_tile<D, P, NV, E>(b.Uin, sU, e0, g.K, g.Kp);
+  // warm L2 with everything this tile reads later: neighbour traces, published
+  // viscous traces, RK registers (their latency is otherwise exposed mid-kernel)
+  prefetch_traces<D, P, NV, E>(g, b.Tu, e0, false);
+  if constexpr (Ph::VISC) prefetch_traces<D, P, NV, E>(g, b.Tg, e0, true);
+  if (stage == 1 || stage == 2) prefetch_rows<D, P, NV, E>(b.U, e0, g.Kp);
+  if (stage >= 1) prefetch_rows<D, P, NV, E>(b.ACC, e0, g.Kp);
+  wait_tile();
   __syncthreads();
   if constexpr (Ph::VISC) {
     gradient_lines<D, P, EQ, E>(g, L, ph, b.Tu, sU, sQ, e0);
     __syncthreads();
   }
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+#pragma unroll
   for (int d = 0; d < D; ++d) {
     const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
     for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
