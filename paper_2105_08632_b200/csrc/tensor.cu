@@ -283,52 +283,109 @@ __global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev 
     __syncthreads();
   }
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
-#pragma unroll
+  // neighbour element ids of the tile, once: sNb[2d + side][el]
+  __shared__ int sNb[2 * D][E];
+  for (int idx = threadIdx.x; idx < 2 * D * E; idx += blockDim.x) {
+    const int el = idx % E, k = idx / E;
+    const int64_t e = e0 + el;
+    sNb[k][el] = e < g.K ? (int)tnbr<D>(g, e, k / 2, (k % 2) ? 1 : -1) : 0;
+  }
+  __syncthreads();
+  const int Kp = (int)g.Kp;
+  // one code copy for all directions (runtime d): keeps the kernel inside the I-cache
+#pragma unroll 1
   for (int d = 0; d < D; ++d) {
     const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
+    const int str = (d == 0 ? 1 : (d == 1 ? n : n * n)) * NV * E;  // point stride along the line
     for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
       const int el = item % E, t = item / E;
-      const int64_t e = e0 + el;
+      const int e = (int)(e0 + el);
       if (e >= g.K) continue;
-      double u[n][NV];
+      const int base = d == 0 ? n * t : (d == 1 ? (D == 2 ? t : (t % n) + n * n * (t / n)) : t);
+      const double* pu = sU + base * NV * E + el;
+      const double* pq = sQ + base * NV * E + el;
+      double* pr = sR + base * NV * E + el;
+      // issue the line-end global loads first (consumed after the internal points)
+      const int mlo = sNb[2 * d][el], mhi = sNb[2 * d + 1][el];
+      const int xL = (2 * d + 1) * NL + t, xR = (2 * d) * NL + t;  // left's +face, right's -face
+      double un0[NV], un1[NV], gs0[NV], gs1[NV];
 #pragma unroll
-      for (int i = 0; i < n; ++i)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) u[i][v] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
-      double q[Ph::VISC ? n : 1][Ph::VISC ? D * NV : 1];
-      if constexpr (Ph::VISC) {
-#pragma unroll
-        for (int i = 0; i < n; ++i)
-#pragma unroll
-          for (int dd = 0; dd < D; ++dd)
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-              q[i][dd * NV + v] = sQ[((dd * NS + sidx<D, P>(d, t, i)) * NV + v) * E + el];
+      for (int v = 0; v < NV; ++v) {
+        un0[v] = b.Tu[(xL * NV + v) * Kp + mlo];   // left neighbour's trace (I am right)
+        un1[v] = b.Tu[(xR * NV + v) * Kp + mhi];   // right neighbour's trace (I am left)
+        if constexpr (Ph::VISC) {
+          const double* tg = b.Tg;
+          double a0 = 0.0, a1 = 0.0;
+          if (wl != 0.0) {
+            a0 = wl * tg[(xL * NV + v) * Kp + mlo];
+            a1 = wl * tg[(xL * NV + v) * Kp + e];
+          }
+          if (wr != 0.0) {
+            a0 = fma(wr, tg[(xR * NV + v) * Kp + e], a0);
+            a1 = fma(wr, tg[(xR * NV + v) * Kp + mhi], a1);
+          }
+          gs0[v] = a0;
+          gs1[v] = a1;
+        }
       }
       double r[n][NV];
 #pragma unroll
       for (int i = 0; i < n; ++i)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) r[i][v] = d == 0 ? 0.0 : sR[(sidx<D, P>(d, t, i) * NV + v) * E + el];
-      // internal flux points along the line (normal e_d): F~ = detJ (J^-1 f)_d
+        for (int v = 0; v < NV; ++v) r[i][v] = d == 0 ? 0.0 : pr[i * str + v * E];
+      // both ends: common flux with canonical (left, right) = (x_d- element, x_d+ element)
+      double nL[D];
 #pragma unroll
+      for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        double uo[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double ul[n];
+#pragma unroll
+          for (int i = 0; i < n; ++i) ul[i] = pu[i * str + v * E];
+          uo[v] = interp_end<n>(L.Iend[side], ul);
+        }
+        const double* uL = side ? uo : un0;
+        const double* uR = side ? un1 : uo;
+        double F[NV];
+        Ph::conv_common(ph, uL, uR, nL, F);
+        if constexpr (Ph::VISC) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) F[v] += (side ? gs1[v] : gs0[v]) + ph.eta * (uL[v] - uR[v]);
+        }
+        const double sD = side ? g.sface[d] : -g.sface[d];
+        // M14 column of this end: -L_0' (x_d = -1), +L_{p+1}' (x_d = +1)
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double m14 = side ? L.Dfl[i][P + 1] : -L.Dfl[i][0];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) r[i][v] = fma(m14, sD * F[v], r[i][v]);
+        }
+      }
+      // internal flux points along the line (normal e_d): F~ = detJ (J^-1 f)_d
+      // (not unrolled: bounds the live range to one point)
+#pragma unroll 1
       for (int a = 0; a < P; ++a) {
         double ua[NV], qa[Ph::VISC ? D * NV : 1], w[D], f[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          double s = 0.0;
+          double sacc = 0.0;
 #pragma unroll
-          for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i][v], s);
-          ua[v] = s;
+          for (int i = 0; i < n; ++i) sacc = fma(L.Iint[a][i], pu[i * str + v * E], sacc);
+          ua[v] = sacc;
         }
         if constexpr (Ph::VISC) {
 #pragma unroll
-          for (int k = 0; k < D * NV; ++k) {
-            double s = 0.0;
+          for (int dd = 0; dd < D; ++dd)
 #pragma unroll
-            for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], q[i][k], s);
-            qa[k] = s;
-          }
+            for (int v = 0; v < NV; ++v) {
+              double sacc = 0.0;
+#pragma unroll
+              for (int i = 0; i < n; ++i) sacc = fma(L.Iint[a][i], pq[dd * NS * NV * E + i * str + v * E], sacc);
+              qa[dd * NV + v] = sacc;
+            }
         }
 #pragma unroll
         for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
@@ -344,52 +401,10 @@ __global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev 
 #pragma unroll
           for (int v = 0; v < NV; ++v) r[i][v] = fma(L.Dfl[i][a + 1], f[v], r[i][v]);
       }
-      // both ends: common flux with canonical (left, right) = (x_d-side element, x_d+side)
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int64_t m = tnbr<D>(g, e, d, side ? 1 : -1);
-        const int ext_own = (2 * d + side) * NL + t, ext_nbr = (2 * d + 1 - side) * NL + t;
-        double uo[NV], un[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double ul[n];
-#pragma unroll
-          for (int i = 0; i < n; ++i) ul[i] = u[i][v];
-          uo[v] = interp_end<n>(L.Iend[side], ul);
-          un[v] = b.Tu[((int64_t)ext_nbr * NV + v) * g.Kp + m];
-        }
-        const double* uL = side ? uo : un;
-        const double* uR = side ? un : uo;
-        double nL[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
-        double F[NV];
-        Ph::conv_common(ph, uL, uR, nL, F);
-        if constexpr (Ph::VISC) {
-          const int64_t eL = side ? e : m, eR = side ? m : e;
-          const int xL = (2 * d + 1) * NL + t, xR = (2 * d) * NL + t;
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            double fv = 0.0;
-            if (wl != 0.0) fv = wl * b.Tg[((int64_t)xL * NV + v) * g.Kp + eL];
-            if (wr != 0.0) fv = fma(wr, b.Tg[((int64_t)xR * NV + v) * g.Kp + eR], fv);
-            F[v] += fv + ph.eta * (uL[v] - uR[v]);
-          }
-        }
-        (void)ext_own;
-        const double sD = side ? g.sface[d] : -g.sface[d];
-        // M14 column of this end: -L_0' (x_d = -1), +L_{p+1}' (x_d = +1)
-#pragma unroll
-        for (int i = 0; i < n; ++i) {
-          const double m14 = side ? L.Dfl[i][P + 1] : -L.Dfl[i][0];
-#pragma unroll
-          for (int v = 0; v < NV; ++v) r[i][v] = fma(m14, sD * F[v], r[i][v]);
-        }
-      }
 #pragma unroll
       for (int i = 0; i < n; ++i)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sR[(sidx<D, P>(d, t, i) * NV + v) * E + el] = r[i][v];
+        for (int v = 0; v < NV; ++v) pr[i * str + v * E] = r[i][v];
     }
     __syncthreads();
   }
