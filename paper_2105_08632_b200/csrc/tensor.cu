@@ -139,6 +139,13 @@ __device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
     const int64_t mlo = tnbr<D>(g, e, d, -1), mhi = tnbr<D>(g, e, d, +1);
+    // neighbour traces for all variables first (loads in flight together)
+    double nbl[NV], nbh[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      nbl[v] = Tu[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kp + mlo];
+      nbh[v] = Tu[((int64_t)((2 * d + 0) * NL + t) * NV + v) * g.Kp + mhi];
+    }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double u[n];
@@ -146,8 +153,8 @@ __device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D
       for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
       // common values at both ends (own trace recomputed bit-identically, neighbour read)
       const double own0 = interp_end<n>(L.Iend[0], u), own1 = interp_end<n>(L.Iend[1], u);
-      const double nb0 = Tu[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kp + mlo];
-      const double nb1 = Tu[((int64_t)((2 * d + 0) * NL + t) * NV + v) * g.Kp + mhi];
+      const double nb0 = nbl[v];
+      const double nb1 = nbh[v];
       const double c0 = wl * nb0 + wr * own0;   // face x_d = -1: this element is RIGHT
       const double c1 = wl * own1 + wr * nb1;   // face x_d = +1: this element is LEFT
       double ui[P];
@@ -408,42 +415,63 @@ __global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev 
     }
     __syncthreads();
   }
-  // dU/dt = -R~/detJ, RK4 (3-register form), new state into sU
+  // dU/dt = -R~/detJ, RK4 (3-register form), new state into sU.  Rows are processed in
+  // batches of RB_RK per thread with all global loads of a batch issued before use.
   const double idet = 1.0 / g.detJ;
-  for (int idx = threadIdx.x; idx < NS * NV * E; idx += blockDim.x) {
-    const int el = idx % E, row = idx / E;
-    const int64_t e = e0 + el;
-    if (e >= g.K) continue;
-    const int64_t gi = (int64_t)row * g.Kp + e;
-    const double k = -sR[idx] * idet;
-    double nu;
-    switch (stage) {
-      case -1:
-        b.out[gi] = k;
-        nu = 0.0;
-        break;
-      case 0: {
-        const double u0 = sU[idx];
-        b.ACC[gi] = fma(dt / 6.0, k, u0);
-        nu = fma(0.5 * dt, k, u0);
-        b.Us[gi] = nu;
-      } break;
-      case 1:
-        b.ACC[gi] = fma(dt / 3.0, k, b.ACC[gi]);
-        nu = fma(0.5 * dt, k, b.U[gi]);
-        b.Us[gi] = nu;
-        break;
-      case 2:
-        b.ACC[gi] = fma(dt / 3.0, k, b.ACC[gi]);
-        nu = fma(dt, k, b.U[gi]);
-        b.Us[gi] = nu;
-        break;
-      default:
-        nu = fma(dt / 6.0, k, b.ACC[gi]);
-        b.U[gi] = nu;
-        break;
+  constexpr int TOT = NS * NV * E;
+  constexpr int RB_RK = 5;
+  const int nth = blockDim.x;
+  for (int base0 = threadIdx.x; base0 < TOT; base0 += RB_RK * nth) {
+    double a0[RB_RK], a1[RB_RK];
+    int64_t gi[RB_RK];
+    bool ok[RB_RK];
+#pragma unroll
+    for (int k = 0; k < RB_RK; ++k) {
+      const int idx = base0 + k * nth;
+      const int el = idx % E, row = idx / E;
+      ok[k] = idx < TOT && e0 + el < g.K;
+      gi[k] = (int64_t)row * g.Kp + e0 + el;
+      a0[k] = 0.0;
+      a1[k] = 0.0;
+      if (ok[k]) {
+        if (stage >= 1) a0[k] = __ldcs(b.ACC + gi[k]);
+        if (stage == 1 || stage == 2) a1[k] = __ldcs(b.U + gi[k]);
+      }
     }
-    sU[idx] = nu;
+#pragma unroll
+    for (int k = 0; k < RB_RK; ++k) {
+      if (!ok[k]) continue;
+      const int idx = base0 + k * nth;
+      const double kk = -sR[idx] * idet;
+      double nu;
+      switch (stage) {
+        case -1:
+          b.out[gi[k]] = kk;
+          nu = 0.0;
+          break;
+        case 0: {
+          const double u0 = sU[idx];
+          b.ACC[gi[k]] = fma(dt / 6.0, kk, u0);
+          nu = fma(0.5 * dt, kk, u0);
+          b.Us[gi[k]] = nu;
+        } break;
+        case 1:
+          b.ACC[gi[k]] = fma(dt / 3.0, kk, a0[k]);
+          nu = fma(0.5 * dt, kk, a1[k]);
+          b.Us[gi[k]] = nu;
+          break;
+        case 2:
+          b.ACC[gi[k]] = fma(dt / 3.0, kk, a0[k]);
+          nu = fma(dt, kk, a1[k]);
+          b.Us[gi[k]] = nu;
+          break;
+        default:
+          nu = fma(dt / 6.0, kk, a0[k]);
+          b.U[gi[k]] = nu;
+          break;
+      }
+      sU[idx] = nu;
+    }
   }
   if (stage < 0) return;
   __syncthreads();
