@@ -25,6 +25,7 @@
 #include "capi_internal.h"
 #include "ctx.h"
 #include "tensor.cuh"
+#include "simplex.cuh"
 
 namespace sdrt {
 
@@ -295,7 +296,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, off_tu0, off_tu1, off_tg, total;
+      off_bad, off_tu0, off_tu1, off_tg, off_sops, total;
   size_t ops_bytes;
 };
 
@@ -332,11 +333,12 @@ static void build_ops(const Operators& O, int D, Mat ops[5]) {
 using namespace sdrt;
 
 enum KTag { T_M0 = 0, T_M12, T_CV, T_GRAD, T_METRIC, T_QEXT, T_QU, T_IFLUX, T_FFLUX, T_DIV, T_RK,
-            T_TRACE, T_FA, T_FB, T_NTAGS };
+            T_TRACE, T_FA, T_FB, T_STRACE, T_SA, T_SB, T_NTAGS };
 static const char* KTAG_NAMES[T_NTAGS] = {"interp_ext(M0)", "interp_int(M12)", "common_value", "gradient(M16|M15P)",
                                           "metric_grad", "grad_interp_ext(M5)", "grad_interp_int(M18)",
                                           "int_flux", "face_flux", "divergence(M14|M13M19P2)", "rk_update",
-                                          "tensor_traces", "tensor_grad(A)", "tensor_stage(B)"};
+                                          "tensor_traces", "tensor_grad(A)", "tensor_stage(B)",
+                                          "simplex_traces", "simplex_grad(A)", "simplex_stage(B)"};
 
 struct sdrt_ctx {
   bool timing = false;
@@ -360,7 +362,63 @@ struct sdrt_ctx {
   double* Tu[2] = {nullptr, nullptr};
   double* Tg = nullptr;
   int cur = 0;
+  // fused simplex path
+  bool sfused = false;
+  SimplexOps sops;
 };
+
+struct OpHost4 {
+  std::vector<int> ptr, col;
+  std::vector<double> val;
+  int rows, cols, nblk;
+};
+
+static OpHost4 pack4(const Mat& M, const std::vector<int>* colmap = nullptr) {
+  OpHost4 o;
+  o.rows = M.rows;
+  o.cols = M.cols;
+  o.nblk = (M.rows + SRB - 1) / SRB;
+  o.ptr.push_back(0);
+  for (int b = 0; b < o.nblk; ++b) {
+    for (int c = 0; c < M.cols; ++c) {
+      bool nz = false;
+      for (int r = b * SRB; r < std::min(M.rows, (b + 1) * SRB); ++r) nz = nz || M(r, c) != 0.0;
+      if (!nz) continue;
+      o.col.push_back(colmap ? (*colmap)[c] : c);
+      for (int r = b * SRB; r < (b + 1) * SRB; ++r) o.val.push_back(r < M.rows ? M(r, c) : 0.0);
+    }
+    o.ptr.push_back((int)o.col.size());
+  }
+  return o;
+}
+
+// simplex operators: M0, M12, G = [M16 | M15 P] rows (s,d), M14, M13 M19 P2 (cols (d,u))
+static void simplex_pack(const Operators& O, int D, std::vector<OpHost4>* out, Mat* M0dense) {
+  const RefElement& r = O.ref;
+  int ns = r.nsol;
+  Mat G(ns * D, r.next + r.nu);
+  for (int s2 = 0; s2 < ns; ++s2)
+    for (int d = 0; d < D; ++d) {
+      for (int e = 0; e < r.next; ++e) G(s2 * D + d, e) = O.M16(d * ns + s2, e);
+      for (int i = 0; i < r.nint; ++i) {
+        double v = O.M15(d * ns + s2, i);
+        if (v != 0.0) G(s2 * D + d, r.next + r.int_u[i]) += v;
+      }
+    }
+  Mat M13F(ns, D * r.nu);
+  for (int s2 = 0; s2 < ns; ++s2)
+    for (int i = 0; i < r.nint; ++i) {
+      double v = O.M13(s2, i);
+      if (v != 0.0) M13F(s2, r.int_dir[i] * r.nu + r.int_u[i]) += v;
+    }
+  out->clear();
+  out->push_back(pack4(O.M0));
+  out->push_back(pack4(O.M12));
+  out->push_back(pack4(G));
+  out->push_back(pack4(O.M14));
+  out->push_back(pack4(M13F));
+  *M0dense = O.M0;
+}
 
 static int nvars(int eq, int D) { return (eq == SDRT_EQ_LINADV || eq == SDRT_EQ_LINADVDIFF) ? 1 : D + 2; }
 
@@ -393,10 +451,20 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.ops_bytes = ob;
   p.off_xm = o; o += align256((size_t)m.nsub * r.next * sizeof(ExtMetric));
   p.off_bad = o; o += 256;
-  size_t tb = etype_tensor(m.etype) ? align256((size_t)r.next * col) : 0;
+  size_t tb = align256((size_t)r.next * col);
   p.off_tu0 = o; o += tb;
   p.off_tu1 = o; o += tb;
   p.off_tg = o; o += tb;
+  p.off_sops = o;
+  if (!etype_tensor(m.etype)) {
+    std::vector<OpHost4> s4;
+    Mat dense;
+    simplex_pack(O, D, &s4, &dense);
+    for (auto& h : s4)
+      o += align256(h.ptr.size() * sizeof(int)) + align256(h.col.size() * sizeof(int) + 4) +
+           align256(h.val.size() * sizeof(double) + 8);
+    o += align256(dense.a.size() * sizeof(double));
+  }
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -548,6 +616,36 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tu[0] = (double*)(base + p.off_tu0);
       c->Tu[1] = (double*)(base + p.off_tu1);
       c->Tg = (double*)(base + p.off_tg);
+    }
+    c->sfused = !etype_tensor(m.etype) && !(fg && fg[0] == '1') && simplex_supported(m.nd, m.p, ph->eq);
+    if (c->sfused) {
+      std::vector<OpHost4> s4;
+      Mat dense;
+      simplex_pack(O, m.nd, &s4, &dense);
+      size_t so = p.off_sops;
+      SOp* dst[5] = {&c->sops.M0, &c->sops.M12, &c->sops.G, &c->sops.M14, &c->sops.M13F};
+      for (int i = 0; i < 5; ++i) {
+        OpHost4& h = s4[i];
+        int* dptr = (int*)(base + so);
+        CUDA_OK(cudaMemcpyAsync(dptr, h.ptr.data(), h.ptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        so += align256(h.ptr.size() * sizeof(int));
+        int* dcol = (int*)(base + so);
+        if (!h.col.empty())
+          CUDA_OK(cudaMemcpyAsync(dcol, h.col.data(), h.col.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        so += align256(h.col.size() * sizeof(int) + 4);
+        double* dval = (double*)(base + so);
+        if (!h.val.empty())
+          CUDA_OK(cudaMemcpyAsync(dval, h.val.data(), h.val.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        so += align256(h.val.size() * sizeof(double) + 8);
+        *dst[i] = SOp{h.rows, h.cols, h.nblk, dptr, dcol, dval};
+      }
+      double* dd = (double*)(base + so);
+      CUDA_OK(cudaMemcpyAsync(dd, dense.a.data(), dense.a.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+      c->sops.M0dense = dd;
+      c->Tu[0] = (double*)(base + p.off_tu0);
+      c->Tu[1] = (double*)(base + p.off_tu1);
+      c->Tg = (double*)(base + p.off_tg);
+      CUDA_OK(cudaStreamSynchronize(st));
     }
     CUDA_OK(cudaStreamSynchronize(st));  // host vectors go out of scope
     *out = c;
@@ -722,6 +820,34 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
   if (stage >= 0) c->cur ^= 1;
 }
 
+static void sfused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
+  Mark mk(c, st, T_STRACE);
+  simplex_launch_traces(c->nd, c->p, c->eq, c->g, c->sops, U, c->Tu[c->cur], st);
+}
+
+static void sfused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, double dt, double* out,
+                         cudaStream_t st) {
+  SimplexBufs b;
+  b.Uin = Uin;
+  b.U = U;
+  b.Us = c->Us;
+  b.ACC = c->ACC;
+  b.out = out;
+  b.Tu = c->Tu[c->cur];
+  b.Tu_next = c->Tu[c->cur ^ 1];
+  b.Tg = c->Tg;
+  b.xm = c->xm;
+  if (c->visc) {
+    Mark mk(c, st, T_SA);
+    simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, st);
+  }
+  {
+    Mark mk(c, st, T_SB);
+    simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, stage, dt, st);
+  }
+  if (stage >= 0) c->cur ^= 1;
+}
+
 typedef void (*ResFn)(sdrt_ctx*, const double*, int, double, double*, double*, cudaStream_t);
 typedef bool (*ChkFn)(sdrt_ctx*, const double*, cudaStream_t, int64_t*);
 
@@ -755,6 +881,9 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
     if (c->fused) {
       fused_traces(c, d_U, st);
       fused_stage(c, d_U, nullptr, -1, 0.0, d_dUdt, st);
+    } else if (c->sfused) {
+      sfused_traces(c, d_U, st);
+      sfused_stage(c, d_U, nullptr, -1, 0.0, d_dUdt, st);
     } else {
       pick_res(c->eq, c->nd)(c, d_U, -1, 0.0, d_dUdt, nullptr, st);
     }
@@ -773,9 +902,11 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
     cudaStream_t st = (cudaStream_t)stream;
     ResFn res = pick_res(c->eq, c->nd);
     if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
+    if (c->sfused && nsteps > 0) sfused_traces(c, d_U, st);
     for (int step = 0; step < nsteps; ++step) {
       for (int s = 0; s < 4; ++s) {
         if (c->fused) fused_stage(c, s == 0 ? d_U : c->Us, d_U, s, dt, nullptr, st);
+        else if (c->sfused) sfused_stage(c, s == 0 ? d_U : c->Us, d_U, s, dt, nullptr, st);
         else res(c, s == 0 ? d_U : c->Us, s, dt, nullptr, d_U, st);
       }
       CUDA_OK(cudaGetLastError());
