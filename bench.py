@@ -8,9 +8,12 @@ configuration's full mesh.  value = N_sol * N_V * K_elems * 4 * steps (summed ov
 ranks) / max-over-ranks device time / 1e9  [GDOF-stage/s]  (1/PM of PAPER.md
 Eq. performance_per_iter_measure l.2942-2951 with N_RK = 4).
 
-N > 1 (torchrun, one rank per GPU): weak scaling, each rank advances its own copy
-of the configuration's periodic mesh (replicas; the NCCL halo path is DESIGN.md
-"next").  --impl reference times the CPU oracle (rank 0 only).
+N > 1 (torchrun, one rank per GPU): weak scaling with the element-partitioned path
+(paper_2105_08632_b200.dist): the global periodic mesh is the configuration's mesh
+repeated pgrid times (1: 1x1x1, 2: 2x1x1, 4: 2x2x1, 8: 2x2x2; same h, so each rank owns
+exactly the configuration's block) and face traces cross rank boundaries through NCCL
+point-to-point halo exchanges every stage.  --impl reference times the CPU oracle
+(rank 0 only).
 """
 from __future__ import annotations
 
@@ -226,7 +229,16 @@ def main():
         dist.barrier()
     from paper_2105_08632_b200.solver import Solver
 
-    S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, **cfg.physics_kwargs())
+    if world > 1:
+        from paper_2105_08632_b200.dist import DistSolver, default_pgrid
+        pgrid = default_pgrid(world, cfg.nd)
+        Ng = [cfg.N * g for g in pgrid]
+        hi = [l + (h - l) * g for l, h, g in zip(cfg.lo, cfg.hi, pgrid)]
+        S = DistSolver(cfg.etype, cfg.p, Ng, cfg.lo, hi, cfg.eq, device=dev, pgrid=pgrid, **cfg.physics_kwargs())
+        parallelism = f"element partition {'x'.join(map(str, pgrid))}, NCCL halo"
+    else:
+        S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, **cfg.physics_kwargs())
+        parallelism = "single"
     U0 = initial_state(cfg, S.sol_coords())
     U = S.to_device(U0)
     nsol, nv, Kp = S.shape
@@ -347,7 +359,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": WORKLOADS[cfg.name], "elements_per_gpu": K, "dof_per_gpu": dof,
-                          "p": cfg.p, "dt": cfg.dt, "parallelism": f"replicas x{world}" if world > 1 else "single",
+                          "p": cfg.p, "dt": cfg.dt, "parallelism": parallelism,
                           "l2": "working set > L2 (state 3 registers + traces >> 126 MB); no flush needed"
                           if dof * 8 * 3 > 126e6 else "working set fits L2 (small config)"},
                "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,

@@ -76,6 +76,7 @@ typedef struct {
   int64_t K;           /* local elements */
   int64_t K_pad;       /* K rounded up to a multiple of 32 */
   int64_t n_faces;     /* local face count (faces whose left element is local) */
+  int64_t K_trace;     /* row stride of the internal trace arrays (K_pad + ghost columns) */
 } sdrt_mesh_info_t;
 
 int sdrt_abi_version(void);
@@ -105,6 +106,21 @@ sdrt_status sdrt_mesh_sol_coords(const sdrt_mesh* m, double* x);
 /* Per-element det J (host, [K]), used for conservation sums. */
 sdrt_status sdrt_mesh_detj(const sdrt_mesh* m, double* detj);
 void sdrt_mesh_destroy(sdrt_mesh* m);
+/* Halo (multi-rank element partition).  Trace arrays carry ghost columns
+ * after K_pad for the neighbouring ranks' boundary elements; one exchange moves, per
+ * slab (axis d, side), the face-point traces of this rank's boundary elements facing the
+ * peer.  force_self_halo = 1 routes periodic wraps of single-rank axes through the same
+ * path (loopback; the library then exchanges by itself).  Call before sdrt_ctx_create. */
+sdrt_status sdrt_mesh_set_halo(sdrt_mesh* m, int force_self_halo);
+/* slab = -1: *count = number of slabs.  Otherwise the slab's peer rank, axis, side,
+ * entry count and (trace row, column) lists in the canonical order (any pointer may be
+ * NULL; host arrays of *count int32).  The peer's send list for its opposite slab
+ * matches this rank's recv list entry by entry. */
+sdrt_status sdrt_mesh_halo_lists(const sdrt_mesh* m, int slab, int* peer, int* d, int* side, int64_t* count,
+                                 int32_t* send_row, int32_t* send_col, int32_t* recv_row, int32_t* recv_col);
+/* Trace column the kernels read for the neighbour of local element e across local face
+ * f (a local element id, or a ghost column >= K_pad), and the neighbour's local face. */
+sdrt_status sdrt_mesh_neighbor(const sdrt_mesh* m, int64_t e, int f, int64_t* col, int* face);
 
 /* Appendix-B operators for (etype, p), built in __float128 and rounded once.
  * Errors: SDRT_E_UNSUPPORTED, SDRT_E_ILL_CONDITIONED (cond(V^f) > 1e12). */
@@ -136,6 +152,25 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
 sdrt_status sdrt_ctx_set_timing(sdrt_ctx* c, int enable);
 sdrt_status sdrt_ctx_kernel_times(sdrt_ctx* c, int max_tags, char* names, double* ms, int64_t* counts,
                                   int* ntags);
+/* Staged stage API for multi-rank runs (caller performs the halo exchange between calls):
+ *   sdrt_stage_traces(U)                       traces of U          -> exchange which=0
+ *   for stage s in 0..3:
+ *     sdrt_stage_grad(U, s)   (viscous only)   viscous traces       -> exchange which=1
+ *     sdrt_stage_flux(U, s, dt, NULL)          RK stage, new traces -> exchange which=0
+ * stage = -1 with d_out computes dU/dt into d_out instead (residual).  The stage input
+ * is U for s <= 0 and the internal stage register otherwise. */
+sdrt_status sdrt_stage_traces(sdrt_ctx* c, const double* d_U, void* stream);
+sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream);
+sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, void* stream);
+/* Halo buffers: *nslab slabs; peer/d/side per slab (arrays of 6), offset[nslab+1] =
+ * value offsets of each slab's segment in the contiguous send / recv buffers (doubles).
+ * pack copies this rank's outgoing traces (which = 0: U traces of the current stage
+ * input, 1: published viscous traces) into d_send; unpack scatters d_recv, where
+ * segment i holds what the peer of slab i sent from its opposite slab, into the ghost
+ * columns.  Device buffers, caller-owned. */
+sdrt_status sdrt_halo_info(const sdrt_ctx* c, int* nslab, int* peer, int* d, int* side, int64_t* offset);
+sdrt_status sdrt_halo_pack(sdrt_ctx* c, int which, double* d_send, void* stream);
+sdrt_status sdrt_halo_unpack(sdrt_ctx* c, int which, const double* d_recv, void* stream);
 /* Number of kernel launches enqueued by the last sdrt_residual / sdrt_rk_step call. */
 int64_t sdrt_ctx_last_launches(const sdrt_ctx* c);
 void sdrt_ctx_destroy(sdrt_ctx* c);

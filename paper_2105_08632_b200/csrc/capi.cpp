@@ -73,6 +73,7 @@ sdrt_status sdrt_mesh_info(const sdrt_mesh* mm, sdrt_mesh_info_t* out) {
   for (int s = 0; s < m.nsub; ++s)
     for (int f = 0; f < r.nfaces; ++f) nl += m.link[s * r.nfaces + f].left;
   out->n_faces = nl * (m.K / m.nsub);
+  out->K_trace = m.Kt;
   return SDRT_OK;
 }
 
@@ -149,6 +150,81 @@ sdrt_status sdrt_mesh_detj(const sdrt_mesh* mm, double* detj) {
 }
 
 void sdrt_mesh_destroy(sdrt_mesh* m) { delete m; }
+
+sdrt_status sdrt_mesh_set_halo(sdrt_mesh* m, int force_self_halo) {
+  if (!m) {
+    sdrt::set_error("null mesh");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    sdrt::build_halo(m->m, force_self_halo != 0);
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_mesh_halo_lists(const sdrt_mesh* mm, int slab, int* peer, int* d, int* side, int64_t* count,
+                                 int32_t* send_row, int32_t* send_col, int32_t* recv_row, int32_t* recv_col) {
+  if (!mm) {
+    sdrt::set_error("null mesh");
+    return SDRT_E_INVALID_ARG;
+  }
+  const sdrt::Mesh& m = mm->m;
+  if (slab < 0 || slab >= (int)m.slabs.size()) {
+    if (count) *count = -1;
+    if (slab == -1 && count) *count = (int64_t)m.slabs.size();
+    if (slab == -1) return SDRT_OK;
+    sdrt::set_error("slab index out of range");
+    return SDRT_E_INVALID_ARG;
+  }
+  const sdrt::HaloSlab& S = m.slabs[slab];
+  if (peer) *peer = S.peer;
+  if (d) *d = S.d;
+  if (side) *side = S.side;
+  if (count) *count = (int64_t)S.send_row.size();
+  for (size_t i = 0; i < S.send_row.size(); ++i) {
+    if (send_row) send_row[i] = S.send_row[i];
+    if (send_col) send_col[i] = S.send_col[i];
+    if (recv_row) recv_row[i] = S.recv_row[i];
+    if (recv_col) recv_col[i] = S.recv_col[i];
+  }
+  return SDRT_OK;
+}
+
+sdrt_status sdrt_mesh_neighbor(const sdrt_mesh* mm, int64_t e, int f, int64_t* col, int* face) {
+  if (!mm || !col || !face) {
+    sdrt::set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  const sdrt::Mesh& m = mm->m;
+  if (e < 0 || e >= m.K || f < 0 || f >= m.ref.nfaces) {
+    sdrt::set_error("element / face out of range");
+    return SDRT_E_INVALID_ARG;
+  }
+  const int s = (int)(e % m.nsub);
+  const sdrt::FaceLink& L = m.link[s * m.ref.nfaces + f];
+  int64_t pat = e / m.nsub;
+  int c[3] = {0, 0, 0};
+  for (int d = 0; d < m.nd; ++d) {
+    c[d] = (int)(pat % m.Nloc[d]);
+    pat /= m.Nloc[d];
+  }
+  *face = L.nface;
+  int64_t id = 0, mul = 1;
+  for (int d = 0; d < m.nd; ++d) {
+    int cc = c[d] + L.off[d];
+    if ((cc < 0 || cc >= m.Nloc[d]) && m.halo[d]) {
+      const int a = d == 0 ? 1 : 0, b = d == 2 ? 1 : 2;
+      const int64_t tang = m.nd == 2 ? c[a] : c[a] + (int64_t)m.Nloc[a] * c[b];
+      *col = m.gbase[d][cc < 0 ? 0 : 1] + tang * m.nsub + L.nshape;
+      return SDRT_OK;
+    }
+    cc = (cc + m.Nloc[d]) % m.Nloc[d];
+    id += mul * cc;
+    mul *= m.Nloc[d];
+  }
+  *col = id * m.nsub + L.nshape;
+  return SDRT_OK;
+}
 
 sdrt_status sdrt_operators_build(int etype, int p, int scheme, sdrt_operators** out) {
   if (!out) {

@@ -27,6 +27,9 @@ struct GeomDev {
   int nd, nsub, nfaces, nfp, next;
   int Nloc[3], Nglob[3], offset[3];
   int64_t K, Kp;
+  int64_t Kt;             // trace row stride (K_pad + ghost columns)
+  int halo[3];            // axis uses ghost slabs
+  int64_t gbase[3][2];    // first ghost column of slab (d, side)
   double detJ[MAXSUB];
   double Jinv[MAXSUB][9];
   // per (shape, face)

@@ -266,6 +266,25 @@ __global__ void k_check(GeomDev g, PhysDev ph, const double* __restrict__ U, int
   }
 }
 
+// halo: pack / unpack trace entries (row, col) x N_V  <->  contiguous buffer
+__global__ void k_halo_pack(const double* __restrict__ T, int64_t Kt, int NV, const int32_t* __restrict__ row,
+                            const int32_t* __restrict__ col, int64_t n, double* __restrict__ buf) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * NV) return;
+  const int64_t k = idx / NV;
+  const int v = (int)(idx % NV);
+  buf[idx] = T[((int64_t)row[k] * NV + v) * Kt + col[k]];
+}
+
+__global__ void k_halo_unpack(double* __restrict__ T, int64_t Kt, int NV, const int32_t* __restrict__ row,
+                              const int32_t* __restrict__ col, int64_t n, const double* __restrict__ buf) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * NV) return;
+  const int64_t k = idx / NV;
+  const int v = (int)(idx % NV);
+  T[((int64_t)row[k] * NV + v) * Kt + col[k]] = buf[idx];
+}
+
 // ------------------------------------------------------------------------ host side
 struct OpHost {
   std::vector<int> ptr, col;
@@ -296,7 +315,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, off_tu0, off_tu1, off_tg, off_sops, total;
+      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, total;
   size_t ops_bytes;
 };
 
@@ -365,6 +384,14 @@ struct sdrt_ctx {
   // fused simplex path
   bool sfused = false;
   SimplexOps sops;
+  // halo exchange
+  bool needs_halo = false, loopback = false;
+  int nslab = 0;
+  int slab_peer[6], slab_d[6], slab_side[6];
+  int64_t slab_off[7];        // entry offsets of each slab in the send/recv lists
+  int32_t *h_srow = nullptr, *h_scol = nullptr, *h_rrow = nullptr, *h_rcol = nullptr;
+  double* h_stage = nullptr;  // loopback staging buffer
+  bool auto_halo = false;     // library performs the (loopback) exchange itself
 };
 
 struct OpHost4 {
@@ -451,7 +478,7 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.ops_bytes = ob;
   p.off_xm = o; o += align256((size_t)m.nsub * r.next * sizeof(ExtMetric));
   p.off_bad = o; o += 256;
-  size_t tb = align256((size_t)r.next * col);
+  size_t tb = align256((size_t)r.next * NV * m.Kt * sizeof(double));
   p.off_tu0 = o; o += tb;
   p.off_tu1 = o; o += tb;
   p.off_tg = o; o += tb;
@@ -465,6 +492,13 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
            align256(h.val.size() * sizeof(double) + 8);
     o += align256(dense.a.size() * sizeof(double));
   }
+  // halo lists: send (row, col) and recv (row, col) int32 for all slabs, + a loopback
+  // staging buffer of the same number of values
+  size_t ent = 0;
+  for (const HaloSlab& S : m.slabs) ent += S.send_row.size();
+  p.halo_entries = ent;
+  p.off_halo = o;
+  o += align256(ent * 4 * sizeof(int32_t)) + align256(ent * NV * sizeof(double));
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -497,9 +531,8 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     set_error("unknown equation");
     return SDRT_E_INVALID_ARG;
   }
-  if (m.nranks != 1) {
-    set_error("multi-rank contexts are created with sdrt_ctx_create on a rank-local mesh; halo exchange "
-              "is not enabled in this build");
+  if (m.slabs.size() > 0 && !((etype_tensor(m.etype) || m.etype == TRI || m.etype == TET))) {
+    set_error("halo exchange needs the fused paths");
     return SDRT_E_UNSUPPORTED;
   }
   SDRT_TRY({
@@ -576,6 +609,51 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         for (int q = 0; q < r.nfp; ++q) g.perm[s][f][q] = (int8_t)L.perm[q];
       }
     }
+    g.Kt = m.Kt;
+    for (int d = 0; d < 3; ++d) {
+      g.halo[d] = m.halo[d];
+      g.gbase[d][0] = m.gbase[d][0];
+      g.gbase[d][1] = m.gbase[d][1];
+    }
+    // halo plan
+    c->nslab = (int)m.slabs.size();
+    c->needs_halo = c->nslab > 0;
+    c->loopback = c->needs_halo;
+    c->auto_halo = false;
+    {
+      int64_t ofs = 0;
+      std::vector<int32_t> lists;
+      std::vector<int32_t> sr, sc, rr, rcol;
+      for (int i = 0; i < c->nslab; ++i) {
+        const HaloSlab& S = m.slabs[i];
+        c->slab_peer[i] = S.peer;
+        c->slab_d[i] = S.d;
+        c->slab_side[i] = S.side;
+        c->slab_off[i] = ofs;
+        if (S.peer != m.rank) c->loopback = false;
+        if (S.send_row.size() != S.recv_row.size()) throw std::runtime_error("internal: halo list sizes differ");
+        sr.insert(sr.end(), S.send_row.begin(), S.send_row.end());
+        sc.insert(sc.end(), S.send_col.begin(), S.send_col.end());
+        rr.insert(rr.end(), S.recv_row.begin(), S.recv_row.end());
+        rcol.insert(rcol.end(), S.recv_col.begin(), S.recv_col.end());
+        ofs += (int64_t)S.send_row.size();
+      }
+      c->slab_off[c->nslab] = ofs;
+      c->auto_halo = c->loopback;
+      if (ofs > 0) {
+        int32_t* hl = (int32_t*)(base + p.off_halo);
+        c->h_srow = hl;
+        c->h_scol = hl + ofs;
+        c->h_rrow = hl + 2 * ofs;
+        c->h_rcol = hl + 3 * ofs;
+        CUDA_OK(cudaMemcpyAsync(c->h_srow, sr.data(), ofs * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(c->h_scol, sc.data(), ofs * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(c->h_rrow, rr.data(), ofs * 4, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(c->h_rcol, rcol.data(), ofs * 4, cudaMemcpyHostToDevice, st));
+        c->h_stage = (double*)(base + p.off_halo + align256(ofs * 4 * sizeof(int32_t)));
+        CUDA_OK(cudaStreamSynchronize(st));
+      }
+    }
     std::vector<ExtMetric> xm(m.nsub * r.next);
     for (int i = 0; i < m.nsub * r.next; ++i)
       xm[i] = ExtMetric{m.sscale[i], m.nleft[i][0], m.nleft[i][1], m.nleft[i][2]};
@@ -594,6 +672,12 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       for (int d = 0; d < 3; ++d) t.N[d] = m.Nloc[d];
       t.K = m.K;
       t.Kp = m.K_pad;
+      t.Kt = m.Kt;
+      for (int d = 0; d < 3; ++d) {
+        t.halo[d] = m.halo[d];
+        t.gbase[d][0] = m.gbase[d][0];
+        t.gbase[d][1] = m.gbase[d][1];
+      }
       t.detJ = m.detJ[0];
       for (int d = 0; d < 3; ++d) {
         t.jinv[d] = d < m.nd ? m.Jinv[0][d * 3 + d] : 0.0;
@@ -618,6 +702,11 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tg = (double*)(base + p.off_tg);
     }
     c->sfused = !etype_tensor(m.etype) && !(fg && fg[0] == '1') && simplex_supported(m.nd, m.p, ph->eq);
+    if (m.slabs.size() > 0 && !c->fused && !c->sfused) {
+      delete c;
+      set_error("unsupported: halo exchange is implemented for the fused paths only");
+      return SDRT_E_UNSUPPORTED;
+    }
     if (c->sfused) {
       std::vector<OpHost4> s4;
       Mat dense;
@@ -793,9 +882,50 @@ static bool check_impl(sdrt_ctx* c, const double* U, cudaStream_t st, int64_t* b
   return host == ~0ull;
 }
 
+static double* trace_buf(sdrt_ctx* c, int which) { return which == 0 ? c->Tu[c->cur] : c->Tg; }
+
+static void halo_pack(sdrt_ctx* c, int which, double* buf, cudaStream_t st) {
+  const int64_t n = c->slab_off[c->nslab];
+  if (n == 0) return;
+  const int64_t tot = n * c->nv;
+  k_halo_pack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(trace_buf(c, which), c->g.Kt, c->nv, c->h_srow,
+                                                              c->h_scol, n, buf);
+  c->launches++;
+}
+
+static void halo_unpack(sdrt_ctx* c, int which, const double* buf, cudaStream_t st) {
+  const int64_t n = c->slab_off[c->nslab];
+  if (n == 0) return;
+  const int64_t tot = n * c->nv;
+  k_halo_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(trace_buf(c, which), c->g.Kt, c->nv, c->h_rrow,
+                                                                c->h_rcol, n, buf);
+  c->launches++;
+}
+
+// loopback: every slab's peer is this rank; slab (d, s) receives what slab (d, 1-s) sent
+static void halo_loopback(sdrt_ctx* c, int which, cudaStream_t st) {
+  if (!c->needs_halo) return;
+  halo_pack(c, which, c->h_stage, st);
+  for (int i = 0; i < c->nslab; ++i) {
+    int j = -1;
+    for (int k = 0; k < c->nslab; ++k)
+      if (c->slab_d[k] == c->slab_d[i] && c->slab_side[k] == 1 - c->slab_side[i]) j = k;
+    const int64_t n = c->slab_off[i + 1] - c->slab_off[i];
+    if (n != c->slab_off[j + 1] - c->slab_off[j]) throw std::runtime_error("internal: loopback slab sizes");
+    const int64_t tot = n * c->nv;
+    k_halo_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        trace_buf(c, which), c->g.Kt, c->nv, c->h_rrow + c->slab_off[i], c->h_rcol + c->slab_off[i], n,
+        c->h_stage + c->slab_off[j] * c->nv);
+    c->launches++;
+  }
+}
+
 static void fused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
-  Mark mk(c, st, T_TRACE);
-  tensor_launch_traces(c->nd, c->p, c->eq, c->tg, c->line, U, c->Tu[c->cur], st);
+  {
+    Mark mk(c, st, T_TRACE);
+    tensor_launch_traces(c->nd, c->p, c->eq, c->tg, c->line, U, c->Tu[c->cur], st);
+  }
+  if (c->auto_halo) halo_loopback(c, 0, st);
 }
 
 static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, double dt, double* out,
@@ -810,19 +940,28 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
   b.Tu_next = c->Tu[c->cur ^ 1];
   b.Tg = c->Tg;
   if (c->visc) {
-    Mark mk(c, st, T_FA);
-    tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, st);
+    {
+      Mark mk(c, st, T_FA);
+      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, st);
+    }
+    if (c->auto_halo) halo_loopback(c, 1, st);
   }
   {
     Mark mk(c, st, T_FB);
     tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, stage, dt, st);
   }
-  if (stage >= 0) c->cur ^= 1;
+  if (stage >= 0) {
+    c->cur ^= 1;
+    if (c->auto_halo) halo_loopback(c, 0, st);
+  }
 }
 
 static void sfused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
-  Mark mk(c, st, T_STRACE);
-  simplex_launch_traces(c->nd, c->p, c->eq, c->g, c->sops, U, c->Tu[c->cur], st);
+  {
+    Mark mk(c, st, T_STRACE);
+    simplex_launch_traces(c->nd, c->p, c->eq, c->g, c->sops, U, c->Tu[c->cur], st);
+  }
+  if (c->auto_halo) halo_loopback(c, 0, st);
 }
 
 static void sfused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, double dt, double* out,
@@ -838,14 +977,20 @@ static void sfused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, d
   b.Tg = c->Tg;
   b.xm = c->xm;
   if (c->visc) {
-    Mark mk(c, st, T_SA);
-    simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, st);
+    {
+      Mark mk(c, st, T_SA);
+      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, st);
+    }
+    if (c->auto_halo) halo_loopback(c, 1, st);
   }
   {
     Mark mk(c, st, T_SB);
     simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, stage, dt, st);
   }
-  if (stage >= 0) c->cur ^= 1;
+  if (stage >= 0) {
+    c->cur ^= 1;
+    if (c->auto_halo) halo_loopback(c, 0, st);
+  }
 }
 
 typedef void (*ResFn)(sdrt_ctx*, const double*, int, double, double*, double*, cudaStream_t);
@@ -878,6 +1023,10 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->needs_halo && !c->auto_halo) {
+      set_error("unsupported: multi-rank context; use the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
+      return SDRT_E_UNSUPPORTED;
+    }
     if (c->fused) {
       fused_traces(c, d_U, st);
       fused_stage(c, d_U, nullptr, -1, 0.0, d_dUdt, st);
@@ -900,6 +1049,10 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->needs_halo && !c->auto_halo) {
+      set_error("unsupported: multi-rank context; use the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
+      return SDRT_E_UNSUPPORTED;
+    }
     ResFn res = pick_res(c->eq, c->nd);
     if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
     if (c->sfused && nsteps > 0) sfused_traces(c, d_U, st);
@@ -921,6 +1074,133 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
         }
       }
     }
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_halo_info(const sdrt_ctx* c, int* nslab, int* peer, int* d, int* side, int64_t* offset) {
+  if (!c || !nslab) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  *nslab = c->nslab;
+  for (int i = 0; i < c->nslab; ++i) {
+    if (peer) peer[i] = c->slab_peer[i];
+    if (d) d[i] = c->slab_d[i];
+    if (side) side[i] = c->slab_side[i];
+  }
+  if (offset)
+    for (int i = 0; i <= c->nslab; ++i) offset[i] = c->slab_off[i] * c->nv;
+  return SDRT_OK;
+}
+
+sdrt_status sdrt_halo_pack(sdrt_ctx* c, int which, double* d_send, void* stream) {
+  if (!c || (which != 0 && which != 1) || (!d_send && c->needs_halo)) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    halo_pack(c, which, d_send, (cudaStream_t)stream);
+    CUDA_OK(cudaGetLastError());
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_halo_unpack(sdrt_ctx* c, int which, const double* d_recv, void* stream) {
+  if (!c || (which != 0 && which != 1) || (!d_recv && c->needs_halo)) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    halo_unpack(c, which, d_recv, (cudaStream_t)stream);
+    CUDA_OK(cudaGetLastError());
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_stage_traces(sdrt_ctx* c, const double* d_U, void* stream) {
+  if (!c || !d_U || (!c->fused && !c->sfused)) {
+    set_error("invalid argument (staged API needs a fused path)");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    c->launches = 0;
+    bool ah = c->auto_halo;
+    c->auto_halo = false;
+    if (c->fused) fused_traces(c, d_U, (cudaStream_t)stream);
+    else sfused_traces(c, d_U, (cudaStream_t)stream);
+    c->auto_halo = ah;
+    CUDA_OK(cudaGetLastError());
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
+  if (!c || !d_U || stage < -1 || stage > 3 || (!c->fused && !c->sfused)) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (!c->visc) return SDRT_OK;
+  SDRT_TRY({
+    cudaStream_t st = (cudaStream_t)stream;
+    const double* Uin = stage <= 0 ? d_U : c->Us;
+    if (c->fused) {
+      TensorBufs b{};
+      b.Uin = Uin;
+      b.Tu = c->Tu[c->cur];
+      b.Tg = c->Tg;
+      Mark mk(c, st, T_FA);
+      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, st);
+    } else {
+      SimplexBufs b{};
+      b.Uin = Uin;
+      b.Tu = c->Tu[c->cur];
+      b.Tg = c->Tg;
+      b.xm = c->xm;
+      Mark mk(c, st, T_SA);
+      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, st);
+    }
+    CUDA_OK(cudaGetLastError());
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, void* stream) {
+  if (!c || !d_U || stage < -1 || stage > 3 || (stage == -1 && !d_out) || (!c->fused && !c->sfused)) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    cudaStream_t st = (cudaStream_t)stream;
+    const double* Uin = stage <= 0 ? d_U : c->Us;
+    if (c->fused) {
+      TensorBufs b;
+      b.Uin = Uin;
+      b.U = d_U;
+      b.Us = c->Us;
+      b.ACC = c->ACC;
+      b.out = d_out;
+      b.Tu = c->Tu[c->cur];
+      b.Tu_next = c->Tu[c->cur ^ 1];
+      b.Tg = c->Tg;
+      Mark mk(c, st, T_FB);
+      tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, stage, dt, st);
+    } else {
+      SimplexBufs b;
+      b.Uin = Uin;
+      b.U = d_U;
+      b.Us = c->Us;
+      b.ACC = c->ACC;
+      b.out = d_out;
+      b.Tu = c->Tu[c->cur];
+      b.Tu_next = c->Tu[c->cur ^ 1];
+      b.Tg = c->Tg;
+      b.xm = c->xm;
+      Mark mk(c, st, T_SB);
+      simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, stage, dt, st);
+    }
+    if (stage >= 0) c->cur ^= 1;
+    CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })
 }

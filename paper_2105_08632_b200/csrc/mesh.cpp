@@ -213,6 +213,8 @@ Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const doub
           }
       }
       if (found != 1) throw std::runtime_error("face pairing failed");
+      if ((L.off[0] != 0) + (L.off[1] != 0) + (L.off[2] != 0) > 1)
+        throw std::runtime_error("internal: face neighbour differs in more than one pattern axis");
       // left rule O14 from the integer outward normal of this face
       int nrm[3] = {0, 0, 0};
       if (etype_tensor(etype)) {
@@ -285,7 +287,83 @@ Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const doub
       auto n = L.left ? nown[s * r.nfaces + f] : nown[L.nshape * r.nfaces + L.nface];
       for (int q = 0; q < r.nfp; ++q) m.nleft[s * r.next + f * r.nfp + q] = n;
     }
+  build_halo(m, false);
   return m;
+}
+
+void build_halo(Mesh& m, bool force_self_halo) {
+  const RefElement& r = m.ref;
+  const int D = m.nd;
+  m.slabs.clear();
+  int64_t cur = m.K_pad;
+  for (int d = 0; d < 3; ++d) {
+    m.halo[d] = d < D && (m.pgrid[d] > 1 || force_self_halo);
+    for (int side = 0; side < 2; ++side) m.gbase[d][side] = 0;
+  }
+  for (int d = 0; d < D; ++d) {
+    if (!m.halo[d]) continue;
+    int64_t tang = 1;
+    for (int c = 0; c < D; ++c)
+      if (c != d) tang *= m.Nloc[c];
+    for (int side = 0; side < 2; ++side) {
+      m.gbase[d][side] = cur;
+      cur += tang * m.nsub;
+    }
+  }
+  m.Kt = (cur + 31) / 32 * 32;
+  // rank coordinates and peers
+  int rc[3] = {m.rank % m.pgrid[0], (m.rank / m.pgrid[0]) % m.pgrid[1], m.rank / (m.pgrid[0] * m.pgrid[1])};
+  auto rank_of = [&](const int c[3]) { return c[0] + m.pgrid[0] * (c[1] + m.pgrid[1] * c[2]); };
+  for (int d = 0; d < D; ++d) {
+    if (!m.halo[d]) continue;
+    int oth[2], no = 0;
+    for (int c = 0; c < D; ++c)
+      if (c != d) oth[no++] = c;
+    for (int side = 0; side < 2; ++side) {
+      HaloSlab S;
+      S.d = d;
+      S.side = side;
+      int pc[3] = {rc[0], rc[1], rc[2]};
+      pc[d] = (pc[d] + (side ? 1 : -1) + m.pgrid[d]) % m.pgrid[d];
+      S.peer = rank_of(pc);
+      const int dir = side ? 1 : -1;
+      // my boundary layer facing `side`, and my ghost slab on `side` (the peer's layer)
+      const int my_layer = side ? m.Nloc[d] - 1 : 0;
+      int na = no > 0 ? m.Nloc[oth[0]] : 1, nb = no > 1 ? m.Nloc[oth[1]] : 1;
+      for (int tb = 0; tb < nb; ++tb)
+        for (int ta = 0; ta < na; ++ta) {
+          int lc[3] = {0, 0, 0};
+          lc[d] = my_layer;
+          if (no > 0) lc[oth[0]] = ta;
+          if (no > 1) lc[oth[1]] = tb;
+          int64_t lp = lc[0] + (int64_t)m.Nloc[0] * (lc[1] + (int64_t)m.Nloc[1] * lc[2]);
+          int64_t tang = ta + (int64_t)na * tb;
+          for (int s = 0; s < m.nsub; ++s)
+            for (int f = 0; f < r.nfaces; ++f) {
+              const FaceLink& L = m.link[s * r.nfaces + f];
+              bool facing = L.off[d] == dir;
+              for (int c = 0; c < D; ++c)
+                if (c != d && L.off[c] != 0) facing = false;
+              if (facing)
+                for (int q = 0; q < r.nfp; ++q) {
+                  S.send_row.push_back(f * r.nfp + q);
+                  S.send_col.push_back((int32_t)(lp * m.nsub + s));
+                }
+              // the peer's element across MY `side` sends its faces facing -dir;
+              // store them in my ghost column for that element
+              bool facing_back = L.off[d] == -dir;
+              for (int c = 0; c < D; ++c)
+                if (c != d && L.off[c] != 0) facing_back = false;
+              if (facing_back)
+                for (int q = 0; q < r.nfp; ++q) {
+                  S.recv_row.push_back(f * r.nfp + q);
+                  S.recv_col.push_back((int32_t)(m.gbase[d][side] + tang * m.nsub + s));
+                }
+            }
+        }
+      m.slabs.push_back(S);
+    }
+  }
 }
 
 }  // namespace sdrt

@@ -16,6 +16,18 @@ struct FaceLink {
   std::vector<int> perm;  // my face point q -> neighbour face point index
 };
 
+// One halo slab: the ghost layer across local face direction (d, side) of this rank's
+// block.  Entries are (trace row, column) pairs of the trace arrays [N_ext][N_V][Kt];
+// each entry carries N_V values.  send: rows of MY boundary elements facing the peer;
+// recv: the same rows written into MY ghost columns for the peer's elements.  Both
+// lists are in the canonical order (tangential pattern, sub-cell, face, point), so the
+// peer's send list matches my recv list entry by entry.
+struct HaloSlab {
+  int d, side;      // side 0: -d direction, 1: +d direction
+  int peer;         // rank owning the neighbouring block (may be this rank: periodic loopback)
+  std::vector<int32_t> send_row, send_col, recv_row, recv_col;
+};
+
 struct Mesh {
   int etype, p, nd, nsub;
   int Nloc[3], Nglob[3], offset[3];
@@ -32,6 +44,11 @@ struct Mesh {
   // per (shape, ext point)
   std::vector<double> sscale;                   // detJ |J^-T n~|
   std::vector<std::array<double, 3>> nleft;     // canonical (left element's) unit normal
+  // halo (multi-rank / loopback): ghost columns after K_pad in the trace arrays
+  int halo[3] = {0, 0, 0};                      // axis uses ghost slabs
+  int64_t Kt = 0;                               // trace row stride = K_pad + ghosts (padded)
+  int64_t gbase[3][2] = {{0, 0}, {0, 0}, {0, 0}};  // first ghost column of slab (d, side)
+  std::vector<HaloSlab> slabs;
 
   int64_t pattern_of(int64_t e) const { return e / nsub; }
   // global pattern coords of local element e
@@ -41,5 +58,8 @@ struct Mesh {
 
 Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const double hi[3], int rank,
                 int nranks, const int pgrid[3]);
+// (Re)build the ghost layout and halo lists; force_self_halo routes periodic wraps of
+// single-rank axes through the halo path as well (loopback testing on one device).
+void build_halo(Mesh& m, bool force_self_halo);
 
 }  // namespace sdrt

@@ -158,6 +158,12 @@ __device__ __forceinline__ int snbr(const GeomDev& g, int64_t e, int s, int f) {
   for (int d = 0; d < 3; ++d)
     if (d < g.nd) {
       int cc = c[d] + g.off[s][f][d];
+      if ((cc < 0 || cc >= g.Nloc[d]) && g.halo[d]) {
+        // ghost column: slab (d, side), tangential pattern index, neighbour sub-cell
+        const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
+        const int64_t tang = g.nd == 2 ? c[a] : c[a] + (int64_t)g.Nloc[a] * c[bb];
+        return (int)(g.gbase[d][cc < 0 ? 0 : 1] + tang * g.nsub + g.nshape[s][f]);
+      }
       cc = cc < 0 ? cc + g.Nloc[d] : (cc >= g.Nloc[d] ? cc - g.Nloc[d] : cc);
       id += mul * cc;
       mul *= g.Nloc[d];
@@ -171,7 +177,7 @@ __device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& p
                                               const double* sUe, const int (*sNb)[E], double* sC, int64_t e0) {
   using S = SDims<D, P>;
   const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
-  const int Kp = (int)g.Kp;
+  const int Kp = (int)g.Kt;  // trace row stride
   for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
   const int64_t e0 = (int64_t)blockIdx.x * E;
   sload<SDims<D, P>::nsol * NV, E>(U, smem, e0, g.Kp);
   __syncthreads();
-  strace_global<NV, E>(O.M0, smem, T, e0, g.K, g.Kp);
+  strace_global<NV, E>(O.M0, smem, T, e0, g.K, g.Kt);
 }
 
 template <int D, int P, int EQ, int E>
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(256) ks_grad(GeomDev g, SimplexOps O, PhysDev 
   const double* sUe = smem + Ly::U * E;
   const double* sQ = smem + (Ly::U + Ly::UE + Ly::R0 + Ly::UU) * E;
   const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
-  const int Kp = (int)g.Kp;
+  const int Kp = (int)g.Kt;  // trace row stride
   for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
@@ -323,7 +329,7 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
   double* sR0 = sUe + Ly::UE * E;
   double* sUu = sR0 + Ly::R0 * E;
   double* sQ = sUu + Ly::UU * E;
-  const int Kp = (int)g.Kp;
+  const int Kp = (int)g.Kt;  // trace row stride
   if constexpr (Ph::VISC) {
     // Q_u = M18 Q (M12 on each of the D*NV gradient rows), into region 0 (C is dead)
     sapply<D * NV, E, false>(O.M12, sQ, 1 << 30, sQ, sR0);
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
   }
   if (stage < 0) return;
   __syncthreads();
-  strace_global<NV, E>(O.M0, sU, b.Tu_next, e0, g.K, g.Kp);
+  strace_global<NV, E>(O.M0, sU, b.Tu_next, e0, g.K, g.Kt);
 }
 
 // ------------------------------------------------------------------ launchers

@@ -61,6 +61,12 @@ __device__ __forceinline__ int64_t tnbr(const TensorGeom& g, int64_t e, int d, i
   r /= g.N[1];
   c[2] = (int)r;
   int v = c[d] + delta;
+  if ((v < 0 || v >= g.N[d]) && g.halo[d]) {
+    // ghost column of the neighbouring rank's element: slab (d, side), tangential index
+    const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
+    const int64_t tang = D == 2 ? c[a] : c[a] + (int64_t)g.N[a] * c[bb];
+    return g.gbase[d][v < 0 ? 0 : 1] + tang;
+  }
   v = v < 0 ? v + g.N[d] : (v >= g.N[d] ? v - g.N[d] : v);
   c[d] = v;
   return (int64_t)c[0] + (int64_t)g.N[0] * (c[1] + (int64_t)g.N[1] * c[2]);
@@ -112,8 +118,8 @@ __device__ __forceinline__ void prefetch_traces(const TensorGeom& g, const doubl
     // the neighbour across face (d, side) reads its opposite face (d, 1-side)
     const int ext_n = (2 * d + 1 - side) * NL + ext % NL;
     const int64_t m = tnbr<D>(g, e0, d, side ? 1 : -1);
-    prefetch_l2(T + ((int64_t)ext_n * NV + v) * g.Kp + m);
-    if (own) prefetch_l2(T + ((int64_t)ext * NV + v) * g.Kp + e0);
+    prefetch_l2(T + ((int64_t)ext_n * NV + v) * g.Kt + m);
+    if (own) prefetch_l2(T + ((int64_t)ext * NV + v) * g.Kt + e0);
   }
 }
 
@@ -143,8 +149,8 @@ __device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D
     double nbl[NV], nbh[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      nbl[v] = Tu[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kp + mlo];
-      nbh[v] = Tu[((int64_t)((2 * d + 0) * NL + t) * NV + v) * g.Kp + mhi];
+      nbl[v] = Tu[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kt + mlo];
+      nbh[v] = Tu[((int64_t)((2 * d + 0) * NL + t) * NV + v) * g.Kt + mhi];
     }
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
@@ -195,7 +201,7 @@ __device__ __forceinline__ void write_traces(const TensorGeom& g, const Line1D& 
       double u[n];
 #pragma unroll
       for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
-      T[((int64_t)ext * NV + v) * g.Kp + e] = interp_end<n>(L.Iend[side], u);
+      T[((int64_t)ext * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[side], u);
     }
   }
 }
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(256) kt_grad(TensorGeom g, Line1D L, PhysDev p
     double gv[NV];
     Ph::visc_dir(ph, u, q, nL, gv);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)ext * NV + v) * g.Kp + e] = gv[v];
+    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)ext * NV + v) * g.Kt + e] = gv[v];
   }
 }
 
@@ -298,7 +304,7 @@ __global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev 
     sNb[k][el] = e < g.K ? (int)tnbr<D>(g, e, k / 2, (k % 2) ? 1 : -1) : 0;
   }
   __syncthreads();
-  const int Kp = (int)g.Kp;
+  const int Kp = (int)g.Kt;  // trace row stride
   // one code copy for all directions (runtime d): keeps the kernel inside the I-cache
 #pragma unroll 1
   for (int d = 0; d < D; ++d) {

@@ -24,8 +24,11 @@ struct Line1D {
 };
 
 struct TensorGeom {
-  int N[3];           // patterns per axis (periodic)
+  int N[3];           // local patterns per axis
   int64_t K, Kp;
+  int64_t Kt;         // trace row stride (K_pad + ghost columns)
+  int halo[3];        // axis d exchanges through ghost slabs (multi-rank / loopback)
+  int64_t gbase[3][2];  // first ghost column of slab (d, side)
   double jinv[3];     // 2 / h_d  (J^-T = diag)
   double detJ;        // prod h_d / 2
   double sface[3];    // detJ * 2 / h_d  (= detJ |J^-T n~| on faces normal to d)

@@ -37,7 +37,7 @@ class MeshInfo(ctypes.Structure):
                 ("nu", ctypes.c_int), ("nfaces", ctypes.c_int), ("nfp", ctypes.c_int),
                 ("nsub", ctypes.c_int), ("N", ctypes.c_int * 3), ("Nglobal", ctypes.c_int * 3),
                 ("offset", ctypes.c_int * 3), ("K", ctypes.c_int64), ("K_pad", ctypes.c_int64),
-                ("n_faces", ctypes.c_int64)]
+                ("n_faces", ctypes.c_int64), ("K_trace", ctypes.c_int64)]
 
 
 class PhysicsT(ctypes.Structure):
@@ -69,6 +69,15 @@ lib.sdrt_ctx_workspace_bytes.restype = ctypes.c_size_t
 lib.sdrt_ctx_create.argtypes = [_vp, _vp, ctypes.POINTER(PhysicsT), _vp, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)]
 lib.sdrt_residual.argtypes = [_vp, _vp, _vp, _vp]
 lib.sdrt_rk_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
+lib.sdrt_mesh_set_halo.argtypes = [_vp, ctypes.c_int]
+lib.sdrt_mesh_halo_lists.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+lib.sdrt_mesh_neighbor.argtypes = [_vp, ctypes.c_int64, ctypes.c_int, _vp, _vp]
+lib.sdrt_halo_info.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+lib.sdrt_halo_pack.argtypes = [_vp, ctypes.c_int, _vp, _vp]
+lib.sdrt_halo_unpack.argtypes = [_vp, ctypes.c_int, _vp, _vp]
+lib.sdrt_stage_traces.argtypes = [_vp, _vp, _vp]
+lib.sdrt_stage_grad.argtypes = [_vp, _vp, ctypes.c_int, _vp]
+lib.sdrt_stage_flux.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_double, _vp, _vp]
 lib.sdrt_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_ctx_kernel_times.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_int)]
 lib.sdrt_ctx_last_launches.argtypes = [_vp]
@@ -80,7 +89,9 @@ EXPORTED = ["sdrt_abi_version", "sdrt_last_error", "sdrt_mesh_create", "sdrt_mes
             "sdrt_mesh_export_maps", "sdrt_mesh_sol_coords", "sdrt_mesh_detj", "sdrt_mesh_destroy",
             "sdrt_operators_build", "sdrt_operators_get", "sdrt_operators_destroy",
             "sdrt_ctx_workspace_bytes", "sdrt_ctx_create", "sdrt_residual", "sdrt_rk_step",
-            "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_kernel_times"]
+            "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_kernel_times",
+            "sdrt_mesh_set_halo", "sdrt_mesh_halo_lists", "sdrt_mesh_neighbor", "sdrt_halo_info",
+            "sdrt_halo_pack", "sdrt_halo_unpack", "sdrt_stage_traces", "sdrt_stage_grad", "sdrt_stage_flux"]
 
 
 def _check(code):
@@ -143,6 +154,32 @@ def mesh_detj(m):
     x = np.zeros(info["K"])
     _check(lib.sdrt_mesh_detj(m, x.ctypes.data))
     return x
+
+
+def mesh_set_halo(m, force_self_halo):
+    _check(lib.sdrt_mesh_set_halo(m, int(bool(force_self_halo))))
+
+
+def mesh_halo_lists(m):
+    """[(peer, d, side, send_row, send_col, recv_row, recv_col)] per slab (numpy int32)."""
+    cnt = ctypes.c_int64()
+    _check(lib.sdrt_mesh_halo_lists(m, -1, None, None, None, ctypes.byref(cnt), None, None, None, None))
+    out = []
+    for i in range(cnt.value):
+        peer, d, side, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+        _check(lib.sdrt_mesh_halo_lists(m, i, ctypes.byref(peer), ctypes.byref(d), ctypes.byref(side),
+                                        ctypes.byref(n), None, None, None, None))
+        a = [np.zeros(n.value, dtype=np.int32) for _ in range(4)]
+        _check(lib.sdrt_mesh_halo_lists(m, i, None, None, None, ctypes.byref(n), *[x.ctypes.data for x in a]))
+        out.append((peer.value, d.value, side.value, *a))
+    return out
+
+
+def mesh_neighbor(m, e, f):
+    """(trace column, neighbour local face) the kernels use across face f of local element e."""
+    col, face = ctypes.c_int64(), ctypes.c_int()
+    _check(lib.sdrt_mesh_neighbor(m, int(e), int(f), ctypes.byref(col), ctypes.byref(face)))
+    return col.value, face.value
 
 
 def mesh_destroy(m):
@@ -211,6 +248,35 @@ def ctx_kernel_times(ctx, max_tags=32):
         if cnt[t]:
             out[nm] = (float(ms[t]), int(cnt[t]))
     return out
+
+
+def halo_info(ctx):
+    n = ctypes.c_int()
+    peer, d, side = (ctypes.c_int * 6)(), (ctypes.c_int * 6)(), (ctypes.c_int * 6)()
+    off = (ctypes.c_int64 * 7)()
+    _check(lib.sdrt_halo_info(ctx, ctypes.byref(n), peer, d, side, off))
+    k = n.value
+    return list(peer[:k]), list(d[:k]), list(side[:k]), list(off[:k + 1])
+
+
+def halo_pack(ctx, which, send_ptr, stream):
+    _check(lib.sdrt_halo_pack(ctx, int(which), _vp(send_ptr), _vp(stream)))
+
+
+def halo_unpack(ctx, which, recv_ptr, stream):
+    _check(lib.sdrt_halo_unpack(ctx, int(which), _vp(recv_ptr), _vp(stream)))
+
+
+def stage_traces(ctx, U_ptr, stream):
+    _check(lib.sdrt_stage_traces(ctx, _vp(U_ptr), _vp(stream)))
+
+
+def stage_grad(ctx, U_ptr, stage, stream):
+    _check(lib.sdrt_stage_grad(ctx, _vp(U_ptr), int(stage), _vp(stream)))
+
+
+def stage_flux(ctx, U_ptr, stage, dt, out_ptr, stream):
+    _check(lib.sdrt_stage_flux(ctx, _vp(U_ptr), int(stage), float(dt), _vp(out_ptr), _vp(stream)))
 
 
 def ctx_last_launches(ctx):

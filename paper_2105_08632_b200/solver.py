@@ -12,14 +12,20 @@ from . import sdrt
 
 
 class Solver:
-    def __init__(self, etype, p, N, lo, hi, eq, device="cuda", rank=0, nranks=1, pgrid=None, **phys):
+    def __init__(self, etype, p, N, lo, hi, eq, device="cuda", rank=0, nranks=1, pgrid=None, _pre_ctx=None,
+                 force_self_halo=False, **phys):
         D = 2 if etype in ("quad", "tri") else 3
         Nl = list(N) if np.ndim(N) else [int(N)] * D
         self.mesh = sdrt.mesh_create(etype, p, Nl, lo, hi, rank=rank, nranks=nranks, pgrid=pgrid)
+        if _pre_ctx is not None:
+            _pre_ctx(self.mesh)
+        elif force_self_halo:
+            sdrt.mesh_set_halo(self.mesh, True)   # loopback halo: the library exchanges itself
         self.ops = sdrt.operators_build(etype, p)
         self.info = sdrt.mesh_info(self.mesh)
         self.phys = sdrt.physics(eq, **phys)
         self.nv = 1 if eq in ("linadv", "linadvdiff") else D + 2
+        self.visc = eq in ("linadvdiff", "ns")
         self.device = torch.device(device)
         nbytes = sdrt.ctx_workspace_bytes(self.mesh, self.ops, self.phys)
         if nbytes == 0:
