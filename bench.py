@@ -77,7 +77,7 @@ def kernel_bytes(cfg, K):
     D, ns, ne, nu = dims(cfg)
     V = cfg.nvars
     b = 8 * V * K
-    return {
+    out = {
         "interp_ext(M0)": b * (ns + ne),
         "interp_int(M12)": b * (ns + nu),
         "common_value": b * (2 * ne + ne),
@@ -94,6 +94,12 @@ def kernel_bytes(cfg, K):
         "tensor_grad(A)": b * (ns + ne + (ne // 2 if abs(cfg.beta) == 0.5 else ne)),
         "tensor_stage(B)": b * (ns + 3 * ns + ne + (ne if cfg.eq in ("ns", "linadvdiff") else 0) + ne),
     }
+    # fused simplex path: the same data flow per element (traces of the neighbours,
+    # published viscous traces of the LDG-weighted side, RK registers, new traces)
+    out["simplex_traces"] = out["tensor_traces"]
+    out["simplex_grad(A)"] = out["tensor_grad(A)"]
+    out["simplex_stage(B)"] = out["tensor_stage(B)"]
+    return out
 
 
 def stage_model_bytes(cfg):

@@ -7,12 +7,13 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "libsdrt.so")
-BUILD = os.path.join(HERE, "build")
+PROF = os.environ.get("SDRT_PHASE_PROF") == "1"  # tools-only phase-cycle build
+OUT = os.path.join(HERE, "libsdrt_prof.so" if PROF else "libsdrt.so")
+BUILD = os.path.join(HERE, "build_prof" if PROF else "build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-              "-Xptxas", "-v"]
+              "-Xptxas", "-v"] + (["-DSDRT_PHASE_PROF"] if PROF else [])
 CXX_FLAGS = ["-O2", "-std=gnu++17", "-fPIC", "-Wall"]
 
 

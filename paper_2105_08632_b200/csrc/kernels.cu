@@ -378,6 +378,7 @@ struct sdrt_ctx {
   int etype = 0, p = 0;
   TensorGeom tg;
   Line1D line;
+  TensorTma tma;
   double* Tu[2] = {nullptr, nullptr};
   double* Tg = nullptr;
   int cur = 0;
@@ -697,6 +698,7 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         L.Dfl[i][m.p + 1] = O.M14(i, 1 * r.nfp + 0);
         for (int a = 0; a < m.p; ++a) L.Dfl[i][a + 1] = O.M13(i, a);
       }
+      tensor_tma_init(&c->tma, m.nd, m.p, ph->eq, m.K_pad);
       c->Tu[0] = (double*)(base + p.off_tu0);
       c->Tu[1] = (double*)(base + p.off_tu1);
       c->Tg = (double*)(base + p.off_tg);
@@ -923,7 +925,7 @@ static void halo_loopback(sdrt_ctx* c, int which, cudaStream_t st) {
 static void fused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
   {
     Mark mk(c, st, T_TRACE);
-    tensor_launch_traces(c->nd, c->p, c->eq, c->tg, c->line, U, c->Tu[c->cur], st);
+    tensor_launch_traces(c->nd, c->p, c->eq, c->tg, c->line, &c->tma, U, c->Tu[c->cur], st);
   }
   if (c->auto_halo) halo_loopback(c, 0, st);
 }
@@ -939,16 +941,17 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
   b.Tu = c->Tu[c->cur];
   b.Tu_next = c->Tu[c->cur ^ 1];
   b.Tg = c->Tg;
+  b.Rv = c->R;
   if (c->visc) {
     {
       Mark mk(c, st, T_FA);
-      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, st);
+      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, st);
     }
     if (c->auto_halo) halo_loopback(c, 1, st);
   }
   {
     Mark mk(c, st, T_FB);
-    tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, stage, dt, st);
+    tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, stage, dt, st);
   }
   if (stage >= 0) {
     c->cur ^= 1;
@@ -1149,8 +1152,9 @@ sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
       b.Uin = Uin;
       b.Tu = c->Tu[c->cur];
       b.Tg = c->Tg;
+      b.Rv = c->R;
       Mark mk(c, st, T_FA);
-      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, st);
+      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, st);
     } else {
       SimplexBufs b{};
       b.Uin = Uin;
@@ -1183,8 +1187,9 @@ sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, doub
       b.Tu = c->Tu[c->cur];
       b.Tu_next = c->Tu[c->cur ^ 1];
       b.Tg = c->Tg;
+      b.Rv = c->R;
       Mark mk(c, st, T_FB);
-      tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, b, stage, dt, st);
+      tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, stage, dt, st);
     } else {
       SimplexBufs b;
       b.Uin = Uin;

@@ -49,44 +49,44 @@ struct SLayout {
 };
 
 // Y[r][w][el] (+)= sum_c M[r][c] X[c][w][el], X rows c < split from X0, else X1.
-// W values per row, processed in chunks of up to 5.
+// W values per row in chunks of WC; one work item = (row block, chunk, element), so
+// every thread of the CTA has work even for short operators.
 template <int W, int E, bool ACCUM>
 __device__ __forceinline__ void sapply(const SOp& M, const double* X0, int split, const double* X1, double* Y) {
   constexpr int WC = W % 5 == 0 ? 5 : (W % 4 == 0 ? 4 : (W % 3 == 0 ? 3 : (W % 2 == 0 ? 2 : 1)));
-  const int nitems = M.nblk * E;
+  constexpr int NWC = W / WC;
+  const int nitems = M.nblk * NWC * E;
   for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
-    const int el = item % E, blk = item / E;
-#pragma unroll 1
-    for (int w0 = 0; w0 < W; w0 += WC) {
-      double acc[SRB][WC];
+    const int el = item % E, r2 = item / E;
+    const int w0 = (r2 % NWC) * WC, blk = r2 / NWC;
+    double acc[SRB][WC];
 #pragma unroll
-      for (int k = 0; k < SRB; ++k)
+    for (int k = 0; k < SRB; ++k)
 #pragma unroll
-        for (int w = 0; w < WC; ++w) acc[k][w] = 0.0;
-      const int b = M.ptr[blk], e = M.ptr[blk + 1];
-      for (int j = b; j < e; ++j) {
-        const int c = __ldg(M.col + j);
-        const double* xr = (c < split ? X0 + c * W * E : X1 + (c - split) * W * E) + w0 * E + el;
-        double x[WC];
+      for (int w = 0; w < WC; ++w) acc[k][w] = 0.0;
+    const int b = M.ptr[blk], e = M.ptr[blk + 1];
+    for (int j = b; j < e; ++j) {
+      const int c = __ldg(M.col + j);
+      const double* xr = (c < split ? X0 + c * W * E : X1 + (c - split) * W * E) + w0 * E + el;
+      double x[WC];
 #pragma unroll
-        for (int w = 0; w < WC; ++w) x[w] = xr[w * E];
-        const double* mv = M.val + (int64_t)j * SRB;
-#pragma unroll
-        for (int k = 0; k < SRB; ++k) {
-          const double m = __ldg(mv + k);
-#pragma unroll
-          for (int w = 0; w < WC; ++w) acc[k][w] = __fma_rn(m, x[w], acc[k][w]);
-        }
-      }
+      for (int w = 0; w < WC; ++w) x[w] = xr[w * E];
+      const double* mv = M.val + (int64_t)j * SRB;
 #pragma unroll
       for (int k = 0; k < SRB; ++k) {
-        const int r = blk * SRB + k;
-        if (r >= M.rows) break;
+        const double m = __ldg(mv + k);
 #pragma unroll
-        for (int w = 0; w < WC; ++w) {
-          double* y = Y + (r * W + w0 + w) * E + el;
-          *y = ACCUM ? *y + acc[k][w] : acc[k][w];
-        }
+        for (int w = 0; w < WC; ++w) acc[k][w] = __fma_rn(m, x[w], acc[k][w]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < SRB; ++k) {
+      const int r = blk * SRB + k;
+      if (r >= M.rows) break;
+#pragma unroll
+      for (int w = 0; w < WC; ++w) {
+        double* y = Y + (r * W + w0 + w) * E + el;
+        *y = ACCUM ? *y + acc[k][w] : acc[k][w];
       }
     }
   }
@@ -144,8 +144,8 @@ __device__ __forceinline__ void sload(const double* __restrict__ src, double* s,
 }
 
 // neighbour of element e across local face f (pattern arithmetic, periodic)
-__device__ __forceinline__ int snbr(const GeomDev& g, int64_t e, int s, int f) {
-  int64_t pat = e / g.nsub;
+__device__ __forceinline__ int snbr(const GeomDev& g, int e, int s, int f) {
+  int pat = e / g.nsub;
   int c[3] = {0, 0, 0};
 #pragma unroll
   for (int d = 0; d < 3; ++d)
@@ -153,7 +153,7 @@ __device__ __forceinline__ int snbr(const GeomDev& g, int64_t e, int s, int f) {
       c[d] = (int)(pat % g.Nloc[d]);
       pat /= g.Nloc[d];
     }
-  int64_t id = 0, mul = 1;
+  int id = 0, mul = 1;
 #pragma unroll
   for (int d = 0; d < 3; ++d)
     if (d < g.nd) {
@@ -161,8 +161,8 @@ __device__ __forceinline__ int snbr(const GeomDev& g, int64_t e, int s, int f) {
       if ((cc < 0 || cc >= g.Nloc[d]) && g.halo[d]) {
         // ghost column: slab (d, side), tangential pattern index, neighbour sub-cell
         const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
-        const int64_t tang = g.nd == 2 ? c[a] : c[a] + (int64_t)g.Nloc[a] * c[bb];
-        return (int)(g.gbase[d][cc < 0 ? 0 : 1] + tang * g.nsub + g.nshape[s][f]);
+        const int tang = g.nd == 2 ? c[a] : c[a] + g.Nloc[a] * c[bb];
+        return (int)g.gbase[d][cc < 0 ? 0 : 1] + tang * g.nsub + g.nshape[s][f];
       }
       cc = cc < 0 ? cc + g.Nloc[d] : (cc >= g.Nloc[d] ? cc - g.Nloc[d] : cc);
       id += mul * cc;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& p
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
-    const int s = (int)(e % g.nsub), f = rho / S::nfp, q = rho % S::nfp;
+    const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
     const int m = sNb[f][el];
     const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
     const bool left = g.left[s][f];
@@ -200,12 +200,11 @@ __device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& p
 
 // Q = J^-T Q~ in place on sQ [nsol][D][NV][E]
 template <int D, int P, int NV, int E>
-__device__ __forceinline__ void metric_grad(const GeomDev& g, double* sQ, int64_t e0) {
+__device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E], double* sQ) {
   using S = SDims<D, P>;
   for (int item = threadIdx.x; item < S::nsol * E; item += blockDim.x) {
     const int el = item % E, sp = item / E;
-    const int64_t e = e0 + el;
-    const int s = (int)(e % g.nsub);
+    const int s = sNb[D + 1][el];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double qt[D];
@@ -222,12 +221,14 @@ __device__ __forceinline__ void metric_grad(const GeomDev& g, double* sQ, int64_
   }
 }
 
+// neighbour ids sNb[f][el] and sub-cell shapes sNb[D+1][el] of a tile, once
 template <int D, int E>
 __device__ __forceinline__ void fill_neighbours(const GeomDev& g, int (*sNb)[E], int64_t e0) {
-  for (int idx = threadIdx.x; idx < (D + 1) * E; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < (D + 2) * E; idx += blockDim.x) {
     const int el = idx % E, f = idx / E;
-    const int64_t e = e0 + el;
-    sNb[f][el] = e < g.K ? snbr(g, e, (int)(e % g.nsub), f) : 0;
+    const int e = (int)e0 + el;
+    const int s = e % g.nsub;
+    sNb[f][el] = f == D + 1 ? s : (e < g.K ? snbr(g, e, s, f) : 0);
   }
 }
 
@@ -256,7 +257,7 @@ __device__ __forceinline__ void prologue(const GeomDev& g, const SimplexOps& O, 
     __syncthreads();
     sapply<NV, E, false>(O.G, sR0, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
     __syncthreads();
-    metric_grad<D, P, NV, E>(g, sQ, e0);
+    metric_grad<D, P, NV, E>(g, sNb, sQ);
     __syncthreads();
   }
 }
@@ -279,37 +280,54 @@ __global__ void __launch_bounds__(256) ks_grad(GeomDev g, SimplexOps O, PhysDev 
   using Ly = SLayout<D, P, Ph::NV, Ph::VISC>;
   constexpr int NV = Ph::NV;
   extern __shared__ double smem[];
-  __shared__ int sNb[D + 1][E];
+  __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
   const int64_t e0 = (int64_t)blockIdx.x * E;
   prologue<D, P, EQ, E>(g, O, ph, b.Uin, b.Tu, smem, sNb, e0);
   const double* sUe = smem + Ly::U * E;
   const double* sQ = smem + (Ly::U + Ly::UE + Ly::R0 + Ly::UU) * E;
   const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
   const int Kp = (int)g.Kt;  // trace row stride
-  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
-    const int el = item % E, rho = item / E;
+  // RP face points per item (same face): the gradient tile entries loaded for one
+  // point serve RP rows of M0
+  constexpr int RP = S::nfp % 2 == 0 ? 2 : 1;
+  for (int item = threadIdx.x; item < (S::next / RP) * E; item += blockDim.x) {
+    const int el = item % E, rho0 = (item / E) * RP;
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
-    const int s = (int)(e % g.nsub), f = rho / S::nfp;
+    const int s = sNb[D + 1][el], f = rho0 / S::nfp;
     const bool left = g.left[s][f];
     if ((left && !pub_left) || (!left && !pub_right)) continue;
-    double u[NV], q[D * NV];
+    double q[RP][D * NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
+    for (int r = 0; r < RP; ++r)
 #pragma unroll
-    for (int k = 0; k < D * NV; ++k) q[k] = 0.0;
-    const double* m0 = O.M0dense + rho * S::nsol;
+      for (int k = 0; k < D * NV; ++k) q[r][k] = 0.0;
+    const double* m0 = O.M0dense + rho0 * S::nsol;
+#pragma unroll 2
     for (int sp = 0; sp < S::nsol; ++sp) {
-      const double m = __ldg(m0 + sp);
+      double m[RP];
 #pragma unroll
-      for (int k = 0; k < D * NV; ++k) q[k] = fma(m, sQ[(sp * D * NV + k) * E + el], q[k]);
+      for (int r = 0; r < RP; ++r) m[r] = __ldg(m0 + r * S::nsol + sp);
+#pragma unroll
+      for (int k = 0; k < D * NV; ++k) {
+        const double x = sQ[(sp * D * NV + k) * E + el];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) q[r][k] = fma(m[r], x, q[r][k]);
+      }
     }
-    const ExtMetric mt = b.xm[s * S::next + rho];
-    const double nl[3] = {mt.n0, mt.n1, mt.n2};
-    double gv[NV];
-    Ph::visc_dir(ph, u, q, nl, gv);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
+    for (int r = 0; r < RP; ++r) {
+      const int rho = rho0 + r;
+      double u[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
+      const ExtMetric mt = b.xm[s * S::next + rho];
+      const double nl[3] = {mt.n0, mt.n1, mt.n2};
+      double gv[NV];
+      Ph::visc_dir(ph, u, q[r], nl, gv);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
+    }
   }
 }
 
@@ -321,7 +339,7 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
   using Ly = SLayout<D, P, Ph::NV, Ph::VISC>;
   constexpr int NV = Ph::NV;
   extern __shared__ double smem[];
-  __shared__ int sNb[D + 1][E];
+  __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
   const int64_t e0 = (int64_t)blockIdx.x * E;
   prologue<D, P, EQ, E>(g, O, ph, b.Uin, b.Tu, smem, sNb, e0);
   double* sU = smem;
@@ -339,8 +357,7 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
   double* sF = sQ;  // [D][nu][NV][E]
   for (int item = threadIdx.x; item < S::nu * E; item += blockDim.x) {
     const int el = item % E, u = item / E;
-    const int64_t e = e0 + el;
-    const int s = (int)(e % g.nsub);
+    const int s = sNb[D + 1][el];
     double uu[NV], qq[Ph::VISC ? D * NV : 1];
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = sUu[(u * NV + v) * E + el];
@@ -373,7 +390,7 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
-    const int s = (int)(e % g.nsub), f = rho / S::nfp, q = rho % S::nfp;
+    const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
     const int m = sNb[f][el];
     const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
     const bool left = g.left[s][f];
@@ -441,7 +458,7 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
       if (!ok[k]) continue;
       const int idx = base0 + k * nth;
       const int el = idx % E;
-      const int s = (int)((e0 + el) % g.nsub);
+      const int s = sNb[D + 1][el];
       const double kk = -sR0[idx] / g.detJ[s];
       double nu;
       switch (stage) {

@@ -24,12 +24,29 @@
 // bitwise (O28).
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
 #include "tensor.cuh"
 
 namespace sdrt {
+
+// Optional per-phase cycle accounting (build with -DSDRT_PHASE_PROF; tools only):
+// thread 0 of every CTA adds the clock64() time of each phase after its barrier.
+#ifdef SDRT_PHASE_PROF
+__device__ unsigned long long g_phase_cycles[2][16];
+#define PH_INIT long long ph_t0 = clock64();
+#define PH(kern, k)                                                           \
+  if (threadIdx.x == 0) {                                                     \
+    const long long ph_t1 = clock64();                                        \
+    atomicAdd(&g_phase_cycles[kern][k], (unsigned long long)(ph_t1 - ph_t0)); \
+    ph_t0 = ph_t1;                                                            \
+  }
+#else
+#define PH_INIT
+#define PH(kern, k)
+#endif
 
 template <int D, int P>
 struct TDims {
@@ -39,37 +56,48 @@ struct TDims {
   static constexpr int NEXT = 2 * D * NL;
 };
 
+// first point index and point stride of line t along direction d
 template <int D, int P>
-__device__ __forceinline__ int sidx(int d, int t, int i) {
+__device__ __forceinline__ int lbase(int d, int t) {
   constexpr int n = P + 1;
-  if constexpr (D == 2) {
-    return d == 0 ? i + n * t : t + n * i;
-  } else {
-    const int ta = t % n, tb = t / n;
-    return d == 0 ? i + n * (ta + n * tb) : (d == 1 ? ta + n * (i + n * tb) : ta + n * (tb + n * i));
-  }
+  if constexpr (D == 2) return d == 0 ? n * t : t;
+  return d == 0 ? n * t : (d == 1 ? (t % n) + n * n * (t / n) : t);
+}
+template <int D, int P>
+__device__ __forceinline__ int lstr(int d) {
+  constexpr int n = P + 1;
+  return d == 0 ? 1 : (d == 1 ? n : n * n);
 }
 
-// neighbour element along axis d (delta = -1 / +1), periodic pattern grid, N_p = 1
+// neighbour element along axis d (delta = -1 / +1), periodic pattern grid, N_p = 1.
+// 32-bit arithmetic (K < 2^31); evaluated once per tile element (fill_nbrs).
 template <int D>
-__device__ __forceinline__ int64_t tnbr(const TensorGeom& g, int64_t e, int d, int delta) {
+__device__ __forceinline__ int tnbr(const TensorGeom& g, int e, int d, int delta) {
   int c[3];
-  int64_t r = e;
-  c[0] = (int)(r % g.N[0]);
-  r /= g.N[0];
-  c[1] = (int)(r % g.N[1]);
-  r /= g.N[1];
-  c[2] = (int)r;
+  c[0] = e % g.N[0];
+  const int r = e / g.N[0];
+  c[1] = D == 2 ? r : r % g.N[1];
+  c[2] = D == 2 ? 0 : r / g.N[1];
   int v = c[d] + delta;
   if ((v < 0 || v >= g.N[d]) && g.halo[d]) {
     // ghost column of the neighbouring rank's element: slab (d, side), tangential index
     const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
-    const int64_t tang = D == 2 ? c[a] : c[a] + (int64_t)g.N[a] * c[bb];
-    return g.gbase[d][v < 0 ? 0 : 1] + tang;
+    const int tang = D == 2 ? c[a] : c[a] + g.N[a] * c[bb];
+    return (int)g.gbase[d][v < 0 ? 0 : 1] + tang;
   }
   v = v < 0 ? v + g.N[d] : (v >= g.N[d] ? v - g.N[d] : v);
   c[d] = v;
-  return (int64_t)c[0] + (int64_t)g.N[0] * (c[1] + (int64_t)g.N[1] * c[2]);
+  return c[0] + g.N[0] * (c[1] + g.N[1] * c[2]);
+}
+
+// neighbour ids of a tile's elements: sNb[2d + side][el] (side 0: x_d - 1, 1: x_d + 1)
+template <int D, int E>
+__device__ __forceinline__ void fill_nbrs(const TensorGeom& g, int (*sNb)[E], int64_t e0) {
+  for (int idx = threadIdx.x; idx < 2 * D * E; idx += blockDim.x) {
+    const int el = idx % E, k = idx / E;
+    const int e = (int)e0 + el;
+    sNb[k][el] = e < g.K ? tnbr<D>(g, e, k / 2, (k % 2) ? 1 : -1) : 0;
+  }
 }
 
 // value at a line end: explicit fma chain in fixed order (bit-identical wherever used)
@@ -79,6 +107,54 @@ __device__ __forceinline__ double interp_end(const double (&Iend)[TMAXP + 1], co
 #pragma unroll
   for (int i = 0; i < n; ++i) acc = __fma_rn(Iend[i], u[i], acc);
   return acc;
+}
+
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers ------------------------------
+struct TileMaps {
+  CUtensorMap uin, un, acc, rv;  // stage input, u_n, RK accumulator, R_int
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// 2-D tile {E columns (elements), box rows} at (x = first element, y = first row)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// rows per TMA box: the largest divisor of the row count that is <= 256
+__host__ __device__ constexpr int tma_box_rows(int rows) {
+  int b = rows < 256 ? rows : 256;
+  while (rows % b) --b;
+  return b;
+}
+
+// whole tile [ROWS][E] of one array, issued by one thread, completing on bar
+template <int ROWS, int E>
+__device__ __forceinline__ void tma_tile(double* dst, const CUtensorMap* map, int64_t e0, uint64_t* bar) {
+  constexpr int BR = tma_box_rows(ROWS);
+#pragma unroll
+  for (int r = 0; r < ROWS; r += BR) tma_load_2d(dst + r * E, map, (int)e0, r, bar);
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -108,8 +184,8 @@ __device__ __forceinline__ void wait_tile() { asm volatile("cp.async.wait_group 
 // L2 prefetch of the rows [N_ext][N_V] of a trace array seen by a tile's face
 // neighbours (and optionally of the tile itself)
 template <int D, int P, int NV, int E>
-__device__ __forceinline__ void prefetch_traces(const TensorGeom& g, const double* __restrict__ T, int64_t e0,
-                                                bool own) {
+__device__ __forceinline__ void prefetch_traces(const TensorGeom& g, const int (*sNb)[E], const double* __restrict__ T,
+                                                int64_t e0, bool own) {
   using Tm = TDims<D, P>;
   constexpr int NL = Tm::NL;
   for (int item = threadIdx.x; item < 2 * D * NL * NV; item += blockDim.x) {
@@ -117,7 +193,7 @@ __device__ __forceinline__ void prefetch_traces(const TensorGeom& g, const doubl
     const int face = ext / NL, d = face / 2, side = face % 2;
     // the neighbour across face (d, side) reads its opposite face (d, 1-side)
     const int ext_n = (2 * d + 1 - side) * NL + ext % NL;
-    const int64_t m = tnbr<D>(g, e0, d, side ? 1 : -1);
+    const int m = sNb[face][0];
     prefetch_l2(T + ((int64_t)ext_n * NV + v) * g.Kt + m);
     if (own) prefetch_l2(T + ((int64_t)ext * NV + v) * g.Kt + e0);
   }
@@ -129,40 +205,55 @@ __device__ __forceinline__ void prefetch_rows(const double* __restrict__ A, int6
   for (int row = threadIdx.x; row < NS * NV; row += blockDim.x) prefetch_l2(A + (int64_t)row * Kp + e0);
 }
 
-// gradient along lines -> sQ[d][s][v][E] = (2/h_d) (M16 C + M15 U_int)   (l.295-302)
-template <int D, int P, int EQ, int E>
-__device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                                               const double* __restrict__ Tu, const double* sU, double* sQ,
-                                               int64_t e0) {
+// Phase: gradient along lines -> sQ[d][s][v][E] = (2/h_d) (M16 C + M15 U_int)
+// (l.282-302).  One work item = (direction, line, variable, element), statically
+// mapped: thread tid owns items tid + k THREADS.  The neighbour traces of all its items
+// are loaded into registers first (GradNb::load, issued before the tile wait), so their
+// latency overlaps the tile load.
+template <int D, int P, int EQ, int E, int THREADS>
+struct GradNb {
   using T = TDims<D, P>;
-  constexpr int n = T::n, NL = T::NL, NS = T::NS;
-  constexpr int NV = Phys<EQ, D>::NV;
-  const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
+  static constexpr int NV = Phys<EQ, D>::NV;
+  static constexpr int ITEMS = D * T::NL * NV * E;
+  static constexpr int CI = (ITEMS + THREADS - 1) / THREADS;
+  double nb[CI][2];
+
+  __device__ __forceinline__ void load(const TensorGeom& g, const double* __restrict__ Tu, const int (*sNb)[E],
+                                       int64_t e0) {
+    constexpr int NL = T::NL;
+    const int Kt = (int)g.Kt;
 #pragma unroll
-  for (int d = 0; d < D; ++d)
-  for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
-    const int el = item % E, t = item / E;
-    const int64_t e = e0 + el;
-    if (e >= g.K) continue;
-    const int64_t mlo = tnbr<D>(g, e, d, -1), mhi = tnbr<D>(g, e, d, +1);
-    // neighbour traces for all variables first (loads in flight together)
-    double nbl[NV], nbh[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      nbl[v] = Tu[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kt + mlo];
-      nbh[v] = Tu[((int64_t)((2 * d + 0) * NL + t) * NV + v) * g.Kt + mhi];
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * THREADS;
+      nb[k][0] = nb[k][1] = 0.0;
+      if (item < ITEMS) {
+        const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
+        if (e0 + el < g.K) {
+          nb[k][0] = Tu[(((2 * d + 1) * NL + t) * NV + v) * Kt + sNb[2 * d][el]];
+          nb[k][1] = Tu[(((2 * d + 0) * NL + t) * NV + v) * Kt + sNb[2 * d + 1][el]];
+        }
+      }
     }
+  }
+
+  __device__ __forceinline__ void compute(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                          double* sQ, int64_t e0) const {
+    constexpr int n = T::n, NL = T::NL, NS = T::NS;
+    const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * THREADS;
+      if (item >= ITEMS) break;
+      const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
+      if (e0 + el >= g.K) continue;
+      const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
       double u[n];
 #pragma unroll
-      for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
+      for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
       // common values at both ends (own trace recomputed bit-identically, neighbour read)
       const double own0 = interp_end<n>(L.Iend[0], u), own1 = interp_end<n>(L.Iend[1], u);
-      const double nb0 = nbl[v];
-      const double nb1 = nbh[v];
-      const double c0 = wl * nb0 + wr * own0;   // face x_d = -1: this element is RIGHT
-      const double c1 = wl * own1 + wr * nb1;   // face x_d = +1: this element is LEFT
+      const double c0 = wl * nb[k][0] + wr * own0;  // face x_d = -1: this element is RIGHT
+      const double c1 = wl * own1 + wr * nb[k][1];  // face x_d = +1: this element is LEFT
       double ui[P];
 #pragma unroll
       for (int a = 0; a < P; ++a) {
@@ -171,329 +262,481 @@ __device__ __forceinline__ void gradient_lines(const TensorGeom& g, const Line1D
         for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i], s);
         ui[a] = s;
       }
+      const double jd = g.jinv[d];
 #pragma unroll
       for (int i = 0; i < n; ++i) {
         double q = L.Dfl[i][0] * c0;
 #pragma unroll
         for (int a = 0; a < P; ++a) q = fma(L.Dfl[i][a + 1], ui[a], q);
         q = fma(L.Dfl[i][P + 1], c1, q);
-        sQ[((d * NS + sidx<D, P>(d, t, i)) * NV + v) * E + el] = g.jinv[d] * q;
+        sQ[((d * NS + (lb + i * ls)) * NV + v) * E + el] = jd * q;
       }
     }
   }
-}
+};
 
-// traces of a state held in shared memory -> T[N_ext][N_V][Kp]
+// traces of a state held in shared memory -> T[N_ext][N_V][Kt]
 template <int D, int P, int NV, int E>
 __device__ __forceinline__ void write_traces(const TensorGeom& g, const Line1D& L, const double* sU,
                                              double* __restrict__ T, int64_t e0) {
   using Tm = TDims<D, P>;
-  constexpr int n = Tm::n, NL = Tm::NL, NEXT = Tm::NEXT;
-  (void)NEXT;
-#pragma unroll
-  for (int face = 0; face < 2 * D; ++face) {
+  constexpr int n = Tm::n, NL = Tm::NL;
+  for (int item = threadIdx.x; item < 2 * D * NL * NV * E; item += blockDim.x) {
+    const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, face = r2 / NL;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
     const int d = face / 2, side = face % 2;
-    for (int item = threadIdx.x; item < NL * NV * E; item += blockDim.x) {
-      const int el = item % E, r = item / E, v = r % NV, t = r / NV;
-      const int64_t e = e0 + el;
-      if (e >= g.K) continue;
-      const int ext = face * NL + t;
-      double u[n];
+    const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+    double u[n];
 #pragma unroll
-      for (int i = 0; i < n; ++i) u[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
-      T[((int64_t)ext * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[side], u);
-    }
+    for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
+    T[((int64_t)(face * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[side], u);
   }
 }
 
 template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const double* __restrict__ U,
+__global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const __grid_constant__ TileMaps tm,
                                                  double* __restrict__ T) {
   constexpr int NV = Phys<EQ, D>::NV;
-  extern __shared__ double smem[];
+  constexpr int ROWS = TDims<D, P>::NS * NV;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t bar;
   const int64_t e0 = (int64_t)blockIdx.x * E;
-  load_tile<D, P, NV, E>(U, smem, e0, g.K, g.Kp);
-  wait_tile();
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, ROWS * E * 8);
+    tma_tile<ROWS, E>(smem, &tm.uin, e0, &bar);
+  }
   __syncthreads();
+  mbar_wait(&bar, 0);
   write_traces<D, P, NV, E>(g, L, smem, T, e0);
 }
 
-// kernel A: gradient + published viscous normal-flux traces
+// Kernel A phase helpers -----------------------------------------------------------
+// publish g = n_L . f^v(u, q) at the face point (d, side, t) of element slot el
 template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b) {
+__device__ __forceinline__ void publish_g(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                          const double* sQ, double* __restrict__ Tg, int64_t e0, int d, int side,
+                                          int t, int el) {
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
-  extern __shared__ double smem[];
+  const int64_t e = e0 + el;
+  if (e >= g.K) return;
+  const int ext = (2 * d + side) * NL + t;
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  double u[NV], q[D * NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double ul[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) ul[i] = sU[((lb + i * ls) * NV + v) * E + el];
+    u[v] = interp_end<n>(L.Iend[side], ul);
+#pragma unroll
+    for (int dd = 0; dd < D; ++dd) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) s = fma(L.Iend[side][i], sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el], s);
+      q[dd * NV + v] = s;
+    }
+  }
+  double nL[D];
+#pragma unroll
+  for (int k2 = 0; k2 < D; ++k2) nL[k2] = (k2 == d) ? 1.0 : 0.0;  // canonical (left) normal +e_d
+  double gv[NV];
+  Ph::visc_dir(ph, u, q, nL, gv);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) Tg[((int64_t)ext * NV + v) * g.Kt + e] = gv[v];
+}
+
+// internal transformed flux F~ = detJ (J^-1 (f^c - f^v))_d at internal point a of d-line t
+// (one normal component, B7; l.305-311) -> sF[t][a][v][el]
+template <int D, int P, int EQ, int E>
+__device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                                              const double* sU, const double* sQ, double* sF, int d, int t, int a,
+                                              int el) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NS = T::NS;
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  double ua[NV], qa[D * NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], sU[((lb + i * ls) * NV + v) * E + el], s);
+    ua[v] = s;
+#pragma unroll
+    for (int dd = 0; dd < D; ++dd) {
+      double s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) s2 = fma(L.Iint[a][i], sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el], s2);
+      qa[dd * NV + v] = s2;
+    }
+  }
+  double w[D], fc[NV], fv[NV];
+  const double wf = g.detJ * g.jinv[d];
+#pragma unroll
+  for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
+  Ph::conv_dir(ph, ua, w, fc);
+  Ph::visc_dir(ph, ua, qa, w, fv);
+#pragma unroll
+  for (int v = 0; v < NV; ++v) sF[((t * P + a) * NV + v) * E + el] = fc[v] + fv[v];
+}
+
+// Kernel A (viscous equations) = the element-local "volume" work: gradient, published
+// viscous normal-flux traces, and the internal-flux part of the divergence
+// R_int = M13 M19 P2 F~ (convective + viscous, l.305-311, l.2919-2925) -> b.Rv
+// [N_sol][N_V][Kp]; kernel B adds the face part M14 D~.
+// Phases after the gradient: [publish g + F_v(d=0)] [div(0) + F_v(1)] [div(1) + F_v(2)]
+// [div(2)], with the internal-flux buffer double-buffered so each phase has work for
+// every thread.
+template <int D, int P, int EQ, int E, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
+                                                    const __grid_constant__ TileMaps tm) {
+  PH_INIT
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, NL = T::NL, NS = T::NS;
+  constexpr int NFB = NL * P * NV * E;  // one internal-flux buffer
+  extern __shared__ __align__(128) double smem[];
   double* sU = smem;
   double* sQ = smem + NS * NV * E;
+  double* sF = sQ + D * NS * NV * E;  // 2 x [NL][P][NV][E]
+  __shared__ int sNb[2 * D][E];
+  __shared__ __align__(8) uint64_t bar;
   const int64_t e0 = (int64_t)blockIdx.x * E;
-  load_tile<D, P, NV, E>(b.Uin, sU, e0, g.K, g.Kp);
-  prefetch_traces<D, P, NV, E>(g, b.Tu, e0, false);
-  wait_tile();
+  if (threadIdx.x == 0) {  // the stage-input tile by TMA
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, NS * NV * E * 8);
+    tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar);
+  }
+  fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();
-  gradient_lines<D, P, EQ, E>(g, L, ph, b.Tu, sU, sQ, e0);
+  PH(0, 0)
+  {
+    GradNb<D, P, EQ, E, NT> gn;
+    gn.load(g, b.Tu, sNb, e0);
+    mbar_wait(&bar, 0);
+    __syncthreads();
+  PH(0, 1)
+    gn.compute(g, L, ph, sU, sQ, e0);
+  }
   __syncthreads();
-  // publish g at face points of the sides that carry weight: side 1 (left) if
-  // 1/2 + beta != 0, side 0 (right) if 1/2 - beta != 0
+  PH(0, 2)
+  // publish on the sides that carry LDG weight: side 1 (left) if 1/2 + beta != 0,
+  // side 0 (right) if 1/2 - beta != 0
   const bool pub1 = (0.5 + ph.beta) != 0.0, pub0 = (0.5 - ph.beta) != 0.0;
+  const int nsides = (pub0 ? 1 : 0) + (pub1 ? 1 : 0);
+  const int npub = D * nsides * NL * E;
+  constexpr int NFI = NL * P * E;   // internal-flux items per direction
+  constexpr int NDI = NL * NV * E;  // divergence items per direction
+#pragma unroll 1
+  for (int ph_ = 0; ph_ <= D; ++ph_) {
+    // phase ph_: fluxes of direction ph_ (buffer ph_&1) [+ publish g in phase 0], then
+    // the divergence of direction ph_-1 (buffer (ph_-1)&1) whose partial sums were
+    // requested from L2 before the flux work
+    constexpr int CD = (NDI + NT - 1) / NT;
+    const int dd = ph_ - 1;
+    double prev[CD][P + 1];
+    if (ph_ >= 2) {
 #pragma unroll
-  for (int face = 0; face < 2 * D; ++face)
-  for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
-    const int el = item % E, t = item / E;
-    const int d = face / 2, side = face % 2, ext = face * NL + t;
-    if ((side == 1 && !pub1) || (side == 0 && !pub0)) continue;
-    const int64_t e = e0 + el;
-    if (e >= g.K) continue;
-    double u[NV], q[D * NV];
+      for (int k = 0; k < CD; ++k) {
+        const int item = threadIdx.x + k * NT;
+        const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+        if (item < NDI && e0 + el < g.K) {
+          const int lb = lbase<D, P>(dd, t), ls = lstr<D, P>(dd);
+          const double* src = b.Rv + (int64_t)(lb * NV + v) * g.Kp + e0 + el;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      double ul[n];
-#pragma unroll
-      for (int i = 0; i < n; ++i) ul[i] = sU[(sidx<D, P>(d, t, i) * NV + v) * E + el];
-      u[v] = interp_end<n>(L.Iend[side], ul);
-#pragma unroll
-      for (int dd = 0; dd < D; ++dd) {
-        double s = 0.0;
-#pragma unroll
-        for (int i = 0; i < n; ++i) s = fma(L.Iend[side][i], sQ[((dd * NS + sidx<D, P>(d, t, i)) * NV + v) * E + el], s);
-        q[dd * NV + v] = s;
+          for (int i = 0; i <= P; ++i) prev[k][i] = src[(int64_t)i * ls * NV * g.Kp];
+        }
       }
     }
-    double nL[D];
+    const int nA = ph_ == 0 ? npub : 0;
+    const int nB = ph_ < D ? NFI : 0;
+    for (int item = threadIdx.x; item < nA + nB; item += blockDim.x) {
+      if (item < nA) {
+        const int el = item % E, r = item / E;
+        const int t = r % NL, r2 = r / NL, k = r2 % nsides, d = r2 / nsides;
+        const int side = (nsides == 2) ? k : (pub1 ? 1 : 0);
+        publish_g<D, P, EQ, E>(g, L, ph, sU, sQ, b.Tg, e0, d, side, t, el);
+      } else {
+        const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % P, t = r / P;
+        visc_internal<D, P, EQ, E>(g, L, ph, sU, sQ, sF + (ph_ & 1) * NFB, ph_, t, a, el);
+      }
+    }
+    if (ph_ >= 1) {
+      const double* f0 = sF + (dd & 1) * NFB;
 #pragma unroll
-    for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;  // canonical (left) normal +e_d
-    double gv[NV];
-    Ph::visc_dir(ph, u, q, nL, gv);
+      for (int k = 0; k < CD; ++k) {
+        const int item = threadIdx.x + k * NT;
+        const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+        if (item >= NDI || e0 + el >= g.K) continue;
+        const int lb = lbase<D, P>(dd, t), ls = lstr<D, P>(dd);
+        double f[P];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)ext * NV + v) * g.Kt + e] = gv[v];
+        for (int a = 0; a < P; ++a) f[a] = f0[((t * P + a) * NV + v) * E + el];
+        double* dst = b.Rv + (int64_t)(lb * NV + v) * g.Kp + e0 + el;
+#pragma unroll
+        for (int i = 0; i <= P; ++i) {
+          double acc = ph_ >= 2 ? prev[k][i] : 0.0;
+#pragma unroll
+          for (int a = 0; a < P; ++a) acc = fma(L.Dfl[i][a + 1], f[a], acc);
+          dst[(int64_t)i * ls * NV * g.Kp] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  PH(0, 3 + ph_)
   }
 }
 
-// kernel B: fluxes, divergence, RK update, new traces
-template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) kt_stage(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
-                                                double dt) {
+// Kernel B: common fluxes at the line ends (Rusanov / upwind + the published viscous
+// traces + LDG jump, l.312-340), the face part of the divergence M14 D~ (l.2919-2925),
+// [inviscid equations: also the internal fluxes and M13 F~, which kernel A does
+// otherwise], R~ = sum + R_int, -R~/detJ, RK4 update, new traces.
+template <int D, int P, int EQ, int E, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
+                                                   double dt, const __grid_constant__ TileMaps tm) {
+  PH_INIT
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
-  extern __shared__ double smem[];
+  constexpr bool INT = !Ph::VISC;     // internal fluxes evaluated here (inviscid only)
+  constexpr int NF = INT ? P + 2 : 2;  // flux-line slots per line held in sF
+  extern __shared__ __align__(128) double smem[];
   double* sU = smem;
-  double* sR = smem + NS * NV * E;
-  double* sQ = sR + NS * NV * E;
-  const int64_t e0 = (int64_t)blockIdx.x * E;
-  load_tile<D, P, NV, E>(b.Uin, sU, e0, g.K, g.Kp);
-  // warm L2 with everything this tile reads later: neighbour traces, published
-  // viscous traces, RK registers (their latency is otherwise exposed mid-kernel)
-  prefetch_traces<D, P, NV, E>(g, b.Tu, e0, false);
-  if constexpr (Ph::VISC) prefetch_traces<D, P, NV, E>(g, b.Tg, e0, true);
-  if (stage == 1 || stage == 2) prefetch_rows<D, P, NV, E>(b.U, e0, g.Kp);
-  if (stage >= 1) prefetch_rows<D, P, NV, E>(b.ACC, e0, g.Kp);
-  wait_tile();
-  __syncthreads();
-  if constexpr (Ph::VISC) {
-    gradient_lines<D, P, EQ, E>(g, L, ph, b.Tu, sU, sQ, e0);
-    __syncthreads();
-  }
-  const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
-  // neighbour element ids of the tile, once: sNb[2d + side][el]
+  double* sR = smem + NS * NV * E;    // R~ accumulator, starts as R_int (kernel A)
+  double* sUn = sR + NS * NV * E;     // RK register u_n (stages 1, 2)
+  double* sAcc = sUn + NS * NV * E;   // RK accumulator (stages 1..3)
+  double* sF = sAcc + NS * NV * E;    // [NL][NF][NV][E] flux-line values of one direction
   __shared__ int sNb[2 * D][E];
-  for (int idx = threadIdx.x; idx < 2 * D * E; idx += blockDim.x) {
-    const int el = idx % E, k = idx / E;
-    const int64_t e = e0 + el;
-    sNb[k][el] = e < g.K ? (int)tnbr<D>(g, e, k / 2, (k % 2) ? 1 : -1) : 0;
+  __shared__ __align__(8) uint64_t bar[2];
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  // every element-local input of the tile is requested up front by TMA: the stage
+  // input (barrier 0), then R_int and the RK registers (barrier 1), waited for only
+  // where they are used
+  constexpr unsigned TB = NS * NV * E * 8;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar[0], TB);
+    tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar[0]);
+    const unsigned later = (Ph::VISC ? TB : 0) + ((stage == 1 || stage == 2) ? TB : 0) + (stage >= 1 ? TB : 0);
+    mbar_expect_tx(&bar[1], later);
+    if constexpr (Ph::VISC) tma_tile<NS * NV, E>(sR, &tm.rv, e0, &bar[1]);
+    if (stage == 1 || stage == 2) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar[1]);
+    if (stage >= 1) tma_tile<NS * NV, E>(sAcc, &tm.acc, e0, &bar[1]);
   }
+  fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();
-  const int Kp = (int)g.Kt;  // trace row stride
-  // one code copy for all directions (runtime d): keeps the kernel inside the I-cache
+  PH(1, 0)
+  // warm L2 with the neighbour traces and published viscous traces
+  prefetch_traces<D, P, NV, E>(g, sNb, b.Tu, e0, false);
+  if constexpr (Ph::VISC) prefetch_traces<D, P, NV, E>(g, sNb, b.Tg, e0, true);
+  mbar_wait(&bar[0], 0);
+  __syncthreads();
+  PH(1, 1)
+  const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+  const int Kt = (int)g.Kt;  // trace row stride
 #pragma unroll 1
   for (int d = 0; d < D; ++d) {
     const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
-    const int str = (d == 0 ? 1 : (d == 1 ? n : n * n)) * NV * E;  // point stride along the line
-    for (int item = threadIdx.x; item < NL * E; item += blockDim.x) {
-      const int el = item % E, t = item / E;
-      const int e = (int)(e0 + el);
-      if (e >= g.K) continue;
-      const int base = d == 0 ? n * t : (d == 1 ? (D == 2 ? t : (t % n) + n * n * (t / n)) : t);
-      const double* pu = sU + base * NV * E + el;
-      const double* pq = sQ + base * NV * E + el;
-      double* pr = sR + base * NV * E + el;
-      // issue the line-end global loads first (consumed after the internal points)
-      const int mlo = sNb[2 * d][el], mhi = sNb[2 * d + 1][el];
+    const double sface = g.sface[d];
+    double nL[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
+    // flux-line values.  End items (t, side, el) are statically owned (item tid + k
+    // NT): their trace loads are issued first and land while the thread computes its
+    // internal-point items (t, a, el); then the common fluxes.
+    constexpr int NEI = 2 * NL * E, CE = (NEI + NT - 1) / NT;
+    double un[CE][NV], gs[CE][NV];
+#pragma unroll
+    for (int k = 0; k < CE; ++k) {
+      const int item = threadIdx.x + k * NT;
+      const int el = item % E, r = item / E, side = r % 2, t = r / 2;
+      const int64_t e = e0 + el;
+      if (item >= NEI) break;
+      const int m = sNb[2 * d + side][el];
+      // canonical (left, right) = (x_d- element, x_d+ element)
       const int xL = (2 * d + 1) * NL + t, xR = (2 * d) * NL + t;  // left's +face, right's -face
-      double un0[NV], un1[NV], gs0[NV], gs1[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        un0[v] = b.Tu[(xL * NV + v) * Kp + mlo];   // left neighbour's trace (I am right)
-        un1[v] = b.Tu[(xR * NV + v) * Kp + mhi];   // right neighbour's trace (I am left)
+        un[k][v] = b.Tu[((side ? xR : xL) * NV + v) * Kt + m];
         if constexpr (Ph::VISC) {
-          const double* tg = b.Tg;
-          double a0 = 0.0, a1 = 0.0;
-          if (wl != 0.0) {
-            a0 = wl * tg[(xL * NV + v) * Kp + mlo];
-            a1 = wl * tg[(xL * NV + v) * Kp + e];
-          }
-          if (wr != 0.0) {
-            a0 = fma(wr, tg[(xR * NV + v) * Kp + e], a0);
-            a1 = fma(wr, tg[(xR * NV + v) * Kp + mhi], a1);
-          }
-          gs0[v] = a0;
-          gs1[v] = a1;
+          const int eL = side ? (int)e : m, eR = side ? m : (int)e;
+          double a0 = 0.0;
+          if (wl != 0.0) a0 = wl * b.Tg[(xL * NV + v) * Kt + eL];
+          if (wr != 0.0) a0 = fma(wr, b.Tg[(xR * NV + v) * Kt + eR], a0);
+          gs[k][v] = a0;
         }
       }
-      double r[n][NV];
+    }
+    for (int item = threadIdx.x; item < (INT ? NL * P * E : 0); item += blockDim.x) {
+      const int el = item % E, r = item / E, a = r % P, t = r / P;
+      const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+      double ua[NV];
 #pragma unroll
-      for (int i = 0; i < n; ++i)
+      for (int v = 0; v < NV; ++v) {
+        double s = 0.0;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) r[i][v] = d == 0 ? 0.0 : pr[i * str + v * E];
-      // both ends: common flux with canonical (left, right) = (x_d- element, x_d+ element)
-      double nL[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        double uo[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double ul[n];
-#pragma unroll
-          for (int i = 0; i < n; ++i) ul[i] = pu[i * str + v * E];
-          uo[v] = interp_end<n>(L.Iend[side], ul);
-        }
-        const double* uL = side ? uo : un0;
-        const double* uR = side ? un1 : uo;
-        double F[NV];
-        Ph::conv_common(ph, uL, uR, nL, F);
-        if constexpr (Ph::VISC) {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) F[v] += (side ? gs1[v] : gs0[v]) + ph.eta * (uL[v] - uR[v]);
-        }
-        const double sD = side ? g.sface[d] : -g.sface[d];
-        // M14 column of this end: -L_0' (x_d = -1), +L_{p+1}' (x_d = +1)
-#pragma unroll
-        for (int i = 0; i < n; ++i) {
-          const double m14 = side ? L.Dfl[i][P + 1] : -L.Dfl[i][0];
-#pragma unroll
-          for (int v = 0; v < NV; ++v) r[i][v] = fma(m14, sD * F[v], r[i][v]);
-        }
+        for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], sU[((lb + i * ls) * NV + v) * E + el], s);
+        ua[v] = s;
       }
-      // internal flux points along the line (normal e_d): F~ = detJ (J^-1 f)_d
-      // (not unrolled: bounds the live range to one point)
-#pragma unroll 1
-      for (int a = 0; a < P; ++a) {
-        double ua[NV], qa[Ph::VISC ? D * NV : 1], w[D], f[NV];
+      double w[D], f[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double sacc = 0.0;
+      for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
+      Ph::conv_dir(ph, ua, w, f);
 #pragma unroll
-          for (int i = 0; i < n; ++i) sacc = fma(L.Iint[a][i], pu[i * str + v * E], sacc);
-          ua[v] = sacc;
-        }
-        if constexpr (Ph::VISC) {
+      for (int v = 0; v < NV; ++v) sF[((t * NF + a + 1) * NV + v) * E + el] = f[v];
+    }
 #pragma unroll
-          for (int dd = 0; dd < D; ++dd)
+    for (int k = 0; k < CE; ++k) {
+      const int item = threadIdx.x + k * NT;
+      if (item >= NEI) break;
+      const int el = item % E, r = item / E, side = r % 2, t = r / 2;
+      const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+      double uo[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              double sacc = 0.0;
+      for (int v = 0; v < NV; ++v) {
+        double ul[n];
 #pragma unroll
-              for (int i = 0; i < n; ++i) sacc = fma(L.Iint[a][i], pq[dd * NS * NV * E + i * str + v * E], sacc);
-              qa[dd * NV + v] = sacc;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
-        Ph::conv_dir(ph, ua, w, f);
-        if constexpr (Ph::VISC) {
-          double fv[NV];
-          Ph::visc_dir(ph, ua, qa, w, fv);
-#pragma unroll
-          for (int v = 0; v < NV; ++v) f[v] += fv[v];
-        }
-#pragma unroll
-        for (int i = 0; i < n; ++i)
-#pragma unroll
-          for (int v = 0; v < NV; ++v) r[i][v] = fma(L.Dfl[i][a + 1], f[v], r[i][v]);
+        for (int i = 0; i < n; ++i) ul[i] = sU[((lb + i * ls) * NV + v) * E + el];
+        uo[v] = interp_end<n>(L.Iend[side], ul);
       }
+      const double* uL = side ? uo : un[k];
+      const double* uR = side ? un[k] : uo;
+      double F[NV];
+      Ph::conv_common(ph, uL, uR, nL, F);
+      if constexpr (Ph::VISC) {
 #pragma unroll
-      for (int i = 0; i < n; ++i)
+        for (int v = 0; v < NV; ++v) F[v] += gs[k][v] + ph.eta * (uL[v] - uR[v]);
+      }
+      const int kf = side ? NF - 1 : 0;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) pr[i * str + v * E] = r[i][v];
+      for (int v = 0; v < NV; ++v) sF[((t * NF + kf) * NV + v) * E + el] = sface * F[v];
+    }
+    if (d == 0) mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed
+    __syncthreads();
+  PH(1, 2)
+    // divergence along the lines: R_i += sum_k L_k'(g_i) Fline_k (M14 at the ends with
+    // the sign of the outward normal folded into L_0', M13 inside when INT)
+    for (int item = threadIdx.x; item < NL * NV * E; item += blockDim.x) {
+      const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+      const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+      double f[NF];
+#pragma unroll
+      for (int k = 0; k < NF; ++k) f[k] = sF[((t * NF + k) * NV + v) * E + el];
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        double* dst = sR + ((lb + i * ls) * NV + v) * E + el;
+        double acc = (d == 0 && INT) ? 0.0 : *dst;
+        if constexpr (INT) {
+#pragma unroll
+          for (int k = 0; k < NF; ++k) acc = fma(L.Dfl[i][k], f[k], acc);
+        } else {
+          acc = fma(L.Dfl[i][0], f[0], acc);
+          acc = fma(L.Dfl[i][P + 1], f[1], acc);
+        }
+        *dst = acc;
+      }
     }
     __syncthreads();
+  PH(1, 3)
   }
-  // dU/dt = -R~/detJ, RK4 (3-register form), new state into sU.  Rows are processed in
-  // batches of RB_RK per thread with all global loads of a batch issued before use.
+  // dU/dt = -R~/detJ (R~ includes R_int), RK4 (3-register form) along x-lines: one item = (x-line,
+  // variable, element) holds the line's new values in registers, writes them to sU and
+  // the registers, and publishes the two x-face traces from the same registers.
   const double idet = 1.0 / g.detJ;
-  constexpr int TOT = NS * NV * E;
-  constexpr int RB_RK = 5;
-  const int nth = blockDim.x;
-  for (int base0 = threadIdx.x; base0 < TOT; base0 += RB_RK * nth) {
-    double a0[RB_RK], a1[RB_RK];
-    int64_t gi[RB_RK];
-    bool ok[RB_RK];
+  for (int item = threadIdx.x; item < NL * NV * E; item += NT) {
+    const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int p0 = n * t;  // x-line t: points n t .. n t + n - 1
+    double un[n];
 #pragma unroll
-    for (int k = 0; k < RB_RK; ++k) {
-      const int idx = base0 + k * nth;
-      const int el = idx % E, row = idx / E;
-      ok[k] = idx < TOT && e0 + el < g.K;
-      gi[k] = (int64_t)row * g.Kp + e0 + el;
-      a0[k] = 0.0;
-      a1[k] = 0.0;
-      if (ok[k]) {
-        if (stage >= 1) a0[k] = __ldcs(b.ACC + gi[k]);
-        if (stage == 1 || stage == 2) a1[k] = __ldcs(b.U + gi[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < RB_RK; ++k) {
-      if (!ok[k]) continue;
-      const int idx = base0 + k * nth;
+    for (int i = 0; i < n; ++i) {
+      const int idx = ((p0 + i) * NV + v) * E + el;
+      const int64_t gi = (int64_t)((p0 + i) * NV + v) * g.Kp + e;
       const double kk = -sR[idx] * idet;
       double nu;
       switch (stage) {
         case -1:
-          b.out[gi[k]] = kk;
+          b.out[gi] = kk;
           nu = 0.0;
           break;
         case 0: {
           const double u0 = sU[idx];
-          b.ACC[gi[k]] = fma(dt / 6.0, kk, u0);
+          b.ACC[gi] = fma(dt / 6.0, kk, u0);
           nu = fma(0.5 * dt, kk, u0);
-          b.Us[gi[k]] = nu;
+          b.Us[gi] = nu;
         } break;
         case 1:
-          b.ACC[gi[k]] = fma(dt / 3.0, kk, a0[k]);
-          nu = fma(0.5 * dt, kk, a1[k]);
-          b.Us[gi[k]] = nu;
+          b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+          nu = fma(0.5 * dt, kk, sUn[idx]);
+          b.Us[gi] = nu;
           break;
         case 2:
-          b.ACC[gi[k]] = fma(dt / 3.0, kk, a0[k]);
-          nu = fma(dt, kk, a1[k]);
-          b.Us[gi[k]] = nu;
+          b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+          nu = fma(dt, kk, sUn[idx]);
+          b.Us[gi] = nu;
           break;
         default:
-          nu = fma(dt / 6.0, kk, a0[k]);
-          b.U[gi[k]] = nu;
+          nu = fma(dt / 6.0, kk, sAcc[idx]);
+          b.U[gi] = nu;
           break;
       }
+      un[i] = nu;
       sU[idx] = nu;
+    }
+    if (stage >= 0) {
+      b.Tu_next[((int64_t)(0 * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[0], un);
+      b.Tu_next[((int64_t)(1 * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[1], un);
     }
   }
   if (stage < 0) return;
   __syncthreads();
-  write_traces<D, P, NV, E>(g, L, sU, b.Tu_next, e0);
+  PH(1, 4)
+  // traces of the new state on the faces normal to y (and z): both ends per item
+  for (int item = threadIdx.x; item < (D - 1) * NL * NV * E; item += blockDim.x) {
+    const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = 1 + r2 / NL;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+    double u[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
+    b.Tu_next[((int64_t)((2 * d) * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[0], u);
+    b.Tu_next[((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[1], u);
+  }
+  PH(1, 15)
 }
 
 // ------------------------------------------------------------------ launchers
 template <int D, int P, int EQ>
 struct TCfg {
   static constexpr int NV = Phys<EQ, D>::NV;
-  static constexpr int E = NV > 1 ? 8 : (D == 3 ? 16 : 32);
+  static constexpr bool VISC = Phys<EQ, D>::VISC;
   static constexpr int NL = TDims<D, P>::NL;
-  static constexpr int THREADS = ((NL * E + 31) / 32) * 32 > 256 ? 256 : ((NL * E + 31) / 32) * 32;
-  static constexpr size_t TILE = (size_t)TDims<D, P>::NS * NV * E * sizeof(double);
-  static constexpr size_t SMEM_A = TILE * (1 + D);
-  static constexpr size_t SMEM_B = TILE * (2 + (Phys<EQ, D>::VISC ? D : 0));
+  static constexpr int NS = TDims<D, P>::NS;
+  // tiles: kernel A (viscous volume work) and kernel B (faces + update) take E elements
+  // per CTA of NT threads; small tiles keep several CTAs resident per SM so their
+  // load / compute / store phases interleave
+  static constexpr int E = NV > 1 ? 8 : (D == 3 ? 16 : 32);  // kernel B and traces
+  static constexpr int EA = E;
+  static constexpr int NTB = 256;
+  static constexpr int NTA = 256;
+  static constexpr int MINB_B = 2;
+  static constexpr int MINB_A = 2;
+  static constexpr int THREADS = 256;
+  static constexpr size_t TILE = (size_t)NS * NV * E * sizeof(double);
+  static constexpr size_t TILEA = (size_t)NS * NV * EA * sizeof(double);
+  static constexpr size_t SMEM_A = TILEA * (1 + D) + 2 * (size_t)NL * P * NV * EA * sizeof(double);
+  // kernel B: sU, sR, the RK registers (u_n, ACC), flux-line slots
+  static constexpr size_t SMEM_B = TILE * 4 + (size_t)NL * (VISC ? 2 : P + 2) * NV * E * sizeof(double);
   static constexpr size_t SMEM_T = TILE;
 };
 
@@ -505,63 +748,126 @@ static void set_smem(const void* k, size_t bytes) {
   }
 }
 
+// TMA descriptor of array ptr (cached per pointer)
+static const CUtensorMap& tma_map(TensorTma* t, const void* ptr) {
+  for (int i = 0; i < 8; ++i)
+    if (t->ptr[i] == ptr) return t->map[i];
+  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      throw std::runtime_error("CUDA: cuTensorMapEncodeTiled unavailable");
+    enc = (EncodeFn)fn;
+  }
+  const int i = t->next;
+  t->next = (t->next + 1) % 8;
+  cuuint64_t dims[2] = {(cuuint64_t)t->Kp, (cuuint64_t)t->rows};
+  cuuint64_t strides[1] = {(cuuint64_t)t->Kp * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)t->E, (cuuint32_t)t->box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(&t->map[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  t->ptr[i] = ptr;
+  return t->map[i];
+}
+
+static TileMaps maps_for(TensorTma* t, const TensorBufs& b, bool full) {
+  TileMaps m;
+  std::memset(&m, 0, sizeof(m));
+  m.uin = tma_map(t, b.Uin);
+  if (full) {
+    if (b.U) m.un = tma_map(t, b.U);
+    if (b.ACC) m.acc = tma_map(t, b.ACC);
+    if (b.Rv) m.rv = tma_map(t, b.Rv);
+  }
+  return m;
+}
+
 template <int D, int P, int EQ>
-static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const TensorBufs& b, int stage,
-                      double dt, cudaStream_t st, int which) {
+static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
+                      int stage, double dt, cudaStream_t st, int which) {
   using C = TCfg<D, P, EQ>;
-  const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
   if (which == 0) {
     if constexpr (Phys<EQ, D>::VISC) {
-      auto ka = kt_grad<D, P, EQ, C::E>;
+      const unsigned grid = (unsigned)((g.K + C::EA - 1) / C::EA);
+      auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A>;
       set_smem<D, P, EQ>((const void*)ka, C::SMEM_A);
-      ka<<<grid, C::THREADS, C::SMEM_A, st>>>(g, L, ph, b);
+      ka<<<grid, C::NTA, C::SMEM_A, st>>>(g, L, ph, b, maps_for(tma, b, false));
     }
   } else {
-    auto kb = kt_stage<D, P, EQ, C::E>;
+    const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
+    auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B>;
     set_smem<D, P, EQ>((const void*)kb, C::SMEM_B);
-    kb<<<grid, C::THREADS, C::SMEM_B, st>>>(g, L, ph, b, stage, dt);
+    kb<<<grid, C::NTB, C::SMEM_B, st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
   }
 }
 
 template <int D, int P, int EQ>
-static void run_traces(const TensorGeom& g, const Line1D& L, const double* U, double* Tu, cudaStream_t st) {
+static void run_traces(const TensorGeom& g, const Line1D& L, TensorTma* tma, const double* U, double* Tu,
+                       cudaStream_t st) {
   using C = TCfg<D, P, EQ>;
   const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
   auto k = kt_traces<D, P, EQ, C::E>;
   set_smem<D, P, EQ>((const void*)k, C::SMEM_T);
-  k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, L, U, Tu);
+  TensorBufs b{};
+  b.Uin = U;
+  k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, L, maps_for(tma, b, false), Tu);
 }
 
-typedef void (*StageFn)(const TensorGeom&, const Line1D&, const PhysDev&, const TensorBufs&, int, double,
+template <int D, int P, int EQ>
+static void init_tma(TensorTma* t, int64_t Kp) {
+  using C = TCfg<D, P, EQ>;
+  t->rows = C::NS * C::NV;
+  t->box_rows = tma_box_rows(t->rows);
+  t->E = C::E;
+  t->Kp = Kp;
+  for (int i = 0; i < 8; ++i) t->ptr[i] = nullptr;
+  t->next = 0;
+}
+
+typedef void (*StageFn)(const TensorGeom&, const Line1D&, const PhysDev&, TensorTma*, const TensorBufs&, int, double,
                         cudaStream_t, int);
-typedef void (*TraceFn)(const TensorGeom&, const Line1D&, const double*, double*, cudaStream_t);
+typedef void (*TraceFn)(const TensorGeom&, const Line1D&, TensorTma*, const double*, double*, cudaStream_t);
+typedef void (*TmaFn)(TensorTma*, int64_t);
 
 template <int D, int P>
-static void pick(int eq, StageFn* s, TraceFn* t) {
+static void pick(int eq, StageFn* s, TraceFn* t, TmaFn* m) {
   switch (eq) {
-    case EQ_LINADV: *s = run_stage<D, P, EQ_LINADV>; *t = run_traces<D, P, EQ_LINADV>; break;
-    case EQ_LINADVDIFF: *s = run_stage<D, P, EQ_LINADVDIFF>; *t = run_traces<D, P, EQ_LINADVDIFF>; break;
-    case EQ_EULER: *s = run_stage<D, P, EQ_EULER>; *t = run_traces<D, P, EQ_EULER>; break;
-    default: *s = run_stage<D, P, EQ_NS>; *t = run_traces<D, P, EQ_NS>; break;
+    case EQ_LINADV: *s = run_stage<D, P, EQ_LINADV>; *t = run_traces<D, P, EQ_LINADV>; *m = init_tma<D, P, EQ_LINADV>; break;
+    case EQ_LINADVDIFF:
+      *s = run_stage<D, P, EQ_LINADVDIFF>;
+      *t = run_traces<D, P, EQ_LINADVDIFF>;
+      *m = init_tma<D, P, EQ_LINADVDIFF>;
+      break;
+    case EQ_EULER: *s = run_stage<D, P, EQ_EULER>; *t = run_traces<D, P, EQ_EULER>; *m = init_tma<D, P, EQ_EULER>; break;
+    default: *s = run_stage<D, P, EQ_NS>; *t = run_traces<D, P, EQ_NS>; *m = init_tma<D, P, EQ_NS>; break;
   }
 }
 
-static void pick_all(int D, int P, int eq, StageFn* s, TraceFn* t) {
+static void pick_all(int D, int P, int eq, StageFn* s, TraceFn* t, TmaFn* m) {
   *s = nullptr;
   *t = nullptr;
+  *m = nullptr;
   if (D == 2) {
     switch (P) {
-      case 1: pick<2, 1>(eq, s, t); break;
-      case 2: pick<2, 2>(eq, s, t); break;
-      case 3: pick<2, 3>(eq, s, t); break;
-      case 4: pick<2, 4>(eq, s, t); break;
+      case 1: pick<2, 1>(eq, s, t, m); break;
+      case 2: pick<2, 2>(eq, s, t, m); break;
+      case 3: pick<2, 3>(eq, s, t, m); break;
+      case 4: pick<2, 4>(eq, s, t, m); break;
     }
   } else {
     switch (P) {
-      case 1: pick<3, 1>(eq, s, t); break;
-      case 2: pick<3, 2>(eq, s, t); break;
-      case 3: pick<3, 3>(eq, s, t); break;
-      case 4: pick<3, 4>(eq, s, t); break;
+      case 1: pick<3, 1>(eq, s, t, m); break;
+      case 2: pick<3, 2>(eq, s, t, m); break;
+      case 3: pick<3, 3>(eq, s, t, m); break;
+      case 4: pick<3, 4>(eq, s, t, m); break;
     }
   }
 }
@@ -569,33 +875,62 @@ static void pick_all(int D, int P, int eq, StageFn* s, TraceFn* t) {
 bool tensor_supported(int D, int P, int eq) {
   StageFn s;
   TraceFn t;
+  TmaFn m;
   if (eq < 0 || eq > 3) return false;
-  pick_all(D, P, eq, &s, &t);
+  pick_all(D, P, eq, &s, &t, &m);
   return s != nullptr;
 }
 
-void tensor_launch_grad(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                        const TensorBufs& b, cudaStream_t st) {
+void tensor_tma_init(TensorTma* tma, int D, int P, int eq, int64_t Kp) {
   StageFn s;
   TraceFn t;
-  pick_all(D, P, eq, &s, &t);
-  s(g, L, ph, b, 0, 0.0, st, 0);
+  TmaFn m;
+  pick_all(D, P, eq, &s, &t, &m);
+  m(tma, Kp);
+}
+
+void tensor_launch_grad(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                        TensorTma* tma, const TensorBufs& b, cudaStream_t st) {
+  StageFn s;
+  TraceFn t;
+  TmaFn m;
+  pick_all(D, P, eq, &s, &t, &m);
+  s(g, L, ph, tma, b, 0, 0.0, st, 0);
 }
 
 void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                        const TensorBufs& b, int stage, double dt, cudaStream_t st) {
+                        TensorTma* tma, const TensorBufs& b, int stage, double dt, cudaStream_t st) {
   StageFn s;
   TraceFn t;
-  pick_all(D, P, eq, &s, &t);
-  s(g, L, ph, b, stage, dt, st, 1);
+  TmaFn m;
+  pick_all(D, P, eq, &s, &t, &m);
+  s(g, L, ph, tma, b, stage, dt, st, 1);
 }
 
-void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const double* U,
-                          double* Tu, cudaStream_t st) {
+void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, TensorTma* tma,
+                          const double* U, double* Tu, cudaStream_t st) {
   StageFn s;
   TraceFn t;
-  pick_all(D, P, eq, &s, &t);
-  t(g, L, U, Tu, st);
+  TmaFn m;
+  pick_all(D, P, eq, &s, &t, &m);
+  t(g, L, tma, U, Tu, st);
 }
+
+#ifdef SDRT_PHASE_PROF
+void tensor_phase_cycles(unsigned long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(g_phase_cycles));
+  if (reset) {
+    static unsigned long long z[2][16] = {};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+  }
+}
+#endif
 
 }  // namespace sdrt
+
+#ifdef SDRT_PHASE_PROF
+// tools-only accessor of the profiling build (libsdrt_prof.so); not part of include/sdrt.h
+extern "C" void sdrt_debug_phase_cycles(unsigned long long* out, int reset) {
+  sdrt::tensor_phase_cycles(out, reset != 0);
+}
+#endif

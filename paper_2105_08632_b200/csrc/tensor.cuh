@@ -1,5 +1,6 @@
 // Fused sum-factorised SDRT stage for tensor-product elements (quad/hex), sm_100a.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,17 +44,30 @@ struct TensorBufs {
   const double* Tu;   // traces of the stage input  [N_ext][N_V][Kp]
   double* Tu_next;    // traces of the stage output
   double* Tg;         // published viscous normal-flux traces [N_ext][N_V][Kp]
+  double* Rv;         // viscous internal-flux divergence M13 F~_v [N_sol][N_V][Kp] (kernel A -> B)
 };
 
+// TMA descriptors of the element-major state-like arrays [N_sol N_V rows][Kp] seen by
+// the fused kernels: 2-D tiles of E elements x box_rows rows land in shared memory in
+// the kernels' own [row][E] layout.  Encoded on the host per array pointer (cached).
+struct TensorTma {
+  int rows = 0, box_rows = 0, E = 0;
+  int64_t Kp = 0;
+  const void* ptr[8] = {};
+  CUtensorMap map[8];
+  int next = 0;
+};
+void tensor_tma_init(TensorTma* t, int D, int P, int eq, int64_t Kp);
+
 // Launchers (tensor.cu).  stage: -1 residual, 0..3 RK4 stages.
-void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const double* U,
-                          double* Tu, cudaStream_t st);
+void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, TensorTma* tma,
+                          const double* U, double* Tu, cudaStream_t st);
 // kernel A (viscous equations only): gradient + published viscous normal-flux traces
 void tensor_launch_grad(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                        const TensorBufs& b, cudaStream_t st);
+                        TensorTma* tma, const TensorBufs& b, cudaStream_t st);
 // kernel B: fluxes, divergence, RK update, new traces
 void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                        const TensorBufs& b, int stage, double dt, cudaStream_t st);
+                        TensorTma* tma, const TensorBufs& b, int stage, double dt, cudaStream_t st);
 bool tensor_supported(int D, int P, int eq);
 
 }  // namespace sdrt

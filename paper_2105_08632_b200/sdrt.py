@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libsdrt.so")
+_LIBPATH = os.environ.get("SDRT_LIB") or os.path.join(_HERE, "libsdrt.so")
 if not os.path.exists(_LIBPATH):
     raise ImportError(f"libsdrt.so not built ({_LIBPATH}); run __graft_entry__.build() or "
                       "python paper_2105_08632_b200/build.py")
