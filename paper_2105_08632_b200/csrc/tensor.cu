@@ -26,6 +26,7 @@
 
 #include <cstring>
 #include <stdexcept>
+#include <type_traits>
 #include <string>
 
 #include "tensor.cuh"
@@ -315,10 +316,10 @@ __global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const _
 
 // Kernel A phase helpers -----------------------------------------------------------
 // publish g = n_L . f^v(u, q) at the face point (d, side, t) of element slot el
-template <int D, int P, int EQ, int E>
+template <int D, int P, int EQ, int E, int d>
 __device__ __forceinline__ void publish_g(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
-                                          const double* sQ, double* __restrict__ Tg, int64_t e0, int d, int side,
-                                          int t, int el) {
+                                          const double* sQ, double* __restrict__ Tg, int64_t e0, int side, int t,
+                                          int el) {
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
@@ -352,10 +353,9 @@ __device__ __forceinline__ void publish_g(const TensorGeom& g, const Line1D& L, 
 
 // internal transformed flux F~ = detJ (J^-1 (f^c - f^v))_d at internal point a of d-line t
 // (one normal component, B7; l.305-311) -> sF[t][a][v][el]
-template <int D, int P, int EQ, int E>
+template <int D, int P, int EQ, int E, int d>
 __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                                              const double* sU, const double* sQ, double* sF, int d, int t, int a,
-                                              int el) {
+                                              const double* sU, const double* sQ, double* sF, int t, int a, int el) {
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NS = T::NS;
@@ -461,10 +461,15 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         const int el = item % E, r = item / E;
         const int t = r % NL, r2 = r / NL, k = r2 % nsides, d = r2 / nsides;
         const int side = (nsides == 2) ? k : (pub1 ? 1 : 0);
-        publish_g<D, P, EQ, E>(g, L, ph, sU, sQ, b.Tg, e0, d, side, t, el);
+        if (d == 0) publish_g<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+        else if (d == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+        else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
       } else {
         const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % P, t = r / P;
-        visc_internal<D, P, EQ, E>(g, L, ph, sU, sQ, sF + (ph_ & 1) * NFB, ph_, t, a, el);
+        double* f1 = sF + (ph_ & 1) * NFB;
+        if (ph_ == 0) visc_internal<D, P, EQ, E, 0>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if (ph_ == 1) visc_internal<D, P, EQ, E, 1>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if constexpr (D == 3) visc_internal<D, P, EQ, E, 2>(g, L, ph, sU, sQ, f1, t, a, el);
       }
     }
     if (ph_ >= 1) {
@@ -542,8 +547,10 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   PH(1, 1)
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
   const int Kt = (int)g.Kt;  // trace row stride
-#pragma unroll 1
-  for (int d = 0; d < D; ++d) {
+  // one direction of the flux-line work; instantiated per direction (compile-time d
+  // removes the structural zeros of the normal e_d from the physics)
+  auto direction = [&](auto dc) {
+    constexpr int d = decltype(dc)::value;
     const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
     const double sface = g.sface[d];
     double nL[D];
@@ -646,7 +653,10 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
     }
     __syncthreads();
   PH(1, 3)
-  }
+  };
+  direction(std::integral_constant<int, 0>{});
+  direction(std::integral_constant<int, 1>{});
+  if constexpr (D == 3) direction(std::integral_constant<int, 2>{});
   // dU/dt = -R~/detJ (R~ includes R_int), RK4 (3-register form) along x-lines: one item = (x-line,
   // variable, element) holds the line's new values in registers, writes them to sU and
   // the registers, and publishes the two x-face traces from the same registers.
