@@ -385,6 +385,7 @@ struct sdrt_ctx {
   // fused simplex path
   bool sfused = false;
   SimplexOps sops;
+  SimplexTma stma;
   // halo exchange
   bool needs_halo = false, loopback = false;
   int nslab = 0;
@@ -395,33 +396,31 @@ struct sdrt_ctx {
   bool auto_halo = false;     // library performs the (loopback) exchange itself
 };
 
-struct OpHost4 {
-  std::vector<int> ptr, col;
-  std::vector<double> val;
-  int rows, cols, nblk;
+// Dense operator in DMMA fragment order (simplex.cuh SOpF): rows padded to 8, columns
+// to 4, frag[(m * kt + k) * 32 + lane] = M[8 m + lane / 4][4 k + lane % 4].
+struct OpHostF {
+  std::vector<double> frag;
+  int rows, cols, mt, kt;
 };
 
-static OpHost4 pack4(const Mat& M, const std::vector<int>* colmap = nullptr) {
-  OpHost4 o;
+static OpHostF pack_frag(const Mat& M) {
+  OpHostF o;
   o.rows = M.rows;
   o.cols = M.cols;
-  o.nblk = (M.rows + SRB - 1) / SRB;
-  o.ptr.push_back(0);
-  for (int b = 0; b < o.nblk; ++b) {
-    for (int c = 0; c < M.cols; ++c) {
-      bool nz = false;
-      for (int r = b * SRB; r < std::min(M.rows, (b + 1) * SRB); ++r) nz = nz || M(r, c) != 0.0;
-      if (!nz) continue;
-      o.col.push_back(colmap ? (*colmap)[c] : c);
-      for (int r = b * SRB; r < (b + 1) * SRB; ++r) o.val.push_back(r < M.rows ? M(r, c) : 0.0);
-    }
-    o.ptr.push_back((int)o.col.size());
-  }
+  o.mt = (M.rows + 7) / 8;
+  o.kt = (M.cols + 3) / 4;
+  o.frag.assign((size_t)o.mt * o.kt * 32, 0.0);
+  for (int m = 0; m < o.mt; ++m)
+    for (int k = 0; k < o.kt; ++k)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int r = 8 * m + lane / 4, c = 4 * k + lane % 4;
+        if (r < M.rows && c < M.cols) o.frag[((size_t)m * o.kt + k) * 32 + lane] = M(r, c);
+      }
   return o;
 }
 
 // simplex operators: M0, M12, G = [M16 | M15 P] rows (s,d), M14, M13 M19 P2 (cols (d,u))
-static void simplex_pack(const Operators& O, int D, std::vector<OpHost4>* out, Mat* M0dense) {
+static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
   const RefElement& r = O.ref;
   int ns = r.nsol;
   Mat G(ns * D, r.next + r.nu);
@@ -440,12 +439,11 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHost4>* out, M
       if (v != 0.0) M13F(s2, r.int_dir[i] * r.nu + r.int_u[i]) += v;
     }
   out->clear();
-  out->push_back(pack4(O.M0));
-  out->push_back(pack4(O.M12));
-  out->push_back(pack4(G));
-  out->push_back(pack4(O.M14));
-  out->push_back(pack4(M13F));
-  *M0dense = O.M0;
+  out->push_back(pack_frag(O.M0));
+  out->push_back(pack_frag(O.M12));
+  out->push_back(pack_frag(G));
+  out->push_back(pack_frag(O.M14));
+  out->push_back(pack_frag(M13F));
 }
 
 static int nvars(int eq, int D) { return (eq == SDRT_EQ_LINADV || eq == SDRT_EQ_LINADVDIFF) ? 1 : D + 2; }
@@ -485,13 +483,9 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.off_tg = o; o += tb;
   p.off_sops = o;
   if (!etype_tensor(m.etype)) {
-    std::vector<OpHost4> s4;
-    Mat dense;
-    simplex_pack(O, D, &s4, &dense);
-    for (auto& h : s4)
-      o += align256(h.ptr.size() * sizeof(int)) + align256(h.col.size() * sizeof(int) + 4) +
-           align256(h.val.size() * sizeof(double) + 8);
-    o += align256(dense.a.size() * sizeof(double));
+    std::vector<OpHostF> s4;
+    simplex_pack(O, D, &s4);
+    for (auto& h : s4) o += align256(h.frag.size() * sizeof(double));
   }
   // halo lists: send (row, col) and recv (row, col) int32 for all slabs, + a loopback
   // staging buffer of the same number of values
@@ -710,29 +704,18 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       return SDRT_E_UNSUPPORTED;
     }
     if (c->sfused) {
-      std::vector<OpHost4> s4;
-      Mat dense;
-      simplex_pack(O, m.nd, &s4, &dense);
+      std::vector<OpHostF> s4;
+      simplex_pack(O, m.nd, &s4);
       size_t so = p.off_sops;
-      SOp* dst[5] = {&c->sops.M0, &c->sops.M12, &c->sops.G, &c->sops.M14, &c->sops.M13F};
+      SOpF* dst[5] = {&c->sops.M0, &c->sops.M12, &c->sops.G, &c->sops.M14, &c->sops.M13F};
       for (int i = 0; i < 5; ++i) {
-        OpHost4& h = s4[i];
-        int* dptr = (int*)(base + so);
-        CUDA_OK(cudaMemcpyAsync(dptr, h.ptr.data(), h.ptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        so += align256(h.ptr.size() * sizeof(int));
-        int* dcol = (int*)(base + so);
-        if (!h.col.empty())
-          CUDA_OK(cudaMemcpyAsync(dcol, h.col.data(), h.col.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        so += align256(h.col.size() * sizeof(int) + 4);
+        OpHostF& h = s4[i];
         double* dval = (double*)(base + so);
-        if (!h.val.empty())
-          CUDA_OK(cudaMemcpyAsync(dval, h.val.data(), h.val.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-        so += align256(h.val.size() * sizeof(double) + 8);
-        *dst[i] = SOp{h.rows, h.cols, h.nblk, dptr, dcol, dval};
+        CUDA_OK(cudaMemcpyAsync(dval, h.frag.data(), h.frag.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        so += align256(h.frag.size() * sizeof(double));
+        *dst[i] = SOpF{h.rows, h.cols, h.mt, h.kt, dval};
       }
-      double* dd = (double*)(base + so);
-      CUDA_OK(cudaMemcpyAsync(dd, dense.a.data(), dense.a.size() * sizeof(double), cudaMemcpyHostToDevice, st));
-      c->sops.M0dense = dd;
+      simplex_tma_init(&c->stma, m.nd, m.p, ph->eq, m.K_pad);
       c->Tu[0] = (double*)(base + p.off_tu0);
       c->Tu[1] = (double*)(base + p.off_tu1);
       c->Tg = (double*)(base + p.off_tg);
@@ -962,7 +945,7 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
 static void sfused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
   {
     Mark mk(c, st, T_STRACE);
-    simplex_launch_traces(c->nd, c->p, c->eq, c->g, c->sops, U, c->Tu[c->cur], st);
+    simplex_launch_traces(c->nd, c->p, c->eq, c->g, c->sops, &c->stma, U, c->Tu[c->cur], st);
   }
   if (c->auto_halo) halo_loopback(c, 0, st);
 }
@@ -978,17 +961,18 @@ static void sfused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, d
   b.Tu = c->Tu[c->cur];
   b.Tu_next = c->Tu[c->cur ^ 1];
   b.Tg = c->Tg;
+  b.Rint = c->R;
   b.xm = c->xm;
   if (c->visc) {
     {
       Mark mk(c, st, T_SA);
-      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, st);
+      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, &c->stma, b, st);
     }
     if (c->auto_halo) halo_loopback(c, 1, st);
   }
   {
     Mark mk(c, st, T_SB);
-    simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, stage, dt, st);
+    simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, &c->stma, b, stage, dt, st);
   }
   if (stage >= 0) {
     c->cur ^= 1;
@@ -1160,9 +1144,10 @@ sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
       b.Uin = Uin;
       b.Tu = c->Tu[c->cur];
       b.Tg = c->Tg;
+      b.Rint = c->R;
       b.xm = c->xm;
       Mark mk(c, st, T_SA);
-      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, st);
+      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, &c->stma, b, st);
     }
     CUDA_OK(cudaGetLastError());
     return SDRT_OK;
@@ -1200,9 +1185,10 @@ sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, doub
       b.Tu = c->Tu[c->cur];
       b.Tu_next = c->Tu[c->cur ^ 1];
       b.Tg = c->Tg;
+      b.Rint = c->R;
       b.xm = c->xm;
       Mark mk(c, st, T_SB);
-      simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, b, stage, dt, st);
+      simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, &c->stma, b, stage, dt, st);
     }
     if (stage >= 0) c->cur ^= 1;
     CUDA_OK(cudaGetLastError());

@@ -1,27 +1,32 @@
 // Fused SDRT stage for simplex elements (tri / tet) on sm_100a, fp64.
 //
 // Simplex operators are dense (App. B l.2855-2925, B7: all N_D components per unique
-// internal point, l.2927-2932), so each App. B product is a small dense matrix applied
-// to a tile of E elements held in shared memory [row][var][E] (element fastest, the ABI
-// layout).  One thread computes SRB rows x all variables for one element: operator
-// entries are warp-uniform reads (L1 broadcast), tile entries are bank-conflict-free.
+// internal point, l.2927-2932), so every App. B product is a small dense matrix times
+// a tile of E elements held in shared memory as [row][var][E] (element fastest, the
+// ABI layout): Y[r][n] = sum_c M[r][c] X[c][n], n = (var, element).  These products
+// run on the FP64 tensor cores (mma.sync m8n8k4 f64, DMMA): operator fragments come
+// from a fragment-ordered copy in global memory (L1-resident), tile fragments from
+// shared memory; each output is accumulated in the fixed k order, so the same product
+// on the same data gives the same bits wherever it is evaluated (the own trace
+// recomputed by an element equals the trace it published, O28).
 //
-//   kernel A (viscous): U_ext = M0 U, U_u = M12 U, C (l.282-291, neighbour traces),
-//     Q~ = [M16 | M15 P][C; U_u] (l.2877-2880), Q = J^-T Q~ (l.299-302), and the
+//   kernel A (viscous, "volume"): U_ext = M0 U, U_u = M12 U, C (l.282-291, neighbour
+//     traces), Q~ = [M16 | M15 P][C; U_u] (l.2877-2880), Q = J^-T Q~ (l.299-302), the
 //     published viscous normal flux g = n_L . f^v(u, M0 Q) at the face points of the
-//     side carrying LDG weight (l.330-335).
-//   kernel B: the same gradient, Q_u = M18 Q (l.2897-2900), internal fluxes F~ =
-//     detJ J^-1 f (l.305-311), common fluxes D~ = +/- s F (l.312-340, canonical L/R),
-//     R~ = M14 D~ + M13 M19 P2 F~ (l.2919-2925), -R~/detJ, RK4 update, new traces.
-// Face values are exchanged only through double-buffered traces; the own trace is
-// recomputed by the same operator routine (fixed fma order), so both neighbours
-// evaluate each face point's common flux from bit-identical inputs (O28).
+//     LDG-weighted side (l.330-335), Q_u = M18 Q (l.2897-2900), internal fluxes
+//     F~ = detJ J^-1 (f^c - f^v) (l.305-311), R_int = M13 M19 P2 F~ -> HBM.
+//   kernel B ("faces + update"): U_ext = M0 U, common fluxes D~ = +/- s F (l.312-340,
+//     canonical L/R), R~ = R_int + M14 D~ (l.2919-2925) [inviscid: U_u, F~ and M13 F~
+//     here too], -R~/detJ, RK4 update, new traces M0 U_new.
+// Tiles arrive by TMA; face values are exchanged only through double-buffered traces.
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <stdexcept>
 #include <string>
 
 #include "simplex.cuh"
+#include "tma.cuh"
 
 namespace sdrt {
 
@@ -37,112 +42,94 @@ struct SDims {
 template <typename T>
 __host__ __device__ constexpr T cmax(T a, T b) { return a > b ? a : b; }
 
-template <int D, int P, int NV, bool VISC>
-struct SLayout {
-  using S = SDims<D, P>;
-  static constexpr int U = S::nsol * NV;
-  static constexpr int UE = S::next * NV;
-  static constexpr int R0 = cmax(cmax(S::next * NV, VISC ? S::nu * D * NV : 0), S::nsol * NV);
-  static constexpr int UU = S::nu * NV;
-  static constexpr int Q = cmax(VISC ? S::nsol * D * NV : 0, S::nu * D * NV);
-  static constexpr int TOTAL = U + UE + R0 + UU + Q;  // doubles per element
+struct STileMaps {
+  CUtensorMap uin, un, acc, rint;
 };
 
-// Y[r][w][el] (+)= sum_c M[r][c] X[c][w][el], X rows c < split from X0, else X1.
-// W values per row in chunks of WC; one work item = (row block, chunk, element), so
-// every thread of the CTA has work even for short operators.
-template <int W, int E, bool ACCUM>
-__device__ __forceinline__ void sapply(const SOp& M, const double* X0, int split, const double* X1, double* Y) {
-  constexpr int WC = W % 5 == 0 ? 5 : (W % 4 == 0 ? 4 : (W % 3 == 0 ? 3 : (W % 2 == 0 ? 2 : 1)));
-  constexpr int NWC = W / WC;
-  const int nitems = M.nblk * NWC * E;
-  for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
-    const int el = item % E, r2 = item / E;
-    const int w0 = (r2 % NWC) * WC, blk = r2 / NWC;
-    double acc[SRB][WC];
+// ---------------------------------------------------------------- DMMA products
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// largest divisor of n that is <= 5 (n-tiles per warp job)
+__host__ __device__ constexpr int ngroup(int n) {
+  return n % 5 == 0 ? 5 : (n % 4 == 0 ? 4 : (n % 3 == 0 ? 3 : (n % 2 == 0 ? 2 : 1)));
+}
+
+// One operator application Y (+)= M X over a tile: X rows c < split from X0, others
+// from X1 (row stride N = W E doubles); Y rows r < M.rows.  Warp jobs = (m-tile,
+// group of NGR n-tiles); the A fragment of a k step serves the whole group.
+template <int W, int E>
+struct Dmm {
+  static constexpr int N = W * E;
+  static_assert(N % 8 == 0, "tile columns must be a multiple of 8");
+  static constexpr int NT8 = N / 8;
+  static constexpr int NGR = ngroup(NT8);
+  static constexpr int NG = NT8 / NGR;
+
+  __device__ __forceinline__ static int jobs(const SOpF& M) { return M.mt * NG; }
+
+  template <bool ACCUM>
+  __device__ __forceinline__ static void job(const SOpF& M, int j, const double* X0, int split, const double* X1,
+                                             double* Y) {
+    const int lane = threadIdx.x & 31;
+    const int m = j / NG, ng = j % NG;
+    const int n0 = ng * NGR * 8 + (lane >> 2);
+    double c[NGR][2];
 #pragma unroll
-    for (int k = 0; k < SRB; ++k)
+    for (int q = 0; q < NGR; ++q) c[q][0] = c[q][1] = 0.0;
+    const double* af = M.frag + (int64_t)m * M.kt * 32 + lane;
+#pragma unroll 2
+    for (int k = 0; k < M.kt; ++k) {
+      const double a = __ldg(af + k * 32);
+      const int col = 4 * k + (lane & 3);
+      const double* xr = col < split ? X0 + col * N : X1 + (col - split) * N;
+      const bool ok = col < M.cols;
 #pragma unroll
-      for (int w = 0; w < WC; ++w) acc[k][w] = 0.0;
-    const int b = M.ptr[blk], e = M.ptr[blk + 1];
-    for (int j = b; j < e; ++j) {
-      const int c = __ldg(M.col + j);
-      const double* xr = (c < split ? X0 + c * W * E : X1 + (c - split) * W * E) + w0 * E + el;
-      double x[WC];
-#pragma unroll
-      for (int w = 0; w < WC; ++w) x[w] = xr[w * E];
-      const double* mv = M.val + (int64_t)j * SRB;
-#pragma unroll
-      for (int k = 0; k < SRB; ++k) {
-        const double m = __ldg(mv + k);
-#pragma unroll
-        for (int w = 0; w < WC; ++w) acc[k][w] = __fma_rn(m, x[w], acc[k][w]);
+      for (int q = 0; q < NGR; ++q) {
+        const double b = ok ? xr[n0 + 8 * q] : 0.0;
+        dmma(c[q][0], c[q][1], a, b);
       }
     }
+    const int r = 8 * m + (lane >> 2);
+    if (r < M.rows) {
 #pragma unroll
-    for (int k = 0; k < SRB; ++k) {
-      const int r = blk * SRB + k;
-      if (r >= M.rows) break;
-#pragma unroll
-      for (int w = 0; w < WC; ++w) {
-        double* y = Y + (r * W + w0 + w) * E + el;
-        *y = ACCUM ? *y + acc[k][w] : acc[k][w];
+      for (int q = 0; q < NGR; ++q) {
+        double2* y = reinterpret_cast<double2*>(Y + r * N + ng * NGR * 8 + 8 * q + 2 * (lane & 3));
+        if (ACCUM) {
+          const double2 o = *y;
+          *y = make_double2(o.x + c[q][0], o.y + c[q][1]);
+        } else {
+          *y = make_double2(c[q][0], c[q][1]);
+        }
       }
     }
   }
-}
+};
 
-// traces to global: T[r][v][Kp] = (M0 U)[r][v] for valid elements (same fma order as sapply)
-template <int NV, int E>
-__device__ __forceinline__ void strace_global(const SOp& M, const double* X, double* __restrict__ T, int64_t e0,
-                                              int64_t K, int64_t Kp) {
-  const int nitems = M.nblk * E;
-  for (int item = threadIdx.x; item < nitems; item += blockDim.x) {
-    const int el = item % E, blk = item / E;
-    const int64_t e = e0 + el;
-    double acc[SRB][NV];
-#pragma unroll
-    for (int k = 0; k < SRB; ++k)
-#pragma unroll
-      for (int w = 0; w < NV; ++w) acc[k][w] = 0.0;
-    const int b = M.ptr[blk], en = M.ptr[blk + 1];
-    for (int j = b; j < en; ++j) {
-      const int c = __ldg(M.col + j);
-      double x[NV];
-#pragma unroll
-      for (int w = 0; w < NV; ++w) x[w] = X[(c * NV + w) * E + el];
-      const double* mv = M.val + (int64_t)j * SRB;
-#pragma unroll
-      for (int k = 0; k < SRB; ++k) {
-        const double m = __ldg(mv + k);
-#pragma unroll
-        for (int w = 0; w < NV; ++w) acc[k][w] = __fma_rn(m, x[w], acc[k][w]);
-      }
-    }
-    if (e >= K) continue;
-#pragma unroll
-    for (int k = 0; k < SRB; ++k) {
-      const int r = blk * SRB + k;
-      if (r >= M.rows) break;
-#pragma unroll
-      for (int w = 0; w < NV; ++w) T[((int64_t)r * NV + w) * Kp + e] = acc[k][w];
-    }
+// Y1 = M1 X1 (W1 per row) and Y2 = M2 X2 (W2) in one phase (independent products;
+// M2.frag == nullptr skips the second)
+template <int W1, int W2, int E, bool ACC1, bool ACC2>
+__device__ __forceinline__ void dmm2(const SOpF& M1, const double* X1a, int s1, const double* X1b, double* Y1,
+                                     const SOpF& M2, const double* X2a, int s2, const double* X2b, double* Y2) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int j1 = Dmm<W1, E>::jobs(M1), j2 = M2.frag ? Dmm<W2, E>::jobs(M2) : 0;
+  for (int j = warp; j < j1 + j2; j += nw) {
+    if (j < j1) Dmm<W1, E>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
+    else Dmm<W2, E>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
   }
 }
 
-template <int ROWS, int E>
-__device__ __forceinline__ void sload(const double* __restrict__ src, double* s, int64_t e0, int64_t Kp) {
-  constexpr int CH = E / 2;
-  for (int idx = threadIdx.x; idx < ROWS * CH; idx += blockDim.x) {
-    const int c = idx % CH, row = idx / CH;
-    const double* g = src + (int64_t)row * Kp + e0 + 2 * c;
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(s + row * E + 2 * c);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g));
-  }
-  asm volatile("cp.async.commit_group;");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
+template <int W, int E, bool ACC>
+__device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split, const double* X1, double* Y) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nj = Dmm<W, E>::jobs(M);
+  for (int j = warp; j < nj; j += nw) Dmm<W, E>::template job<ACC>(M, j, X0, split, X1, Y);
 }
 
+// ---------------------------------------------------------------- tile helpers
 // neighbour of element e across local face f (pattern arithmetic, periodic)
 __device__ __forceinline__ int snbr(const GeomDev& g, int e, int s, int f) {
   int pat = e / g.nsub;
@@ -150,7 +137,7 @@ __device__ __forceinline__ int snbr(const GeomDev& g, int e, int s, int f) {
 #pragma unroll
   for (int d = 0; d < 3; ++d)
     if (d < g.nd) {
-      c[d] = (int)(pat % g.Nloc[d]);
+      c[d] = pat % g.Nloc[d];
       pat /= g.Nloc[d];
     }
   int id = 0, mul = 1;
@@ -168,7 +155,18 @@ __device__ __forceinline__ int snbr(const GeomDev& g, int e, int s, int f) {
       id += mul * cc;
       mul *= g.Nloc[d];
     }
-  return (int)(id * g.nsub + g.nshape[s][f]);
+  return id * g.nsub + g.nshape[s][f];
+}
+
+// neighbour ids sNb[f][el] and sub-cell shapes sNb[D+1][el] of a tile, once
+template <int D, int E>
+__device__ __forceinline__ void fill_neighbours(const GeomDev& g, int (*sNb)[E], int64_t e0) {
+  for (int idx = threadIdx.x; idx < (D + 2) * E; idx += blockDim.x) {
+    const int el = idx % E, f = idx / E;
+    const int e = (int)e0 + el;
+    const int s = e % g.nsub;
+    sNb[f][el] = f == D + 1 ? s : (e < g.K ? snbr(g, e, s, f) : 0);
+  }
 }
 
 // C = (1/2 - b) u_L + (1/2 + b) u_R at external points into sC [next][NV][E]
@@ -181,7 +179,11 @@ __device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& p
   for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
-    if (e >= g.K) continue;
+    if (e >= g.K) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sC[(rho * NV + v) * E + el] = 0.0;
+      continue;
+    }
     const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
     const int m = sNb[f][el];
     const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
@@ -221,175 +223,229 @@ __device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E
   }
 }
 
-// neighbour ids sNb[f][el] and sub-cell shapes sNb[D+1][el] of a tile, once
-template <int D, int E>
-__device__ __forceinline__ void fill_neighbours(const GeomDev& g, int (*sNb)[E], int64_t e0) {
-  for (int idx = threadIdx.x; idx < (D + 2) * E; idx += blockDim.x) {
-    const int el = idx % E, f = idx / E;
-    const int e = (int)e0 + el;
-    const int s = e % g.nsub;
-    sNb[f][el] = f == D + 1 ? s : (e < g.K ? snbr(g, e, s, f) : 0);
-  }
-}
-
-// shared prologue: tile, own traces, U_u, [C, Q]
+// internal transformed fluxes for all D components (B7: simplices keep all) at the
+// unique internal points: F~[d][u] = detJ (J^-1 (f^c - f^v))_d -> sF [D][nu][NV][E]
 template <int D, int P, int EQ, int E>
-__device__ __forceinline__ void prologue(const GeomDev& g, const SimplexOps& O, const PhysDev& ph,
-                                         const double* Uin, const double* Tu, double* smem, int (*sNb)[E],
-                                         int64_t e0) {
+__device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev& ph, const int (*sNb)[E],
+                                                const double* sUu, const double* sQu, double* sF, int64_t e0) {
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
-  using Ly = SLayout<D, P, Ph::NV, Ph::VISC>;
   constexpr int NV = Ph::NV;
-  double* sU = smem;
-  double* sUe = sU + Ly::U * E;
-  double* sR0 = sUe + Ly::UE * E;
-  double* sUu = sR0 + Ly::R0 * E;
-  double* sQ = sUu + Ly::UU * E;
-  fill_neighbours<D, E>(g, sNb, e0);
-  sload<S::nsol * NV, E>(Uin, sU, e0, g.Kp);
-  __syncthreads();
-  sapply<NV, E, false>(O.M0, sU, 1 << 30, sU, sUe);
-  sapply<NV, E, false>(O.M12, sU, 1 << 30, sU, sUu);
-  __syncthreads();
-  if constexpr (Ph::VISC) {
-    common_values<D, P, NV, E>(g, ph, Tu, sUe, sNb, sR0, e0);
-    __syncthreads();
-    sapply<NV, E, false>(O.G, sR0, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
-    __syncthreads();
-    metric_grad<D, P, NV, E>(g, sNb, sQ);
-    __syncthreads();
-  }
-}
-
-template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const double* __restrict__ U,
-                                                 double* __restrict__ T) {
-  constexpr int NV = Phys<EQ, D>::NV;
-  extern __shared__ double smem[];
-  const int64_t e0 = (int64_t)blockIdx.x * E;
-  sload<SDims<D, P>::nsol * NV, E>(U, smem, e0, g.Kp);
-  __syncthreads();
-  strace_global<NV, E>(O.M0, smem, T, e0, g.K, g.Kt);
-}
-
-template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b) {
-  using Ph = Phys<EQ, D>;
-  using S = SDims<D, P>;
-  using Ly = SLayout<D, P, Ph::NV, Ph::VISC>;
-  constexpr int NV = Ph::NV;
-  extern __shared__ double smem[];
-  __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
-  const int64_t e0 = (int64_t)blockIdx.x * E;
-  prologue<D, P, EQ, E>(g, O, ph, b.Uin, b.Tu, smem, sNb, e0);
-  const double* sUe = smem + Ly::U * E;
-  const double* sQ = smem + (Ly::U + Ly::UE + Ly::R0 + Ly::UU) * E;
-  const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
-  const int Kp = (int)g.Kt;  // trace row stride
-  // RP face points per item (same face): the gradient tile entries loaded for one
-  // point serve RP rows of M0
-  constexpr int RP = S::nfp % 2 == 0 ? 2 : 1;
-  for (int item = threadIdx.x; item < (S::next / RP) * E; item += blockDim.x) {
-    const int el = item % E, rho0 = (item / E) * RP;
-    const int64_t e = e0 + el;
-    if (e >= g.K) continue;
-    const int s = sNb[D + 1][el], f = rho0 / S::nfp;
-    const bool left = g.left[s][f];
-    if ((left && !pub_left) || (!left && !pub_right)) continue;
-    double q[RP][D * NV];
-#pragma unroll
-    for (int r = 0; r < RP; ++r)
-#pragma unroll
-      for (int k = 0; k < D * NV; ++k) q[r][k] = 0.0;
-    const double* m0 = O.M0dense + rho0 * S::nsol;
-#pragma unroll 2
-    for (int sp = 0; sp < S::nsol; ++sp) {
-      double m[RP];
-#pragma unroll
-      for (int r = 0; r < RP; ++r) m[r] = __ldg(m0 + r * S::nsol + sp);
-#pragma unroll
-      for (int k = 0; k < D * NV; ++k) {
-        const double x = sQ[(sp * D * NV + k) * E + el];
-#pragma unroll
-        for (int r = 0; r < RP; ++r) q[r][k] = fma(m[r], x, q[r][k]);
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < RP; ++r) {
-      const int rho = rho0 + r;
-      double u[NV];
-#pragma unroll
-      for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
-      const ExtMetric mt = b.xm[s * S::next + rho];
-      const double nl[3] = {mt.n0, mt.n1, mt.n2};
-      double gv[NV];
-      Ph::visc_dir(ph, u, q[r], nl, gv);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
-    }
-  }
-}
-
-template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
-                                                double dt) {
-  using Ph = Phys<EQ, D>;
-  using S = SDims<D, P>;
-  using Ly = SLayout<D, P, Ph::NV, Ph::VISC>;
-  constexpr int NV = Ph::NV;
-  extern __shared__ double smem[];
-  __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
-  const int64_t e0 = (int64_t)blockIdx.x * E;
-  prologue<D, P, EQ, E>(g, O, ph, b.Uin, b.Tu, smem, sNb, e0);
-  double* sU = smem;
-  double* sUe = sU + Ly::U * E;
-  double* sR0 = sUe + Ly::UE * E;
-  double* sUu = sR0 + Ly::R0 * E;
-  double* sQ = sUu + Ly::UU * E;
-  const int Kp = (int)g.Kt;  // trace row stride
-  if constexpr (Ph::VISC) {
-    // Q_u = M18 Q (M12 on each of the D*NV gradient rows), into region 0 (C is dead)
-    sapply<D * NV, E, false>(O.M12, sQ, 1 << 30, sQ, sR0);
-    __syncthreads();
-  }
-  // internal transformed fluxes for all D components (B7: simplex keeps all), into sQ
-  double* sF = sQ;  // [D][nu][NV][E]
   for (int item = threadIdx.x; item < S::nu * E; item += blockDim.x) {
     const int el = item % E, u = item / E;
+    if (e0 + el >= g.K) {  // padding columns: finite zeros
+#pragma unroll
+      for (int d = 0; d < D; ++d)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = 0.0;
+      continue;
+    }
     const int s = sNb[D + 1][el];
     double uu[NV], qq[Ph::VISC ? D * NV : 1];
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = sUu[(u * NV + v) * E + el];
     if constexpr (Ph::VISC) {
 #pragma unroll
-      for (int k = 0; k < D * NV; ++k) qq[k] = sR0[(u * D * NV + k) * E + el];
+      for (int k = 0; k < D * NV; ++k) qq[k] = sQu[(u * D * NV + k) * E + el];
     }
-    double fo[D][NV];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
-      double w[D];
+      double w[D], fo[NV];
 #pragma unroll
       for (int j = 0; j < D; ++j) w[j] = g.detJ[s] * g.Jinv[s][d * 3 + j];
-      Ph::conv_dir(ph, uu, w, fo[d]);
+      Ph::conv_dir(ph, uu, w, fo);
       if constexpr (Ph::VISC) {
         double fv[NV];
         Ph::visc_dir(ph, uu, qq, w, fv);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) fo[d][v] += fv[v];
+        for (int v = 0; v < NV; ++v) fo[v] += fv[v];
       }
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = fo[v];
     }
-#pragma unroll
-    for (int d = 0; d < D; ++d)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = fo[d][v];
   }
-  // common fluxes D~ = +/- s F at external points, in place over the own traces
-  const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+}
+
+// rows [ROWS][E] of a tile in smem -> global T[row][ld] (element columns e0..)
+template <int ROWS, int E>
+__device__ __forceinline__ void store_rows(const GeomDev& g, const double* sY, double* __restrict__ T, int64_t ld,
+                                           int64_t e0) {
+  for (int idx = threadIdx.x; idx < ROWS * E; idx += blockDim.x) {
+    const int el = idx % E, r = idx / E;
+    if (e0 + el < g.K) T[(int64_t)r * ld + e0 + el] = sY[idx];
+  }
+}
+
+// ---------------------------------------------------------------- kernels
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const __grid_constant__ STileMaps tm,
+                                                 double* __restrict__ T) {
+  using S = SDims<D, P>;
+  constexpr int NV = Phys<EQ, D>::NV;
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;
+  double* sUe = smem + S::nsol * NV * E;
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, S::nsol * NV * E * 8);
+    tma_tile<S::nsol * NV, E>(sU, &tm.uin, e0, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  dmm1<NV, E, false>(O.M0, sU, 1 << 30, sU, sUe);
+  __syncthreads();
+  store_rows<S::next * NV, E>(g, sUe, T, g.Kt, e0);
+}
+
+// Kernel A.  Shared-memory regions (doubles per element) by liveness:
+//   X  [max(nsol NV, next D NV, D nu NV)]: U, then C, then Q_ext, then F~
+//   UE [max(next NV, nu D NV)]: U_ext, then Q_u
+//   UU [nu NV]: U_u
+//   Q  [nsol D NV]: Q, then R_int (nsol NV)
+template <int D, int P, int NV>
+struct SLayoutA {
+  using S = SDims<D, P>;
+  static constexpr int X = cmax(cmax(S::nsol * NV, S::next * D * NV), S::nu * D * NV);
+  static constexpr int UE = cmax(S::next * NV, S::nu * D * NV);
+  static constexpr int UU = S::nu * NV;
+  static constexpr int Q = S::nsol * D * NV;
+  static constexpr int TOTAL = X + UE + UU + Q;
+};
+
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
+                                               const __grid_constant__ STileMaps tm) {
+  using Ph = Phys<EQ, D>;
+  using S = SDims<D, P>;
+  using Ly = SLayoutA<D, P, Ph::NV>;
+  constexpr int NV = Ph::NV;
+  extern __shared__ __align__(128) double smem[];
+  double* sX = smem;
+  double* sUe = sX + Ly::X * E;
+  double* sUu = sUe + Ly::UE * E;
+  double* sQ = sUu + Ly::UU * E;
+  __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, S::nsol * NV * E * 8);
+    tma_tile<S::nsol * NV, E>(sX, &tm.uin, e0, &bar);
+  }
+  fill_neighbours<D, E>(g, sNb, e0);
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  // U_ext = M0 U, U_u = M12 U
+  dmm2<NV, NV, E, false, false>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30, sX, sUu);
+  __syncthreads();
+  common_values<D, P, NV, E>(g, ph, b.Tu, sUe, sNb, sX, e0);  // C into X (U is dead)
+  __syncthreads();
+  dmm1<NV, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
+  __syncthreads();
+  metric_grad<D, P, NV, E>(g, sNb, sQ);
+  __syncthreads();
+  // gradient at the external points (M0 on each of the D NV gradient rows) into X
+  dmm1<D * NV, E, false>(O.M0, sQ, 1 << 30, sQ, sX);
+  __syncthreads();
+  // publish g at the face points of the LDG-weighted side
+  const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
+  const int Kp = (int)g.Kt;  // trace row stride
   for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
     if (e >= g.K) continue;
+    const int s = sNb[D + 1][el], f = rho / S::nfp;
+    const bool left = g.left[s][f];
+    if ((left && !pub_left) || (!left && !pub_right)) continue;
+    double u[NV], q[D * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
+#pragma unroll
+    for (int k = 0; k < D * NV; ++k) q[k] = sX[(rho * D * NV + k) * E + el];
+    const ExtMetric mt = b.xm[s * S::next + rho];
+    const double nl[3] = {mt.n0, mt.n1, mt.n2};
+    double gv[NV];
+    Ph::visc_dir(ph, u, q, nl, gv);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
+  }
+  __syncthreads();
+  dmm1<D * NV, E, false>(O.M12, sQ, 1 << 30, sQ, sUe);  // Q_u = M18 Q [nu][D NV] into UE
+  __syncthreads();
+  internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
+  __syncthreads();
+  dmm1<NV, E, false>(O.M13F, sX, 1 << 30, sX, sQ);  // R_int into Q (Q is dead)
+  __syncthreads();
+  store_rows<S::nsol * NV, E>(g, sQ, b.Rint, g.Kp, e0);
+}
+
+// Kernel B.  Regions (doubles per element): U [nsol NV] (stage input), R [nsol NV]
+// (R_int, accumulated), UN, ACC [nsol NV] (RK registers), UE [next NV] (own traces,
+// then D~, then the new traces); inviscid: UU [nu NV], F [D nu NV].
+template <int D, int P, int NV, bool INT>
+struct SLayoutB {
+  using S = SDims<D, P>;
+  static constexpr int U = S::nsol * NV;
+  static constexpr int UE = S::next * NV;
+  static constexpr int UU = INT ? S::nu * NV : 0;
+  static constexpr int F = INT ? D * S::nu * NV : 0;
+  static constexpr int TOTAL = 4 * U + UE + UU + F;
+};
+
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
+                                                double dt, const __grid_constant__ STileMaps tm) {
+  using Ph = Phys<EQ, D>;
+  using S = SDims<D, P>;
+  constexpr bool INT = !Ph::VISC;  // internal fluxes evaluated here (inviscid only)
+  using Ly = SLayoutB<D, P, Ph::NV, INT>;
+  constexpr int NV = Ph::NV;
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;
+  double* sR = sU + Ly::U * E;
+  double* sUn = sR + Ly::U * E;
+  double* sAcc = sUn + Ly::U * E;
+  double* sUe = sAcc + Ly::U * E;
+  double* sUu = sUe + Ly::UE * E;
+  double* sF = sUu + Ly::UU * E;
+  __shared__ int sNb[D + 2][E];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  constexpr unsigned TB = S::nsol * NV * E * 8;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar[0], TB);
+    tma_tile<S::nsol * NV, E>(sU, &tm.uin, e0, &bar[0]);
+    const unsigned later = (INT ? 0 : TB) + ((stage == 1 || stage == 2) ? TB : 0) + (stage >= 1 ? TB : 0);
+    mbar_expect_tx(&bar[1], later);
+    if constexpr (!INT) tma_tile<S::nsol * NV, E>(sR, &tm.rint, e0, &bar[1]);
+    if (stage == 1 || stage == 2) tma_tile<S::nsol * NV, E>(sUn, &tm.un, e0, &bar[1]);
+    if (stage >= 1) tma_tile<S::nsol * NV, E>(sAcc, &tm.acc, e0, &bar[1]);
+  }
+  fill_neighbours<D, E>(g, sNb, e0);
+  __syncthreads();
+  mbar_wait(&bar[0], 0);
+  // own traces (and, inviscid, U_u)
+  const SOpF none{0, 0, 0, 0, nullptr};
+  dmm2<NV, NV, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, INT ? O.M12 : none, sU, 1 << 30, sU, sUu);
+  __syncthreads();
+  // common fluxes D~ = +/- s F at external points, in place over the own traces
+  const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+  const int Kp = (int)g.Kt;  // trace row stride
+  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
+    const int el = item % E, rho = item / E;
+    const int64_t e = e0 + el;
+    if (e >= g.K) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sUe[(rho * NV + v) * E + el] = 0.0;
+      continue;
+    }
     const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
     const int m = sNb[f][el];
     const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
@@ -427,78 +483,72 @@ __global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev
       sUe[(rho * NV + v) * E + el] = sc * Fv;
     }
   }
+  if constexpr (INT) internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, nullptr, sF, e0);
+  mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed
   __syncthreads();
-  // R~ = [M14 | M13 M19 P2] [D~; F~]  into region 0
-  sapply<NV, E, false>(O.M14, sUe, 1 << 30, sUe, sR0);
-  sapply<NV, E, true>(O.M13F, sF, 1 << 30, sF, sR0);
+  // R~ = R_int + M14 D~ [+ M13 M19 P2 F~]
+  if constexpr (INT) {
+    dmm1<NV, E, false>(O.M14, sUe, 1 << 30, sUe, sR);
+    __syncthreads();
+    dmm1<NV, E, true>(O.M13F, sF, 1 << 30, sF, sR);
+  } else {
+    dmm1<NV, E, true>(O.M14, sUe, 1 << 30, sUe, sR);
+  }
   __syncthreads();
-  // -R~/detJ and the RK4 update (batched register loads)
-  constexpr int TOT = S::nsol * NV * E;
-  constexpr int RB_RK = 4;
-  const int nth = blockDim.x;
-  for (int base0 = threadIdx.x; base0 < TOT; base0 += RB_RK * nth) {
-    double a0[RB_RK], a1[RB_RK];
-    int64_t gi[RB_RK];
-    bool ok[RB_RK];
-#pragma unroll
-    for (int k = 0; k < RB_RK; ++k) {
-      const int idx = base0 + k * nth;
-      const int el = idx % E, row = idx / E;
-      ok[k] = idx < TOT && e0 + el < g.K;
-      gi[k] = (int64_t)row * g.Kp + e0 + el;
-      a0[k] = 0.0;
-      a1[k] = 0.0;
-      if (ok[k]) {
-        if (stage >= 1) a0[k] = __ldcs(b.ACC + gi[k]);
-        if (stage == 1 || stage == 2) a1[k] = __ldcs(b.U + gi[k]);
-      }
+  // -R~/detJ and the RK4 update (registers from shared memory), new state into sU
+  for (int idx = threadIdx.x; idx < S::nsol * NV * E; idx += blockDim.x) {
+    const int el = idx % E, row = idx / E;
+    const int64_t e = e0 + el;
+    if (e >= g.K) {
+      sU[idx] = 0.0;
+      continue;
     }
-#pragma unroll
-    for (int k = 0; k < RB_RK; ++k) {
-      if (!ok[k]) continue;
-      const int idx = base0 + k * nth;
-      const int el = idx % E;
-      const int s = sNb[D + 1][el];
-      const double kk = -sR0[idx] / g.detJ[s];
-      double nu;
-      switch (stage) {
-        case -1: b.out[gi[k]] = kk; nu = 0.0; break;
-        case 0: {
-          const double u0 = sU[idx];
-          b.ACC[gi[k]] = fma(dt / 6.0, kk, u0);
-          nu = fma(0.5 * dt, kk, u0);
-          b.Us[gi[k]] = nu;
-        } break;
-        case 1:
-          b.ACC[gi[k]] = fma(dt / 3.0, kk, a0[k]);
-          nu = fma(0.5 * dt, kk, a1[k]);
-          b.Us[gi[k]] = nu;
-          break;
-        case 2:
-          b.ACC[gi[k]] = fma(dt / 3.0, kk, a0[k]);
-          nu = fma(dt, kk, a1[k]);
-          b.Us[gi[k]] = nu;
-          break;
-        default:
-          nu = fma(dt / 6.0, kk, a0[k]);
-          b.U[gi[k]] = nu;
-          break;
-      }
-      sU[idx] = nu;
+    const int64_t gi = (int64_t)row * g.Kp + e;
+    const int s = sNb[D + 1][el];
+    const double kk = -sR[idx] / g.detJ[s];
+    double nu;
+    switch (stage) {
+      case -1: b.out[gi] = kk; nu = 0.0; break;
+      case 0: {
+        const double u0 = sU[idx];
+        b.ACC[gi] = fma(dt / 6.0, kk, u0);
+        nu = fma(0.5 * dt, kk, u0);
+        b.Us[gi] = nu;
+      } break;
+      case 1:
+        b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+        nu = fma(0.5 * dt, kk, sUn[idx]);
+        b.Us[gi] = nu;
+        break;
+      case 2:
+        b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+        nu = fma(dt, kk, sUn[idx]);
+        b.Us[gi] = nu;
+        break;
+      default:
+        nu = fma(dt / 6.0, kk, sAcc[idx]);
+        b.U[gi] = nu;
+        break;
     }
+    sU[idx] = nu;
   }
   if (stage < 0) return;
   __syncthreads();
-  strace_global<NV, E>(O.M0, sU, b.Tu_next, e0, g.K, g.Kt);
+  dmm1<NV, E, false>(O.M0, sU, 1 << 30, sU, sUe);  // traces of the new state
+  __syncthreads();
+  store_rows<S::next * NV, E>(g, sUe, b.Tu_next, g.Kt, e0);
 }
 
 // ------------------------------------------------------------------ launchers
 template <int D, int P, int EQ>
 struct SCfg {
-  static constexpr int E = 16;
+  static constexpr int NV = Phys<EQ, D>::NV;
+  static constexpr bool VISC = Phys<EQ, D>::VISC;
+  static constexpr int E = 8;  // tile width: MMA rows hold NV E (a multiple of 8) columns
   static constexpr int THREADS = 256;
-  using Ly = SLayout<D, P, Phys<EQ, D>::NV, Phys<EQ, D>::VISC>;
-  static constexpr size_t SMEM = (size_t)Ly::TOTAL * E * sizeof(double);
+  static constexpr size_t SMEM_A = (size_t)SLayoutA<D, P, NV>::TOTAL * E * sizeof(double);
+  static constexpr size_t SMEM_B = (size_t)SLayoutB<D, P, NV, !VISC>::TOTAL * E * sizeof(double);
+  static constexpr size_t SMEM_T = (size_t)(SDims<D, P>::nsol + SDims<D, P>::next) * NV * E * sizeof(double);
 };
 
 static void sset_smem(const void* k, size_t bytes) {
@@ -508,78 +558,113 @@ static void sset_smem(const void* k, size_t bytes) {
   }
 }
 
+static STileMaps smaps(SimplexTma* t, const SimplexBufs& b, const double* uin, bool full) {
+  STileMaps m;
+  std::memset(&m, 0, sizeof(m));
+  m.uin = cached_tile_map(t, uin);
+  if (full) {
+    if (b.U) m.un = cached_tile_map(t, b.U);
+    if (b.ACC) m.acc = cached_tile_map(t, b.ACC);
+    if (b.Rint) m.rint = cached_tile_map(t, b.Rint);
+  }
+  return m;
+}
+
 template <int D, int P, int EQ>
-static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, const SimplexBufs& b, int stage,
-                 double dt, cudaStream_t st, int which, const double* U, double* T) {
+static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, SimplexTma* tma, const SimplexBufs& b,
+                 int stage, double dt, cudaStream_t st, int which, const double* U, double* T) {
   using C = SCfg<D, P, EQ>;
   const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
   if (which == 0) {
     if constexpr (Phys<EQ, D>::VISC) {
       auto k = ks_grad<D, P, EQ, C::E>;
-      sset_smem((const void*)k, C::SMEM);
-      k<<<grid, C::THREADS, C::SMEM, st>>>(g, O, ph, b);
+      sset_smem((const void*)k, C::SMEM_A);
+      k<<<grid, C::THREADS, C::SMEM_A, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
     }
   } else if (which == 1) {
     auto k = ks_stage<D, P, EQ, C::E>;
-    sset_smem((const void*)k, C::SMEM);
-    k<<<grid, C::THREADS, C::SMEM, st>>>(g, O, ph, b, stage, dt);
+    sset_smem((const void*)k, C::SMEM_B);
+    k<<<grid, C::THREADS, C::SMEM_B, st>>>(g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true));
   } else {
     auto k = ks_traces<D, P, EQ, C::E>;
-    const size_t sm = (size_t)SDims<D, P>::nsol * Phys<EQ, D>::NV * C::E * sizeof(double);
-    sset_smem((const void*)k, sm);
-    k<<<grid, C::THREADS, sm, st>>>(g, O, U, T);
+    sset_smem((const void*)k, C::SMEM_T);
+    k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, O, smaps(tma, b, U, false), T);
   }
 }
 
-typedef void (*SFn)(const GeomDev&, const SimplexOps&, const PhysDev&, const SimplexBufs&, int, double,
+template <int D, int P, int EQ>
+static void stma(SimplexTma* t, int64_t Kp) {
+  using C = SCfg<D, P, EQ>;
+  t->rows = SDims<D, P>::nsol * C::NV;
+  t->E = C::E;
+  t->Kp = Kp;
+  for (int i = 0; i < 8; ++i) t->ptr[i] = nullptr;
+  t->next = 0;
+}
+
+typedef void (*SFn)(const GeomDev&, const SimplexOps&, const PhysDev&, SimplexTma*, const SimplexBufs&, int, double,
                     cudaStream_t, int, const double*, double*);
+typedef void (*STmaFn)(SimplexTma*, int64_t);
 
 template <int D, int P>
-static SFn spick_eq(int eq) {
+static SFn spick_eq(int eq, STmaFn* m) {
   switch (eq) {
-    case EQ_LINADV: return srun<D, P, EQ_LINADV>;
-    case EQ_LINADVDIFF: return srun<D, P, EQ_LINADVDIFF>;
-    case EQ_EULER: return srun<D, P, EQ_EULER>;
-    case EQ_NS: return srun<D, P, EQ_NS>;
+    case EQ_LINADV: *m = stma<D, P, EQ_LINADV>; return srun<D, P, EQ_LINADV>;
+    case EQ_LINADVDIFF: *m = stma<D, P, EQ_LINADVDIFF>; return srun<D, P, EQ_LINADVDIFF>;
+    case EQ_EULER: *m = stma<D, P, EQ_EULER>; return srun<D, P, EQ_EULER>;
+    case EQ_NS: *m = stma<D, P, EQ_NS>; return srun<D, P, EQ_NS>;
   }
   return nullptr;
 }
 
-static SFn spick(int D, int P, int eq) {
+static SFn spick(int D, int P, int eq, STmaFn* m) {
+  *m = nullptr;
   if (D == 2) {
     switch (P) {
-      case 1: return spick_eq<2, 1>(eq);
-      case 2: return spick_eq<2, 2>(eq);
-      case 3: return spick_eq<2, 3>(eq);
-      case 4: return spick_eq<2, 4>(eq);
+      case 1: return spick_eq<2, 1>(eq, m);
+      case 2: return spick_eq<2, 2>(eq, m);
+      case 3: return spick_eq<2, 3>(eq, m);
+      case 4: return spick_eq<2, 4>(eq, m);
     }
   } else {
     switch (P) {
-      case 1: return spick_eq<3, 1>(eq);
-      case 2: return spick_eq<3, 2>(eq);
-      case 3: return spick_eq<3, 3>(eq);
+      case 1: return spick_eq<3, 1>(eq, m);
+      case 2: return spick_eq<3, 2>(eq, m);
+      case 3: return spick_eq<3, 3>(eq, m);
     }
   }
   return nullptr;
 }
 
-bool simplex_supported(int D, int P, int eq) { return spick(D, P, eq) != nullptr; }
+bool simplex_supported(int D, int P, int eq) {
+  STmaFn m;
+  return spick(D, P, eq, &m) != nullptr;
+}
 
-void simplex_launch_traces(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, const double* U,
-                           double* Tu, cudaStream_t st) {
+void simplex_tma_init(SimplexTma* t, int D, int P, int eq, int64_t Kp) {
+  STmaFn m;
+  spick(D, P, eq, &m);
+  m(t, Kp);
+}
+
+void simplex_launch_traces(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, SimplexTma* tma,
+                           const double* U, double* Tu, cudaStream_t st) {
   SimplexBufs b{};
   PhysDev ph{};
-  spick(D, P, eq)(g, O, ph, b, 0, 0.0, st, 2, U, Tu);
+  STmaFn m;
+  spick(D, P, eq, &m)(g, O, ph, tma, b, 0, 0.0, st, 2, U, Tu);
 }
 
 void simplex_launch_grad(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, const PhysDev& ph,
-                         const SimplexBufs& b, cudaStream_t st) {
-  spick(D, P, eq)(g, O, ph, b, 0, 0.0, st, 0, nullptr, nullptr);
+                         SimplexTma* tma, const SimplexBufs& b, cudaStream_t st) {
+  STmaFn m;
+  spick(D, P, eq, &m)(g, O, ph, tma, b, 0, 0.0, st, 0, nullptr, nullptr);
 }
 
 void simplex_launch_flux(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, const PhysDev& ph,
-                         const SimplexBufs& b, int stage, double dt, cudaStream_t st) {
-  spick(D, P, eq)(g, O, ph, b, stage, dt, st, 1, nullptr, nullptr);
+                         SimplexTma* tma, const SimplexBufs& b, int stage, double dt, cudaStream_t st) {
+  STmaFn m;
+  spick(D, P, eq, &m)(g, O, ph, tma, b, stage, dt, st, 1, nullptr, nullptr);
 }
 
 }  // namespace sdrt

@@ -1,5 +1,6 @@
 // Fused SDRT stage for simplex elements (tri / tet), sm_100a, fp64.
 #pragma once
+#include <cuda.h>  // CUtensorMap (TMA descriptors)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -9,23 +10,21 @@
 
 namespace sdrt {
 
-constexpr int SRB = 4;  // rows per register block of the dense operator products
-
-// Dense App. B operator in row blocks of SRB rows with the block's non-zero columns.
-struct SOp {
-  int rows, cols, nblk;
-  const int* ptr;      // [nblk+1]
-  const int* col;      // [nnz]
-  const double* val;   // [nnz][SRB]
+// Dense App. B operator packed for the FP64 tensor-core MMA (mma.sync m8n8k4 f64):
+// zero-padded to R8 = 8*mt rows and C4 = 4*kt columns, stored fragment by fragment,
+// frag[(m * kt + k) * 32 + lane] = M[8 m + lane/4][4 k + lane%4], so one warp-wide
+// 256-byte coalesced load fetches one A fragment.
+struct SOpF {
+  int rows, cols, mt, kt;
+  const double* frag;
 };
 
 struct SimplexOps {
-  SOp M0;    // N_ext x N_sol
-  SOp M12;   // N_u x N_sol
-  SOp G;     // (N_sol*D) x (N_ext + N_u): rows (s, d), [M16 | M15 P]
-  SOp M14;   // N_sol x N_ext
-  SOp M13F;  // N_sol x (D N_u): M13 M19 P2, columns (d, u)
-  const double* M0dense;  // N_ext x N_sol (row-major) for per-point gradient traces
+  SOpF M0;    // N_ext x N_sol
+  SOpF M12;   // N_u x N_sol
+  SOpF G;     // (N_sol*D) x (N_ext + N_u): rows (s, d), [M16 | M15 P]
+  SOpF M14;   // N_sol x N_ext
+  SOpF M13F;  // N_sol x (D N_u): M13 M19 P2, columns (d, u)
 };
 
 struct SimplexBufs {
@@ -37,15 +36,28 @@ struct SimplexBufs {
   const double* Tu;
   double* Tu_next;
   double* Tg;
-  const ExtMetric* xm;  // [nsub][N_ext]
+  double* Rint;          // internal-flux divergence M13 M19 P2 F~ [N_sol][N_V][Kp] (kernel A -> B)
+  const ExtMetric* xm;   // [nsub][N_ext]
+};
+
+// TMA descriptors of [N_sol N_V rows][Kp] arrays (cached per pointer), tiles of E elements
+struct SimplexTma {
+  int rows = 0, E = 0;
+  int64_t Kp = 0;
+  const void* ptr[8] = {};
+  CUtensorMap map[8];
+  int next = 0;
 };
 
 bool simplex_supported(int D, int P, int eq);
-void simplex_launch_traces(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, const double* U,
-                           double* Tu, cudaStream_t st);
+void simplex_tma_init(SimplexTma* t, int D, int P, int eq, int64_t Kp);
+void simplex_launch_traces(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, SimplexTma* tma,
+                           const double* U, double* Tu, cudaStream_t st);
+// kernel A (viscous): gradient, published viscous traces, internal fluxes -> Rint
 void simplex_launch_grad(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, const PhysDev& ph,
-                         const SimplexBufs& b, cudaStream_t st);
+                         SimplexTma* tma, const SimplexBufs& b, cudaStream_t st);
+// kernel B: face fluxes, M14 lift (+ internal fluxes for inviscid equations), RK, traces
 void simplex_launch_flux(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, const PhysDev& ph,
-                         const SimplexBufs& b, int stage, double dt, cudaStream_t st);
+                         SimplexTma* tma, const SimplexBufs& b, int stage, double dt, cudaStream_t st);
 
 }  // namespace sdrt

@@ -30,6 +30,7 @@
 #include <string>
 
 #include "tensor.cuh"
+#include "tma.cuh"
 
 namespace sdrt {
 
@@ -114,49 +115,6 @@ __device__ __forceinline__ double interp_end(const double (&Iend)[TMAXP + 1], co
 struct TileMaps {
   CUtensorMap uin, un, acc, rv;  // stage input, u_n, RK accumulator, R_int
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  unsigned ok = 0;
-  do {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-// 2-D tile {E columns (elements), box rows} at (x = first element, y = first row)
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// rows per TMA box: the largest divisor of the row count that is <= 256
-__host__ __device__ constexpr int tma_box_rows(int rows) {
-  int b = rows < 256 ? rows : 256;
-  while (rows % b) --b;
-  return b;
-}
-
-// whole tile [ROWS][E] of one array, issued by one thread, completing on bar
-template <int ROWS, int E>
-__device__ __forceinline__ void tma_tile(double* dst, const CUtensorMap* map, int64_t e0, uint64_t* bar) {
-  constexpr int BR = tma_box_rows(ROWS);
-#pragma unroll
-  for (int r = 0; r < ROWS; r += BR) tma_load_2d(dst + r * E, map, (int)e0, r, bar);
-}
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
@@ -758,35 +716,7 @@ static void set_smem(const void* k, size_t bytes) {
   }
 }
 
-// TMA descriptor of array ptr (cached per pointer)
-static const CUtensorMap& tma_map(TensorTma* t, const void* ptr) {
-  for (int i = 0; i < 8; ++i)
-    if (t->ptr[i] == ptr) return t->map[i];
-  typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn enc = nullptr;
-  if (!enc) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      throw std::runtime_error("CUDA: cuTensorMapEncodeTiled unavailable");
-    enc = (EncodeFn)fn;
-  }
-  const int i = t->next;
-  t->next = (t->next + 1) % 8;
-  cuuint64_t dims[2] = {(cuuint64_t)t->Kp, (cuuint64_t)t->rows};
-  cuuint64_t strides[1] = {(cuuint64_t)t->Kp * sizeof(double)};
-  cuuint32_t box[2] = {(cuuint32_t)t->E, (cuuint32_t)t->box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = enc(&t->map[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  t->ptr[i] = ptr;
-  return t->map[i];
-}
+static const CUtensorMap& tma_map(TensorTma* t, const void* ptr) { return cached_tile_map(t, ptr); }
 
 static TileMaps maps_for(TensorTma* t, const TensorBufs& b, bool full) {
   TileMaps m;
@@ -835,7 +765,6 @@ template <int D, int P, int EQ>
 static void init_tma(TensorTma* t, int64_t Kp) {
   using C = TCfg<D, P, EQ>;
   t->rows = C::NS * C::NV;
-  t->box_rows = tma_box_rows(t->rows);
   t->E = C::E;
   t->Kp = Kp;
   for (int i = 0; i < 8; ++i) t->ptr[i] = nullptr;

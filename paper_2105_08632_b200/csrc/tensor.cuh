@@ -51,7 +51,7 @@ struct TensorBufs {
 // the fused kernels: 2-D tiles of E elements x box_rows rows land in shared memory in
 // the kernels' own [row][E] layout.  Encoded on the host per array pointer (cached).
 struct TensorTma {
-  int rows = 0, box_rows = 0, E = 0;
+  int rows = 0, E = 0;
   int64_t Kp = 0;
   const void* ptr[8] = {};
   CUtensorMap map[8];
