@@ -8,12 +8,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 PROF = os.environ.get("SDRT_PHASE_PROF") == "1"  # tools-only phase-cycle build
-OUT = os.path.join(HERE, "libsdrt_prof.so" if PROF else "libsdrt.so")
-BUILD = os.path.join(HERE, "build_prof" if PROF else "build")
+# tools-only tuning variants: SDRT_VARIANT=name SDRT_DEFS="-DFOO=1" -> libsdrt_<name>.so
+VARIANT = os.environ.get("SDRT_VARIANT", "prof" if PROF else "")
+EXTRA_DEFS = os.environ.get("SDRT_DEFS", "").split()
+OUT = os.path.join(HERE, f"libsdrt_{VARIANT}.so" if VARIANT else "libsdrt.so")
+BUILD = os.path.join(HERE, f"build_{VARIANT}" if VARIANT else "build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-              "-Xptxas", "-v"] + (["-DSDRT_PHASE_PROF"] if PROF else [])
+              "-Xptxas", "-v"] + (["-DSDRT_PHASE_PROF"] if PROF else []) + EXTRA_DEFS
 CXX_FLAGS = ["-O2", "-std=gnu++17", "-fPIC", "-Wall"]
 
 

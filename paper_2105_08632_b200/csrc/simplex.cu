@@ -53,9 +53,20 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// largest divisor of n that is <= 5 (n-tiles per warp job)
+// n-tiles per warp job: one A fragment serves NGR MMAs; small groups give every warp of
+// the CTA a job in the short products (n = number of 8-column tiles)
+#ifndef SDRT_NGR_MODE
+#define SDRT_NGR_MODE 0
+#endif
+#ifndef SDRT_SA_MINB
+#define SDRT_SA_MINB 3
+#endif
+#ifndef SDRT_SB_MINB
+#define SDRT_SB_MINB 4
+#endif
 __host__ __device__ constexpr int ngroup(int n) {
-  return n % 5 == 0 ? 5 : (n % 4 == 0 ? 4 : (n % 3 == 0 ? 3 : (n % 2 == 0 ? 2 : 1)));
+  return SDRT_NGR_MODE == 1 ? (n % 3 == 0 && n > 5 ? 3 : (n % 2 == 0 && n > 5 ? 2 : 1))
+                            : (n % 5 == 0 ? 5 : (n % 4 == 0 ? 4 : (n % 3 == 0 ? 3 : (n % 2 == 0 ? 2 : 1))));
 }
 
 // One operator application Y (+)= M X over a tile: X rows c < split from X0, others
@@ -316,7 +327,7 @@ struct SLayoutA {
 };
 
 template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
+__global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
                                                const __grid_constant__ STileMaps tm) {
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
@@ -397,7 +408,7 @@ struct SLayoutB {
 };
 
 template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
+__global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
                                                 double dt, const __grid_constant__ STileMaps tm) {
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
