@@ -102,6 +102,64 @@ def kernel_bytes(cfg, K):
     return out
 
 
+# FP64 peak for ALU/tensor-bound kernels: 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz
+# (B200_PROFILING.md unit counts and clocks.max.sm); tools/fp64_peak measured 37.1 TF
+# for both DFMA and DMMA (mma.sync m8n8k4 f64) on the pool's B200s.
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+# pointwise flop counts per point (fp64 operations; div and sqrt count 1): convective
+# flux along one direction, viscous flux along one direction, common (Rusanov/upwind)
+# flux incl. the LDG combination
+def _pointwise(cfg):
+    D = cfg.nd
+    if cfg.eq in ("linadv", "linadvdiff"):
+        return 2 * D, (2 * D if cfg.eq == "linadvdiff" else 0), 2 * D + 4
+    fc = 6 * D + 8
+    fv = 90 if D == 3 else 50
+    return fc, (fv if cfg.eq == "ns" else 0), 2 * fc + 30
+
+
+def kernel_flops(cfg, K):
+    """Algorithmic fp64 flops per launch of each fused kernel: 2 x the structural-nonzero
+    MACs of the App. B products the kernel applies (tensor
+    elements by their 1D line factors, simplices dense with the M16 face sparsity) plus
+    the pointwise physics at the points it evaluates, each face point's common flux
+    counted once.  A model, stated in DESIGN.md §5; not a SASS count."""
+    D, ns, ne, nu = dims(cfg)
+    V = cfg.nvars
+    p = cfg.p
+    fc, fv, fr = _pointwise(cfg)
+    visc = cfg.eq in ("ns", "linadvdiff")
+    nsides = 1 if abs(cfg.beta) == 0.5 else 2
+    out = {}
+    if cfg.etype in ("quad", "hex"):
+        n = p + 1
+        NL = n ** (D - 1)
+        grad = 2 * D * NL * V * (2 * n + p * n + n * (p + 2)) + D * ns * V + 3 * D * NL * 2 * V
+        pub = D * NL * nsides * (2 * (1 + D) * V * n + fv)
+        intf = D * NL * p * (2 * ((1 + D) * V if visc else V) * n + fc + fv)
+        m13 = 2 * D * NL * V * n * p
+        a = grad + pub + intf + m13
+        b = 2 * 2 * D * NL * V * n + D * NL * fr + 2 * D * NL * V * n * 2 + 4 * ns * V + 2 * 2 * D * NL * V * n
+        if not visc:
+            b += D * NL * p * (2 * V * n + fc) + m13
+        out["tensor_grad(A)"] = K * a
+        out["tensor_stage(B)"] = K * b
+        out["tensor_traces"] = K * 2 * 2 * D * NL * V * n
+    else:
+        grad = 2 * (ne + nu) * ns * V + 3 * ne * V + 2 * ns * D * (ne / 2 + nu) * V + 2 * ns * V * D * D
+        pub = (ne / 2) * (2 * ns * D * V + fv)
+        intf = 2 * nu * ns * D * V + nu * D * (fc + fv) + 2 * ns * D * nu * V
+        a = grad + pub + intf
+        b = 2 * ne * ns * V + (ne / 2) * fr + 2 * ns * ne * V + 4 * ns * V + 2 * ne * ns * V
+        if not visc:
+            b += 2 * nu * ns * V + nu * D * fc + 2 * ns * D * nu * V
+        out["simplex_grad(A)"] = K * a
+        out["simplex_stage(B)"] = K * b
+        out["simplex_traces"] = K * 2 * ne * ns * V
+    return out
+
+
 def stage_model_bytes(cfg):
     """SURVEY.md §8(d) algorithmic bytes per DOF-stage (element-local data flow)."""
     D, ns, ne, nu = dims(cfg)
@@ -335,13 +393,26 @@ def main():
     tf = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}.json")
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(dom)
-    achieved = kb[dom] / (dom_ms / dom_n * 1e-3) / 1e9 if dom in kb else None
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm if achieved else None, "traffic": traffic,
-            "bytes_per_launch": kb.get(dom), "avg_launch_ms": dom_ms / dom_n if dom else None,
-            "launches_per_step": dom_n / args.steps if dom else None,
-            "peak_source": peak_note,
-            "step_share": dom_ms / ms if dom else None}
+    kf = kernel_flops(cfg, K)
+    t_launch = dom_ms / dom_n * 1e-3 if dom else None
+    gbs = kb[dom] / t_launch / 1e9 if dom in kb else None
+    tfs = kf[dom] / t_launch / 1e12 if dom in kf else None
+    f_hbm = gbs / hbm if gbs else 0.0
+    f_alu = tfs / FP64_PEAK_TFLOPS if tfs else 0.0
+    # the dominant kernel's binding resource: the larger of its HBM and FP64 fractions
+    if f_alu > f_hbm:
+        roof = {"bound": "alu", "kernel": dom, "achieved": tfs, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": f_alu, "traffic": traffic,
+                "peak_source": "148 SMs x 64 DFMA/clk x 2 x 1.965 GHz (B200_PROFILING.md units and clocks); "
+                               "tools/fp64_peak measured 37.1 TF (DFMA and DMMA)"}
+    else:
+        roof = {"bound": "hbm", "kernel": dom, "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_hbm,
+                "traffic": traffic, "peak_source": peak_note}
+    roof.update({"bytes_per_launch": kb.get(dom), "flops_per_launch": kf.get(dom),
+                 "hbm_frac": f_hbm, "fp64_frac": f_alu,
+                 "avg_launch_ms": dom_ms / dom_n if dom else None,
+                 "launches_per_step": dom_n / args.steps if dom else None,
+                 "step_share": dom_ms / ms if dom else None})
     model_b = stage_model_bytes(cfg)
     stage_roof = {"model_bytes_per_dof_stage": model_b,
                   "achieved_gbs": model_b * dof * 4 * args.steps / (ms_clean_max * 1e-3) / 1e9,
