@@ -470,11 +470,13 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   constexpr bool INT = !Ph::VISC;     // internal fluxes evaluated here (inviscid only)
   constexpr int NF = INT ? P + 2 : 2;  // flux-line slots per line held in sF
   extern __shared__ __align__(128) double smem[];
+  // regions allocated per stage (the launcher sizes dynamic smem the same way):
+  // sU, sR, sF always; u_n for stages 1, 2; ACC for stages 1..3
   double* sU = smem;
   double* sR = smem + NS * NV * E;    // R~ accumulator, starts as R_int (kernel A)
-  double* sUn = sR + NS * NV * E;     // RK register u_n (stages 1, 2)
-  double* sAcc = sUn + NS * NV * E;   // RK accumulator (stages 1..3)
-  double* sF = sAcc + NS * NV * E;    // [NL][NF][NV][E] flux-line values of one direction
+  double* sF = sR + NS * NV * E;      // [NL][NF][NV][E] flux-line values of one direction
+  double* sAcc = sF + NL * NF * NV * E;                             // RK accumulator (stages 1..3)
+  double* sUn = sAcc + (stage >= 1 ? NS * NV * E : 0);              // RK register u_n (stages 1, 2)
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t e0 = (int64_t)blockIdx.x * E;
@@ -497,28 +499,18 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();
   PH(1, 0)
-  // warm L2 with the neighbour traces and published viscous traces
-  prefetch_traces<D, P, NV, E>(g, sNb, b.Tu, e0, false);
-  if constexpr (Ph::VISC) prefetch_traces<D, P, NV, E>(g, sNb, b.Tg, e0, true);
-  mbar_wait(&bar[0], 0);
-  __syncthreads();
-  PH(1, 1)
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
   const int Kt = (int)g.Kt;  // trace row stride
   // one direction of the flux-line work; instantiated per direction (compile-time d
   // removes the structural zeros of the normal e_d from the physics)
-  auto direction = [&](auto dc) {
+  // End items (t, side, el) of every direction are statically owned (item tid + k NT):
+  // the traces they need (neighbour U trace, published viscous traces) for direction
+  // d+1 are requested while direction d finishes, and for d = 0 before the tile wait,
+  // so their latency overlaps other work.  Raw values only; combined at use.
+  constexpr int NEI = 2 * NL * E, CE = (NEI + NT - 1) / NT;
+  double un[CE][NV], tga[CE][NV], tgb[CE][NV];
+  auto load_dir = [&](auto dc) {
     constexpr int d = decltype(dc)::value;
-    const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
-    const double sface = g.sface[d];
-    double nL[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
-    // flux-line values.  End items (t, side, el) are statically owned (item tid + k
-    // NT): their trace loads are issued first and land while the thread computes its
-    // internal-point items (t, a, el); then the common fluxes.
-    constexpr int NEI = 2 * NL * E, CE = (NEI + NT - 1) / NT;
-    double un[CE][NV], gs[CE][NV];
 #pragma unroll
     for (int k = 0; k < CE; ++k) {
       const int item = threadIdx.x + k * NT;
@@ -533,13 +525,19 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
         un[k][v] = b.Tu[((side ? xR : xL) * NV + v) * Kt + m];
         if constexpr (Ph::VISC) {
           const int eL = side ? (int)e : m, eR = side ? m : (int)e;
-          double a0 = 0.0;
-          if (wl != 0.0) a0 = wl * b.Tg[(xL * NV + v) * Kt + eL];
-          if (wr != 0.0) a0 = fma(wr, b.Tg[(xR * NV + v) * Kt + eR], a0);
-          gs[k][v] = a0;
+          tga[k][v] = wl != 0.0 ? b.Tg[(xL * NV + v) * Kt + eL] : 0.0;
+          tgb[k][v] = wr != 0.0 ? b.Tg[(xR * NV + v) * Kt + eR] : 0.0;
         }
       }
     }
+  };
+  auto direction = [&](auto dc) {
+    constexpr int d = decltype(dc)::value;
+    const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
+    const double sface = g.sface[d];
+    double nL[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
     for (int item = threadIdx.x; item < (INT ? NL * P * E : 0); item += blockDim.x) {
       const int el = item % E, r = item / E, a = r % P, t = r / P;
       const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
@@ -578,12 +576,18 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
       Ph::conv_common(ph, uL, uR, nL, F);
       if constexpr (Ph::VISC) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) F[v] += gs[k][v] + ph.eta * (uL[v] - uR[v]);
+        for (int v = 0; v < NV; ++v) {
+          double gsum = 0.0;
+          if (wl != 0.0) gsum = wl * tga[k][v];
+          if (wr != 0.0) gsum = fma(wr, tgb[k][v], gsum);
+          F[v] += gsum + ph.eta * (uL[v] - uR[v]);
+        }
       }
       const int kf = side ? NF - 1 : 0;
 #pragma unroll
       for (int v = 0; v < NV; ++v) sF[((t * NF + kf) * NV + v) * E + el] = sface * F[v];
     }
+    if constexpr (d + 1 < D) load_dir(std::integral_constant<int, d + 1>{});
     if (d == 0) mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed
     __syncthreads();
   PH(1, 2)
@@ -612,6 +616,10 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
     __syncthreads();
   PH(1, 3)
   };
+  load_dir(std::integral_constant<int, 0>{});
+  mbar_wait(&bar[0], 0);
+  __syncthreads();
+  PH(1, 1)
   direction(std::integral_constant<int, 0>{});
   direction(std::integral_constant<int, 1>{});
   if constexpr (D == 3) direction(std::integral_constant<int, 2>{});
@@ -697,14 +705,21 @@ struct TCfg {
   static constexpr int EA = E;
   static constexpr int NTB = 256;
   static constexpr int NTA = 256;
-  static constexpr int MINB_B = 2;
+#ifndef SDRT_TB_MINB
+#define SDRT_TB_MINB 3
+#endif
+  static constexpr int MINB_B = SDRT_TB_MINB;
   static constexpr int MINB_A = 2;
   static constexpr int THREADS = 256;
   static constexpr size_t TILE = (size_t)NS * NV * E * sizeof(double);
   static constexpr size_t TILEA = (size_t)NS * NV * EA * sizeof(double);
   static constexpr size_t SMEM_A = TILEA * (1 + D) + 2 * (size_t)NL * P * NV * EA * sizeof(double);
-  // kernel B: sU, sR, the RK registers (u_n, ACC), flux-line slots
-  static constexpr size_t SMEM_B = TILE * 4 + (size_t)NL * (VISC ? 2 : P + 2) * NV * E * sizeof(double);
+  // kernel B: sU, sR, flux-line slots, + the RK registers the stage reads (ACC: stages
+  // 1..3, u_n: stages 1, 2)
+  static constexpr size_t SMEM_B0 = TILE * 2 + (size_t)NL * (VISC ? 2 : P + 2) * NV * E * sizeof(double);
+  static size_t smem_b(int stage) {
+    return SMEM_B0 + (stage >= 1 ? TILE : 0) + ((stage == 1 || stage == 2) ? TILE : 0);
+  }
   static constexpr size_t SMEM_T = TILE;
 };
 
@@ -744,8 +759,8 @@ static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, T
   } else {
     const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
     auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B>;
-    set_smem<D, P, EQ>((const void*)kb, C::SMEM_B);
-    kb<<<grid, C::NTB, C::SMEM_B, st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
+    set_smem<D, P, EQ>((const void*)kb, C::smem_b(2));
+    kb<<<grid, C::NTB, C::smem_b(stage), st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
   }
 }
 
