@@ -37,6 +37,11 @@ struct SDims {
   static constexpr int nu = D == 2 ? P * (P + 1) / 2 : P * (P + 1) * (P + 2) / 6;
   static constexpr int nfaces = D + 1;
   static constexpr int nfp = next / nfaces;
+  // k steps (columns / 4) of the packed operators
+  static constexpr int kt_sol = (nsol + 3) / 4;          // M0, M12 (columns: solution points)
+  static constexpr int kt_G = (next + nu + 3) / 4;       // [M16 | M15 P]
+  static constexpr int kt_ext = (next + 3) / 4;          // M14
+  static constexpr int kt_F = (D * nu + 3) / 4;          // M13 M19 P2
 };
 
 template <typename T>
@@ -65,14 +70,16 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #define SDRT_SB_MINB 4
 #endif
 __host__ __device__ constexpr int ngroup(int n) {
-  return SDRT_NGR_MODE == 1 ? (n % 3 == 0 && n > 5 ? 3 : (n % 2 == 0 && n > 5 ? 2 : 1))
-                            : (n % 5 == 0 ? 5 : (n % 4 == 0 ? 4 : (n % 3 == 0 ? 3 : (n % 2 == 0 ? 2 : 1))));
+  return SDRT_NGR_MODE == 1   ? (n % 3 == 0 && n > 5 ? 3 : (n % 2 == 0 && n > 5 ? 2 : 1))
+         : SDRT_NGR_MODE == 2 ? (n <= 15 ? n : (n % 5 == 0 ? 5 : 1))
+                              : (n % 5 == 0 ? 5 : (n % 4 == 0 ? 4 : (n % 3 == 0 ? 3 : (n % 2 == 0 ? 2 : 1))));
 }
 
 // One operator application Y (+)= M X over a tile: X rows c < split from X0, others
 // from X1 (row stride N = W E doubles); Y rows r < M.rows.  Warp jobs = (m-tile,
-// group of NGR n-tiles); the A fragment of a k step serves the whole group.
-template <int W, int E>
+// group of NGR n-tiles).  KT (k steps) is a compile-time constant: all A fragments
+// of a job are requested at once (one L1/L2 round trip per job), then the MMAs run.
+template <int W, int E, int KT>
 struct Dmm {
   static constexpr int N = W * E;
   static_assert(N % 8 == 0, "tile columns must be a multiple of 8");
@@ -88,20 +95,22 @@ struct Dmm {
     const int lane = threadIdx.x & 31;
     const int m = j / NG, ng = j % NG;
     const int n0 = ng * NGR * 8 + (lane >> 2);
+    const double* af = M.frag + (int64_t)m * KT * 32 + lane;
+    double a[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) a[k] = __ldg(af + k * 32);
     double c[NGR][2];
 #pragma unroll
     for (int q = 0; q < NGR; ++q) c[q][0] = c[q][1] = 0.0;
-    const double* af = M.frag + (int64_t)m * M.kt * 32 + lane;
-#pragma unroll 2
-    for (int k = 0; k < M.kt; ++k) {
-      const double a = __ldg(af + k * 32);
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
       const int col = 4 * k + (lane & 3);
       const double* xr = col < split ? X0 + col * N : X1 + (col - split) * N;
       const bool ok = col < M.cols;
 #pragma unroll
       for (int q = 0; q < NGR; ++q) {
         const double b = ok ? xr[n0 + 8 * q] : 0.0;
-        dmma(c[q][0], c[q][1], a, b);
+        dmma(c[q][0], c[q][1], a[k], b);
       }
     }
     const int r = 8 * m + (lane >> 2);
@@ -120,24 +129,24 @@ struct Dmm {
   }
 };
 
-// Y1 = M1 X1 (W1 per row) and Y2 = M2 X2 (W2) in one phase (independent products;
-// M2.frag == nullptr skips the second)
-template <int W1, int W2, int E, bool ACC1, bool ACC2>
+// Y1 = M1 X1 (W1 per row, KT1 k steps) and Y2 = M2 X2 (W2, KT2) in one phase
+// (independent products; M2.frag == nullptr skips the second)
+template <int W1, int KT1, int W2, int KT2, int E, bool ACC1, bool ACC2>
 __device__ __forceinline__ void dmm2(const SOpF& M1, const double* X1a, int s1, const double* X1b, double* Y1,
                                      const SOpF& M2, const double* X2a, int s2, const double* X2b, double* Y2) {
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int j1 = Dmm<W1, E>::jobs(M1), j2 = M2.frag ? Dmm<W2, E>::jobs(M2) : 0;
+  const int j1 = Dmm<W1, E, KT1>::jobs(M1), j2 = M2.frag ? Dmm<W2, E, KT2>::jobs(M2) : 0;
   for (int j = warp; j < j1 + j2; j += nw) {
-    if (j < j1) Dmm<W1, E>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
-    else Dmm<W2, E>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
+    if (j < j1) Dmm<W1, E, KT1>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
+    else Dmm<W2, E, KT2>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
   }
 }
 
-template <int W, int E, bool ACC>
+template <int W, int KT, int E, bool ACC>
 __device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split, const double* X1, double* Y) {
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nj = Dmm<W, E>::jobs(M);
-  for (int j = warp; j < nj; j += nw) Dmm<W, E>::template job<ACC>(M, j, X0, split, X1, Y);
+  const int nj = Dmm<W, E, KT>::jobs(M);
+  for (int j = warp; j < nj; j += nw) Dmm<W, E, KT>::template job<ACC>(M, j, X0, split, X1, Y);
 }
 
 // ---------------------------------------------------------------- tile helpers
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  dmm1<NV, E, false>(O.M0, sU, 1 << 30, sU, sUe);
+  dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sUe);
   __syncthreads();
   store_rows<S::next * NV, E>(g, sUe, T, g.Kt, e0);
 }
@@ -351,16 +360,16 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
   __syncthreads();
   mbar_wait(&bar, 0);
   // U_ext = M0 U, U_u = M12 U
-  dmm2<NV, NV, E, false, false>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30, sX, sUu);
+  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30, sX, sUu);
   __syncthreads();
   common_values<D, P, NV, E>(g, ph, b.Tu, sUe, sNb, sX, e0);  // C into X (U is dead)
   __syncthreads();
-  dmm1<NV, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
+  dmm1<NV, S::kt_G, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
   __syncthreads();
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
   // gradient at the external points (M0 on each of the D NV gradient rows) into X
-  dmm1<D * NV, E, false>(O.M0, sQ, 1 << 30, sQ, sX);
+  dmm1<D * NV, S::kt_sol, E, false>(O.M0, sQ, 1 << 30, sQ, sX);
   __syncthreads();
   // publish g at the face points of the LDG-weighted side
   const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
@@ -385,11 +394,11 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
     for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
   }
   __syncthreads();
-  dmm1<D * NV, E, false>(O.M12, sQ, 1 << 30, sQ, sUe);  // Q_u = M18 Q [nu][D NV] into UE
+  dmm1<D * NV, S::kt_sol, E, false>(O.M12, sQ, 1 << 30, sQ, sUe);  // Q_u = M18 Q [nu][D NV] into UE
   __syncthreads();
   internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
   __syncthreads();
-  dmm1<NV, E, false>(O.M13F, sX, 1 << 30, sX, sQ);  // R_int into Q (Q is dead)
+  dmm1<NV, S::kt_F, E, false>(O.M13F, sX, 1 << 30, sX, sQ);  // R_int into Q (Q is dead)
   __syncthreads();
   store_rows<S::nsol * NV, E>(g, sQ, b.Rint, g.Kp, e0);
 }
@@ -444,7 +453,8 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   mbar_wait(&bar[0], 0);
   // own traces (and, inviscid, U_u)
   const SOpF none{0, 0, 0, 0, nullptr};
-  dmm2<NV, NV, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, INT ? O.M12 : none, sU, 1 << 30, sU, sUu);
+  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, INT ? O.M12 : none, sU, 1 << 30,
+                                                        sU, sUu);
   __syncthreads();
   // common fluxes D~ = +/- s F at external points, in place over the own traces
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
@@ -499,11 +509,11 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   __syncthreads();
   // R~ = R_int + M14 D~ [+ M13 M19 P2 F~]
   if constexpr (INT) {
-    dmm1<NV, E, false>(O.M14, sUe, 1 << 30, sUe, sR);
+    dmm1<NV, S::kt_ext, E, false>(O.M14, sUe, 1 << 30, sUe, sR);
     __syncthreads();
-    dmm1<NV, E, true>(O.M13F, sF, 1 << 30, sF, sR);
+    dmm1<NV, S::kt_F, E, true>(O.M13F, sF, 1 << 30, sF, sR);
   } else {
-    dmm1<NV, E, true>(O.M14, sUe, 1 << 30, sUe, sR);
+    dmm1<NV, S::kt_ext, E, true>(O.M14, sUe, 1 << 30, sUe, sR);
   }
   __syncthreads();
   // -R~/detJ and the RK4 update (registers from shared memory), new state into sU
@@ -545,7 +555,7 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   }
   if (stage < 0) return;
   __syncthreads();
-  dmm1<NV, E, false>(O.M0, sU, 1 << 30, sU, sUe);  // traces of the new state
+  dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sUe);  // traces of the new state
   __syncthreads();
   store_rows<S::next * NV, E>(g, sUe, b.Tu_next, g.Kt, e0);
 }
