@@ -415,3 +415,35 @@ def test_tau_max_advection_rk4_table(etype, p):
     lam = VN.spectrum(B, [k * d for k in np.linspace(0, np.pi / np.abs(d).max(), 401)])
     ref = GOLD["tau_max_advection"][etype][str(p)][1]
     assert abs(VN.tau_max(lam, 4) - ref) <= 2.5e-3
+
+
+# ----------------------------------------------------------------- design order
+def _advection_l2_error(etype, p, N, T=0.05, dt=2.5e-4):
+    """Linear advection c = (1, 1) on the periodic unit square, u0 = sin 2pi x sin 2pi y,
+    classical RK4 to time T; L2 error against the exact translate u0(x - t, y - t),
+    quadrature sum_e detJ_e sum_r w_r (u - u_ex)^2 at the solution points."""
+    m = build_mesh(etype, p, N, (0.0, 0.0), (1.0, 1.0))
+    R = Residual(m, Physics("linadv", 2, c=(1.0, 1.0)))
+    x = m.sol_coords()  # (N_sol, 2, K)
+
+    def exact(t):
+        return (np.sin(2 * np.pi * (x[:, 0] - t)) * np.sin(2 * np.pi * (x[:, 1] - t)))[:, None, :]
+
+    u = exact(0.0)
+    nsteps = int(round(T / dt))
+    for _ in range(nsteps):
+        u = rk4_step(R, u, dt)
+    err = (u - exact(nsteps * dt))[:, 0, :] ** 2
+    w = build_operators(etype, p).w
+    return math.sqrt(float(np.einsum("r,rk,k->", w, err, m.detJ)))
+
+
+@pytest.mark.parametrize("etype,p", [("quad", 1), ("quad", 2), ("tri", 1), ("tri", 2)])
+def test_design_order_linear_advection(etype, p):
+    """Measured against the analytical solution (m = 1), SDRT shows p+1 order of
+    accuracy for smooth pure advection (§5.1.1, l.1680-1698).  Error ratio over
+    one mesh halving must give an observed order within 0.35 of p+1."""
+    e1 = _advection_l2_error(etype, p, 8)
+    e2 = _advection_l2_error(etype, p, 16)
+    order = math.log2(e1 / e2)
+    assert abs(order - (p + 1)) < 0.35, (etype, p, e1, e2, order)
