@@ -45,7 +45,7 @@ def _pair(cfg, N):
     return m, R, S
 
 
-RES_CASES = [("c1", 5), ("c1", (3, 7)), ("c2", 5), ("c3", 3), ("c4", (3, 4, 5)), ("c5", 3)]
+RES_CASES = [("c1", 5), ("c1", (3, 7)), ("c2", 5), ("c3", 3), ("c4", (3, 4, 5)), ("c5", 3), ("c5", (5, 6, 7))]
 
 
 @pytest.mark.parametrize("name,N", RES_CASES)
@@ -107,3 +107,38 @@ def test_divergence_is_reported():
     with pytest.raises(sdrt.SdrtError) as e:
         S.rk_step(Ud, 0.0, 1, check_every=1)
     assert e.value.code == -7 and "element" in str(e.value)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_full_size_invariants(name):
+    """BASELINE.json full sizes in the bench launch configuration, checked through
+    properties that hold at any size (the oracle does not fit the c5 mesh in a test):
+    freestream preservation and discrete conservation
+    sum_e detJ_e sum_r w_r (dU/dt)_{r,e} = 0 to round-off (l.312-318; w from the oracle's
+    quadrature weights), plus one finite RK4 step of the configuration's initial field."""
+    from oracle.operators import build_operators
+    from paper_2105_08632_b200 import sdrt
+    from paper_2105_08632_b200.solver import Solver
+    cfg = CONFIGS[name]
+    S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device="cuda", **cfg.physics_kwargs())
+    nsol, nv, Kp = S.shape
+    K = S.K
+    # freestream: constant state (Euler/NS: rho = 1, v = (0.3, -0.2, 0.1) |c|, p from the config)
+    U0 = initial_state(cfg, S.sol_coords())
+    const = U0[:, :, :K].mean(axis=(0, 2))
+    Uc = np.broadcast_to(const[None, :, None], (nsol, nv, K)).copy()
+    r = S.to_host(S.residual(S.to_device(Uc)))[:, :, :K]
+    scale = np.abs(Uc).max()
+    assert np.abs(r).max() <= 1e-10 * max(scale, 1.0), np.abs(r).max()
+    # conservation on the initial field
+    r = S.to_host(S.residual(S.to_device(U0)))[:, :, :K]
+    w = build_operators(cfg.etype, cfg.p).w
+    detj = sdrt.mesh_detj(S.mesh)[:K]
+    total = np.einsum("r,rvk,k->v", w, r, detj)
+    mag = np.einsum("r,rvk,k->v", w, np.abs(r), detj)
+    assert (np.abs(total) <= 1e-12 * np.maximum(mag, 1e-300)).all(), (total, mag)
+    # one RK4 step stays finite
+    Ud = S.to_device(U0)
+    S.rk_step(Ud, cfg.dt, 1)
+    assert np.isfinite(S.to_host(Ud)[:, :, :K]).all()
+    S.close()
