@@ -30,6 +30,21 @@
 
 namespace sdrt {
 
+// Optional per-phase cycle accounting (build with -DSDRT_PHASE_PROF; tools only)
+#ifdef SDRT_PHASE_PROF
+__device__ unsigned long long g_sphase_cycles[2][16];
+#define SPH_INIT long long ph_t0 = clock64();
+#define SPH(kern, k)                                                           \
+  if (threadIdx.x == 0) {                                                      \
+    const long long ph_t1 = clock64();                                         \
+    atomicAdd(&g_sphase_cycles[kern][k], (unsigned long long)(ph_t1 - ph_t0)); \
+    ph_t0 = ph_t1;                                                             \
+  }
+#else
+#define SPH_INIT
+#define SPH(kern, k)
+#endif
+
 template <int D, int P>
 struct SDims {
   static constexpr int nsol = D == 2 ? (P + 1) * (P + 2) / 2 : (P + 1) * (P + 2) * (P + 3) / 6;
@@ -189,36 +204,59 @@ __device__ __forceinline__ void fill_neighbours(const GeomDev& g, int (*sNb)[E],
   }
 }
 
-// C = (1/2 - b) u_L + (1/2 + b) u_R at external points into sC [next][NV][E]
-template <int D, int P, int NV, int E>
-__device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& ph, const double* __restrict__ Tu,
-                                              const double* sUe, const int (*sNb)[E], double* sC, int64_t e0) {
+// C = (1/2 - b) u_L + (1/2 + b) u_R at external points into sC [next][NV][E].  Items
+// (rho, el) are statically owned (item tid + k NT); NbGather::load issues every
+// neighbour-trace load of this thread at the kernel start, so the gathers overlap
+// the tile load and the first products.
+template <int D, int P, int NV, int E, int NT>
+struct NbGather {
   using S = SDims<D, P>;
-  const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
-  const int Kp = (int)g.Kt;  // trace row stride
-  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
-    const int el = item % E, rho = item / E;
-    const int64_t e = e0 + el;
-    if (e >= g.K) {
+  static constexpr int ITEMS = S::next * E;
+  static constexpr int CI = (ITEMS + NT - 1) / NT;
+  double nb[CI][NV];
+
+  __device__ __forceinline__ void load(const GeomDev& g, const double* __restrict__ Tu, const int (*sNb)[E],
+                                       int64_t e0) {
+    const int Kp = (int)g.Kt;  // trace row stride
 #pragma unroll
-      for (int v = 0; v < NV; ++v) sC[(rho * NV + v) * E + el] = 0.0;
-      continue;
-    }
-    const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
-    const int m = sNb[f][el];
-    const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
-    const bool left = g.left[s][f];
-    double nb[NV];
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * NT;
+      const int el = item % E, rho = item / E;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) nb[v] = Tu[(rho2 * NV + v) * Kp + m];
+      for (int v = 0; v < NV; ++v) nb[k][v] = 0.0;
+      if (item >= ITEMS || e0 + el >= g.K) continue;
+      const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
+      const int m = sNb[f][el];
+      const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double own = sUe[(rho * NV + v) * E + el];
-      const double uL = left ? own : nb[v], uR = left ? nb[v] : own;
-      sC[(rho * NV + v) * E + el] = wl * uL + wr * uR;
+      for (int v = 0; v < NV; ++v) nb[k][v] = Tu[(rho2 * NV + v) * Kp + m];
     }
   }
-}
+
+  __device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& ph, const double* sUe,
+                                                const int (*sNb)[E], double* sC, int64_t e0) const {
+    const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
+#pragma unroll
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * NT;
+      const int el = item % E, rho = item / E;
+      if (item >= ITEMS) break;
+      if (e0 + el >= g.K) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sC[(rho * NV + v) * E + el] = 0.0;
+        continue;
+      }
+      const int s = sNb[D + 1][el], f = rho / S::nfp;
+      const bool left = g.left[s][f];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double own = sUe[(rho * NV + v) * E + el];
+        const double uL = left ? own : nb[k][v], uR = left ? nb[k][v] : own;
+        sC[(rho * NV + v) * E + el] = wl * uL + wr * uR;
+      }
+    }
+  }
+};
 
 // Q = J^-T Q~ in place on sQ [nsol][D][NV][E]
 template <int D, int P, int NV, int E>
@@ -338,6 +376,7 @@ struct SLayoutA {
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
                                                const __grid_constant__ STileMaps tm) {
+  SPH_INIT
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
   using Ly = SLayoutA<D, P, Ph::NV>;
@@ -358,19 +397,27 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
   }
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
+  SPH(0, 0)
+  NbGather<D, P, NV, E, 256> gath;
+  gath.load(g, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
   // U_ext = M0 U, U_u = M12 U
   dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30, sX, sUu);
   __syncthreads();
-  common_values<D, P, NV, E>(g, ph, b.Tu, sUe, sNb, sX, e0);  // C into X (U is dead)
+  SPH(0, 1)
+  gath.common_values(g, ph, sUe, sNb, sX, e0);  // C into X (U is dead)
   __syncthreads();
+  SPH(0, 2)
   dmm1<NV, S::kt_G, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
   __syncthreads();
+  SPH(0, 3)
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
+  SPH(0, 4)
   // gradient at the external points (M0 on each of the D NV gradient rows) into X
   dmm1<D * NV, S::kt_sol, E, false>(O.M0, sQ, 1 << 30, sQ, sX);
   __syncthreads();
+  SPH(0, 5)
   // publish g at the face points of the LDG-weighted side
   const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
   const int Kp = (int)g.Kt;  // trace row stride
@@ -394,13 +441,18 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
     for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
   }
   __syncthreads();
+  SPH(0, 6)
   dmm1<D * NV, S::kt_sol, E, false>(O.M12, sQ, 1 << 30, sQ, sUe);  // Q_u = M18 Q [nu][D NV] into UE
   __syncthreads();
+  SPH(0, 7)
   internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
   __syncthreads();
+  SPH(0, 8)
   dmm1<NV, S::kt_F, E, false>(O.M13F, sX, 1 << 30, sX, sQ);  // R_int into Q (Q is dead)
   __syncthreads();
+  SPH(0, 9)
   store_rows<S::nsol * NV, E>(g, sQ, b.Rint, g.Kp, e0);
+  SPH(0, 10)
 }
 
 // Kernel B.  Regions (doubles per element): U [nsol NV] (stage input), R [nsol NV]
@@ -419,6 +471,7 @@ struct SLayoutB {
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
                                                 double dt, const __grid_constant__ STileMaps tm) {
+  SPH_INIT
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
   constexpr bool INT = !Ph::VISC;  // internal fluxes evaluated here (inviscid only)
@@ -450,12 +503,14 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   }
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
+  SPH(1, 0)
   mbar_wait(&bar[0], 0);
   // own traces (and, inviscid, U_u)
   const SOpF none{0, 0, 0, 0, nullptr};
   dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, INT ? O.M12 : none, sU, 1 << 30,
                                                         sU, sUu);
   __syncthreads();
+  SPH(1, 1)
   // common fluxes D~ = +/- s F at external points, in place over the own traces
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
   const int Kp = (int)g.Kt;  // trace row stride
@@ -507,15 +562,18 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   if constexpr (INT) internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, nullptr, sF, e0);
   mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed
   __syncthreads();
+  SPH(1, 2)
   // R~ = R_int + M14 D~ [+ M13 M19 P2 F~]
   if constexpr (INT) {
     dmm1<NV, S::kt_ext, E, false>(O.M14, sUe, 1 << 30, sUe, sR);
     __syncthreads();
+  SPH(1, 3)
     dmm1<NV, S::kt_F, E, true>(O.M13F, sF, 1 << 30, sF, sR);
   } else {
     dmm1<NV, S::kt_ext, E, true>(O.M14, sUe, 1 << 30, sUe, sR);
   }
   __syncthreads();
+  SPH(1, 4)
   // -R~/detJ and the RK4 update (registers from shared memory), new state into sU
   for (int idx = threadIdx.x; idx < S::nsol * NV * E; idx += blockDim.x) {
     const int el = idx % E, row = idx / E;
@@ -555,9 +613,12 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   }
   if (stage < 0) return;
   __syncthreads();
+  SPH(1, 5)
   dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sUe);  // traces of the new state
   __syncthreads();
+  SPH(1, 6)
   store_rows<S::next * NV, E>(g, sUe, b.Tu_next, g.Kt, e0);
+  SPH(1, 7)
 }
 
 // ------------------------------------------------------------------ launchers
@@ -688,4 +749,20 @@ void simplex_launch_flux(int D, int P, int eq, const GeomDev& g, const SimplexOp
   spick(D, P, eq, &m)(g, O, ph, tma, b, stage, dt, st, 1, nullptr, nullptr);
 }
 
+#ifdef SDRT_PHASE_PROF
+void simplex_phase_cycles(unsigned long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_sphase_cycles, sizeof(g_sphase_cycles));
+  if (reset) {
+    static unsigned long long z[2][16] = {};
+    cudaMemcpyToSymbol(g_sphase_cycles, z, sizeof(z));
+  }
+}
+#endif
+
 }  // namespace sdrt
+
+#ifdef SDRT_PHASE_PROF
+extern "C" void sdrt_debug_sphase_cycles(unsigned long long* out, int reset) {
+  sdrt::simplex_phase_cycles(out, reset != 0);
+}
+#endif

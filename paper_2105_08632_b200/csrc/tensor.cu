@@ -704,7 +704,10 @@ struct TCfg {
   static constexpr int E = NV > 1 ? 8 : (D == 3 ? 16 : 32);  // kernel B and traces
   static constexpr int EA = E;
   static constexpr int NTB = 256;
-  static constexpr int NTA = 256;
+#ifndef SDRT_TA_NT
+#define SDRT_TA_NT 256
+#endif
+  static constexpr int NTA = SDRT_TA_NT;
 #ifndef SDRT_TB_MINB
 #define SDRT_TB_MINB 3
 #endif

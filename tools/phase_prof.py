@@ -20,14 +20,22 @@ U = S.to_device(initial_state(cfg, S.sol_coords()))
 S.rk_step(U, cfg.dt, 2)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 32)()
-f = sdrt.lib.sdrt_debug_phase_cycles
+simplex = cfg.etype in ("tri", "tet")
+f = sdrt.lib.sdrt_debug_sphase_cycles if simplex else sdrt.lib.sdrt_debug_phase_cycles
 f(buf, 1)
 S.rk_step(U, cfg.dt, 5)
 torch.cuda.synchronize()
 f(buf, 1)
-names = {0: ["nbrs", "tile+nb load", "gradient", "pub+Fv(0)", "div0+Fv(1)", "div1+Fv(2)", "div2"],
-         1: ["nbrs", "tile load", "flux (all d)", "div (all d)", "RK+x traces"] + [""] * 10 + ["y/z traces"]}
+if simplex:
+    names = {0: ["nbrs", "M0,M12", "C", "G", "metric", "M0.Q", "publish", "M12.Q", "int.flux", "M13F", "store"],
+             1: ["nbrs", "M0", "faceflux+wait", "M14", "RK", "M0 new", "store"]}
+    kn = ["ks_grad (A)", "ks_stage (B)"]
+else:
+    names = {0: ["nbrs", "tile+nb load", "gradient", "pub+Fv(0)", "div0+Fv(1)", "div1+Fv(2)", "div2"],
+             1: ["nbrs", "tile load", "flux (all d)", "div (all d)", "RK+x traces"] + [""] * 10 + ["y/z traces"]}
+    kn = ["kt_grad (A)", "kt_stage (B)"]
 for k in range(2):
     v = [buf[16 * k + i] for i in range(16)]
     tot = sum(v) or 1
-    print(["kt_grad (A)", "kt_stage (B)"][k], " ".join(f"{names[k][i] or i}:{100*v[i]/tot:.1f}%" for i in range(16) if v[i]))
+    nm = names[k] + [""] * 16
+    print(kn[k], " ".join(f"{nm[i] or i}:{100*v[i]/tot:.1f}%" for i in range(16) if v[i]))
