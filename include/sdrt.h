@@ -162,6 +162,16 @@ sdrt_status sdrt_ctx_kernel_times(sdrt_ctx* c, int max_tags, char* names, double
 sdrt_status sdrt_stage_traces(sdrt_ctx* c, const double* d_U, void* stream);
 sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream);
 sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, void* stream);
+/* Overlap variants: the same stage on a subset of the element tiles,
+ * part = 0 all, 1 interior tiles (no element in a pattern layer next to a partition
+ * face: they read no ghost values), 2 boundary tiles.  A stage split as
+ *   grad(1) || [exchange 0 in flight], grad(2), flux(1) || [exchange 1], flux(2)
+ * gives results identical to part 0 (every element is in exactly one part; the
+ * trace double buffer flips after part 2).  Without partition faces every tile is
+ * interior and part 2 is empty.  Errors: SDRT_E_INVALID_ARG for part outside 0..2. */
+sdrt_status sdrt_stage_grad_part(sdrt_ctx* c, double* d_U, int stage, int part, void* stream);
+sdrt_status sdrt_stage_flux_part(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, int part,
+                                 void* stream);
 /* Halo buffers: *nslab slabs; peer/d/side per slab (arrays of 6), offset[nslab+1] =
  * value offsets of each slab's segment in the contiguous send / recv buffers (doubles).
  * pack copies this rank's outgoing traces (which = 0: U traces of the current stage

@@ -36,6 +36,8 @@ struct GeomDev {
   int8_t off[MAXSUB][MAXF][3];
   int8_t nshape[MAXSUB][MAXF], nface[MAXSUB][MAXF], left[MAXSUB][MAXF];
   int8_t perm[MAXSUB][MAXF][MAXFP];
+  const int* tiles;       // optional tile list (interior / boundary subsets), nullptr = all
+  int ntiles;
 };
 
 // per (shape, ext point) metric: s scale and canonical normal (global memory)

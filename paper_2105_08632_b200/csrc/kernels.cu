@@ -315,7 +315,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, total;
+      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_tiles, total;
   size_t ops_bytes;
 };
 
@@ -379,6 +379,9 @@ struct sdrt_ctx {
   TensorGeom tg;
   Line1D line;
   TensorTma tma;
+  // interior / boundary tile lists (multi-rank overlap): tiles of tile_w elements
+  int tile_w = 0, n_int = 0, n_bnd = 0;
+  const int* d_tiles = nullptr;  // [n_int interior tiles][n_bnd boundary tiles]
   double* Tu[2] = {nullptr, nullptr};
   double* Tg = nullptr;
   int cur = 0;
@@ -494,6 +497,9 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.halo_entries = ent;
   p.off_halo = o;
   o += align256(ent * 4 * sizeof(int32_t)) + align256(ent * NV * sizeof(double));
+  // interior / boundary tile lists of the fused paths (tiles of >= 8 elements)
+  p.off_tiles = o;
+  o += align256(((size_t)m.K / 8 + 2) * sizeof(int32_t));
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -664,6 +670,7 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     c->fused = etype_tensor(m.etype) && !(fg && fg[0] == '1') && tensor_supported(m.nd, m.p, ph->eq);
     if (c->fused) {
       TensorGeom& t = c->tg;
+      std::memset(&t, 0, sizeof(t));
       for (int d = 0; d < 3; ++d) t.N[d] = m.Nloc[d];
       t.K = m.K;
       t.Kp = m.K_pad;
@@ -720,6 +727,35 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tu[1] = (double*)(base + p.off_tu1);
       c->Tg = (double*)(base + p.off_tg);
       CUDA_OK(cudaStreamSynchronize(st));
+    }
+    // interior / boundary tile lists for the overlapped multi-rank stage:
+    // a tile is interior if none of its elements lies in a pattern layer next to a
+    // partition face (ghost neighbours only occur there)
+    if ((c->fused || c->sfused) && (m.halo[0] || m.halo[1] || m.halo[2])) {
+      c->tile_w = c->fused ? tensor_tile_width(m.nd, m.p, ph->eq) : simplex_tile_width(m.nd, m.p, ph->eq);
+      const int ntile = (int)((m.K + c->tile_w - 1) / c->tile_w);
+      std::vector<int> inner, bnd;
+      for (int tl = 0; tl < ntile; ++tl) {
+        bool b = false;
+        for (int j = 0; j < c->tile_w && !b; ++j) {
+          const int64_t e = (int64_t)tl * c->tile_w + j;
+          if (e >= m.K) break;
+          int64_t pat = e / m.nsub;
+          for (int d = 0; d < m.nd; ++d) {
+            const int cd = (int)(pat % m.Nloc[d]);
+            pat /= m.Nloc[d];
+            if (m.halo[d] && (cd == 0 || cd == m.Nloc[d] - 1)) b = true;
+          }
+        }
+        (b ? bnd : inner).push_back(tl);
+      }
+      c->n_int = (int)inner.size();
+      c->n_bnd = (int)bnd.size();
+      inner.insert(inner.end(), bnd.begin(), bnd.end());
+      int* dt = (int*)(base + p.off_tiles);
+      if (!inner.empty())
+        CUDA_OK(cudaMemcpyAsync(dt, inner.data(), inner.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+      c->d_tiles = dt;
     }
     CUDA_OK(cudaStreamSynchronize(st));  // host vectors go out of scope
     *out = c;
@@ -1123,7 +1159,35 @@ sdrt_status sdrt_stage_traces(sdrt_ctx* c, const double* d_U, void* stream) {
 }
 
 sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
-  if (!c || !d_U || stage < -1 || stage > 3 || (!c->fused && !c->sfused)) {
+  return sdrt_stage_grad_part(c, d_U, stage, 0, stream);
+}
+
+sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, void* stream) {
+  return sdrt_stage_flux_part(c, d_U, stage, dt, d_out, 0, stream);
+}
+
+}  // extern "C"
+
+// geometry restricted to a tile subset: part 0 = all tiles, 1 = interior, 2 = boundary
+static bool part_geom(sdrt_ctx* c, int part, TensorGeom* tg, GeomDev* g) {
+  *tg = c->tg;
+  *g = c->g;
+  if (part == 0) return true;
+  if (!c->d_tiles) {  // no partition faces: everything is interior
+    if (part == 2) return false;
+    return true;
+  }
+  const int* list = part == 1 ? c->d_tiles : c->d_tiles + c->n_int;
+  const int n = part == 1 ? c->n_int : c->n_bnd;
+  tg->tiles = g->tiles = list;
+  tg->ntiles = g->ntiles = n;
+  return n > 0;
+}
+
+extern "C" {
+
+sdrt_status sdrt_stage_grad_part(sdrt_ctx* c, double* d_U, int stage, int part, void* stream) {
+  if (!c || !d_U || stage < -1 || stage > 3 || part < 0 || part > 2 || (!c->fused && !c->sfused)) {
     set_error("invalid argument");
     return SDRT_E_INVALID_ARG;
   }
@@ -1131,6 +1195,9 @@ sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
   SDRT_TRY({
     cudaStream_t st = (cudaStream_t)stream;
     const double* Uin = stage <= 0 ? d_U : c->Us;
+    TensorGeom tgp;
+    GeomDev gp;
+    if (!part_geom(c, part, &tgp, &gp)) return SDRT_OK;
     if (c->fused) {
       TensorBufs b{};
       b.Uin = Uin;
@@ -1138,7 +1205,7 @@ sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
       b.Tg = c->Tg;
       b.Rv = c->R;
       Mark mk(c, st, T_FA);
-      tensor_launch_grad(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, st);
+      tensor_launch_grad(c->nd, c->p, c->eq, tgp, c->line, c->ph, &c->tma, b, st);
     } else {
       SimplexBufs b{};
       b.Uin = Uin;
@@ -1147,21 +1214,33 @@ sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream) {
       b.Rint = c->R;
       b.xm = c->xm;
       Mark mk(c, st, T_SA);
-      simplex_launch_grad(c->nd, c->p, c->eq, c->g, c->sops, c->ph, &c->stma, b, st);
+      simplex_launch_grad(c->nd, c->p, c->eq, gp, c->sops, c->ph, &c->stma, b, st);
     }
     CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })
 }
 
-sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, void* stream) {
-  if (!c || !d_U || stage < -1 || stage > 3 || (stage == -1 && !d_out) || (!c->fused && !c->sfused)) {
+sdrt_status sdrt_stage_flux_part(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, int part,
+                                 void* stream) {
+  if (!c || !d_U || stage < -1 || stage > 3 || (stage == -1 && !d_out) || part < 0 || part > 2 ||
+      (!c->fused && !c->sfused)) {
     set_error("invalid argument");
     return SDRT_E_INVALID_ARG;
   }
   SDRT_TRY({
     cudaStream_t st = (cudaStream_t)stream;
     const double* Uin = stage <= 0 ? d_U : c->Us;
+    TensorGeom tgp;
+    GeomDev gp;
+    const bool any = part_geom(c, part, &tgp, &gp);
+    // the trace double buffer flips once per stage: after the whole mesh (part 0) or
+    // after the boundary part (part 2) of the overlapped sequence interior -> boundary
+    const bool flip = stage >= 0 && part != 1;
+    if (!any) {
+      if (flip) c->cur ^= 1;
+      return SDRT_OK;
+    }
     if (c->fused) {
       TensorBufs b;
       b.Uin = Uin;
@@ -1174,7 +1253,7 @@ sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, doub
       b.Tg = c->Tg;
       b.Rv = c->R;
       Mark mk(c, st, T_FB);
-      tensor_launch_flux(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, stage, dt, st);
+      tensor_launch_flux(c->nd, c->p, c->eq, tgp, c->line, c->ph, &c->tma, b, stage, dt, st);
     } else {
       SimplexBufs b;
       b.Uin = Uin;
@@ -1188,9 +1267,9 @@ sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, doub
       b.Rint = c->R;
       b.xm = c->xm;
       Mark mk(c, st, T_SB);
-      simplex_launch_flux(c->nd, c->p, c->eq, c->g, c->sops, c->ph, &c->stma, b, stage, dt, st);
+      simplex_launch_flux(c->nd, c->p, c->eq, gp, c->sops, c->ph, &c->stma, b, stage, dt, st);
     }
-    if (stage >= 0) c->cur ^= 1;
+    if (flip) c->cur ^= 1;
     CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })

@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
   double* sU = smem;
   double* sUe = smem + S::nsol * NV * E;
   __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_fence_init();
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
   double* sQ = sUu + Ly::UU * E;
   __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
   __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_fence_init();
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   double* sF = sUu + Ly::UU * E;
   __shared__ int sNb[D + 2][E];
   __shared__ __align__(8) uint64_t bar[2];
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   constexpr unsigned TB = S::nsol * NV * E * 8;
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -656,7 +656,8 @@ template <int D, int P, int EQ>
 static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, SimplexTma* tma, const SimplexBufs& b,
                  int stage, double dt, cudaStream_t st, int which, const double* U, double* T) {
   using C = SCfg<D, P, EQ>;
-  const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
+  const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::E - 1) / C::E);
+  if (grid == 0) return;
   if (which == 0) {
     if constexpr (Phys<EQ, D>::VISC) {
       auto k = ks_grad<D, P, EQ, C::E>;
@@ -716,6 +717,11 @@ static SFn spick(int D, int P, int eq, STmaFn* m) {
     }
   }
   return nullptr;
+}
+
+int simplex_tile_width(int D, int P, int eq) {
+  (void)D; (void)P; (void)eq;
+  return 8;  // SCfg<...>::E for every instantiation
 }
 
 bool simplex_supported(int D, int P, int eq) {

@@ -50,6 +50,7 @@ struct SimplexTma {
 };
 
 bool simplex_supported(int D, int P, int eq);
+int simplex_tile_width(int D, int P, int eq);
 void simplex_tma_init(SimplexTma* t, int D, int P, int eq, int64_t Kp);
 void simplex_launch_traces(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, SimplexTma* tma,
                            const double* U, double* Tu, cudaStream_t st);

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const _
   constexpr int ROWS = TDims<D, P>::NS * NV;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_fence_init();
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   double* sF = sQ + D * NS * NV * E;  // 2 x [NL][P][NV][E]
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   if (threadIdx.x == 0) {  // the stage-input tile by TMA
     mbar_init(&bar, 1);
     mbar_fence_init();
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   double* sUn = sAcc + (stage >= 1 ? NS * NV * E : 0);              // RK register u_n (stages 1, 2)
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar[2];
-  const int64_t e0 = (int64_t)blockIdx.x * E;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   // every element-local input of the tile is requested up front by TMA: the stage
   // input (barrier 0), then R_int and the RK registers (barrier 1), waited for only
   // where they are used
@@ -754,13 +754,15 @@ static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, T
   using C = TCfg<D, P, EQ>;
   if (which == 0) {
     if constexpr (Phys<EQ, D>::VISC) {
-      const unsigned grid = (unsigned)((g.K + C::EA - 1) / C::EA);
+      const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::EA - 1) / C::EA);
+      if (grid == 0) return;
       auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A>;
       set_smem<D, P, EQ>((const void*)ka, C::SMEM_A);
       ka<<<grid, C::NTA, C::SMEM_A, st>>>(g, L, ph, b, maps_for(tma, b, false));
     }
   } else {
-    const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
+    const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::E - 1) / C::E);
+    if (grid == 0) return;
     auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B>;
     set_smem<D, P, EQ>((const void*)kb, C::smem_b(2));
     kb<<<grid, C::NTB, C::smem_b(stage), st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
@@ -827,6 +829,21 @@ static void pick_all(int D, int P, int eq, StageFn* s, TraceFn* t, TmaFn* m) {
       case 4: pick<3, 4>(eq, s, t, m); break;
     }
   }
+}
+
+template <int D, int P>
+static int twidth(int eq) {
+  switch (eq) {
+    case EQ_LINADV: return TCfg<D, P, EQ_LINADV>::E;
+    case EQ_LINADVDIFF: return TCfg<D, P, EQ_LINADVDIFF>::E;
+    case EQ_EULER: return TCfg<D, P, EQ_EULER>::E;
+    default: return TCfg<D, P, EQ_NS>::E;
+  }
+}
+
+int tensor_tile_width(int D, int P, int eq) {
+  if (D == 2) return P == 1 ? twidth<2, 1>(eq) : P == 2 ? twidth<2, 2>(eq) : P == 3 ? twidth<2, 3>(eq) : twidth<2, 4>(eq);
+  return P == 1 ? twidth<3, 1>(eq) : P == 2 ? twidth<3, 2>(eq) : P == 3 ? twidth<3, 3>(eq) : twidth<3, 4>(eq);
 }
 
 bool tensor_supported(int D, int P, int eq) {

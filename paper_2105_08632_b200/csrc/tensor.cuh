@@ -33,7 +33,10 @@ struct TensorGeom {
   double jinv[3];     // 2 / h_d  (J^-T = diag)
   double detJ;        // prod h_d / 2
   double sface[3];    // detJ * 2 / h_d  (= detJ |J^-T n~| on faces normal to d)
+  const int* tiles;   // optional tile list (interior / boundary subsets), nullptr = all tiles
+  int ntiles;
 };
+int tensor_tile_width(int D, int P, int eq);
 
 struct TensorBufs {
   const double* Uin;  // stage input (U or Us)

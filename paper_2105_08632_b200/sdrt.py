@@ -78,6 +78,8 @@ lib.sdrt_halo_unpack.argtypes = [_vp, ctypes.c_int, _vp, _vp]
 lib.sdrt_stage_traces.argtypes = [_vp, _vp, _vp]
 lib.sdrt_stage_grad.argtypes = [_vp, _vp, ctypes.c_int, _vp]
 lib.sdrt_stage_flux.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_double, _vp, _vp]
+lib.sdrt_stage_grad_part.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp]
+lib.sdrt_stage_flux_part.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_double, _vp, ctypes.c_int, _vp]
 lib.sdrt_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_ctx_kernel_times.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_int)]
 lib.sdrt_ctx_last_launches.argtypes = [_vp]
@@ -277,6 +279,15 @@ def stage_grad(ctx, U_ptr, stage, stream):
 
 def stage_flux(ctx, U_ptr, stage, dt, out_ptr, stream):
     _check(lib.sdrt_stage_flux(ctx, _vp(U_ptr), int(stage), float(dt), _vp(out_ptr), _vp(stream)))
+
+
+def stage_grad_part(ctx, U_ptr, stage, part, stream):
+    _check(lib.sdrt_stage_grad_part(ctx, _vp(U_ptr), int(stage), int(part), _vp(stream)))
+
+
+def stage_flux_part(ctx, U_ptr, stage, dt, out_ptr, part, stream):
+    _check(lib.sdrt_stage_flux_part(ctx, _vp(U_ptr), int(stage), float(dt), _vp(out_ptr), int(part),
+                                    _vp(stream)))
 
 
 def ctx_last_launches(ctx):
