@@ -144,6 +144,46 @@ struct Dmm {
   }
 };
 
+// Y = M X with the result rows written straight from the MMA fragments to global
+// memory, G[(r W + w) ld + e0 + el] (element-major ABI layout, 16-byte stores), for
+// e0 + el < K.  Saves the shared-memory round trip and a barrier for final products.
+template <int W, int KT, int E>
+__device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, double* __restrict__ Gout, int64_t ld,
+                                            int64_t e0, int64_t K) {
+  using DM = Dmm<W, E, KT>;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int j = warp; j < DM::jobs(M); j += nw) {
+    const int m = j / DM::NG, ng = j % DM::NG;
+    const int n0 = ng * DM::NGR * 8 + (lane >> 2);
+    const double* af = M.frag + (int64_t)m * KT * 32 + lane;
+    double a[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) a[k] = __ldg(af + k * 32);
+    double c[DM::NGR][2];
+#pragma unroll
+    for (int q = 0; q < DM::NGR; ++q) c[q][0] = c[q][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      const int col = 4 * k + (lane & 3);
+      const bool ok = col < M.cols;
+#pragma unroll
+      for (int q = 0; q < DM::NGR; ++q) dmma(c[q][0], c[q][1], a[k], ok ? X[col * DM::N + n0 + 8 * q] : 0.0);
+    }
+    const int r = 8 * m + (lane >> 2);
+    if (r < M.rows) {
+#pragma unroll
+      for (int q = 0; q < DM::NGR; ++q) {
+        const int n = ng * DM::NGR * 8 + 8 * q + 2 * (lane & 3);  // column (w, el), el even
+        const int w = n / E, el = n % E;
+        double* gp = Gout + ((int64_t)r * W + w) * ld + e0 + el;
+        if (e0 + el + 1 < K) *reinterpret_cast<double2*>(gp) = make_double2(c[q][0], c[q][1]);
+        else if (e0 + el < K) gp[0] = c[q][0];
+      }
+    }
+  }
+}
+
 // Y1 = M1 X1 (W1 per row, KT1 k steps) and Y2 = M2 X2 (W2, KT2) in one phase
 // (independent products; M2.frag == nullptr skips the second)
 template <int W1, int KT1, int W2, int KT2, int E, bool ACC1, bool ACC2>
@@ -324,16 +364,6 @@ __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev&
   }
 }
 
-// rows [ROWS][E] of a tile in smem -> global T[row][ld] (element columns e0..)
-template <int ROWS, int E>
-__device__ __forceinline__ void store_rows(const GeomDev& g, const double* sY, double* __restrict__ T, int64_t ld,
-                                           int64_t e0) {
-  for (int idx = threadIdx.x; idx < ROWS * E; idx += blockDim.x) {
-    const int el = idx % E, r = idx / E;
-    if (e0 + el < g.K) T[(int64_t)r * ld + e0 + el] = sY[idx];
-  }
-}
-
 // ---------------------------------------------------------------- kernels
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const __grid_constant__ STileMaps tm,
@@ -353,9 +383,7 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sUe);
-  __syncthreads();
-  store_rows<S::next * NV, E>(g, sUe, T, g.Kt, e0);
+  dmm1_global<NV, S::kt_sol, E>(O.M0, sU, T, g.Kt, e0, g.K);
 }
 
 // Kernel A.  Shared-memory regions (doubles per element) by liveness:
@@ -448,10 +476,8 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
   internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
   __syncthreads();
   SPH(0, 8)
-  dmm1<NV, S::kt_F, E, false>(O.M13F, sX, 1 << 30, sX, sQ);  // R_int into Q (Q is dead)
-  __syncthreads();
+  dmm1_global<NV, S::kt_F, E>(O.M13F, sX, b.Rint, g.Kp, e0, g.K);  // R_int -> HBM
   SPH(0, 9)
-  store_rows<S::nsol * NV, E>(g, sQ, b.Rint, g.Kp, e0);
   SPH(0, 10)
 }
 
@@ -614,10 +640,8 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   if (stage < 0) return;
   __syncthreads();
   SPH(1, 5)
-  dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sUe);  // traces of the new state
-  __syncthreads();
+  dmm1_global<NV, S::kt_sol, E>(O.M0, sU, b.Tu_next, g.Kt, e0, g.K);  // traces of the new state
   SPH(1, 6)
-  store_rows<S::next * NV, E>(g, sUe, b.Tu_next, g.Kt, e0);
   SPH(1, 7)
 }
 
