@@ -267,22 +267,28 @@ __global__ void k_check(GeomDev g, PhysDev ph, const double* __restrict__ U, int
 }
 
 // halo: pack / unpack trace entries (row, col) x N_V  <->  contiguous buffer
+// trace element (point row, variable v, column col): [row][v][Kt] (tensor path) or
+// point-major [row][Kt][v] (simplex path)
+__device__ __forceinline__ int64_t trace_at(int64_t row, int v, int64_t col, int64_t Kt, int NV, bool pm) {
+  return pm ? (row * Kt + col) * NV + v : (row * NV + v) * Kt + col;
+}
+
 __global__ void k_halo_pack(const double* __restrict__ T, int64_t Kt, int NV, const int32_t* __restrict__ row,
-                            const int32_t* __restrict__ col, int64_t n, double* __restrict__ buf) {
+                            const int32_t* __restrict__ col, int64_t n, double* __restrict__ buf, bool pm) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * NV) return;
   const int64_t k = idx / NV;
   const int v = (int)(idx % NV);
-  buf[idx] = T[((int64_t)row[k] * NV + v) * Kt + col[k]];
+  buf[idx] = T[trace_at(row[k], v, col[k], Kt, NV, pm)];
 }
 
 __global__ void k_halo_unpack(double* __restrict__ T, int64_t Kt, int NV, const int32_t* __restrict__ row,
-                              const int32_t* __restrict__ col, int64_t n, const double* __restrict__ buf) {
+                              const int32_t* __restrict__ col, int64_t n, const double* __restrict__ buf, bool pm) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * NV) return;
   const int64_t k = idx / NV;
   const int v = (int)(idx % NV);
-  T[((int64_t)row[k] * NV + v) * Kt + col[k]] = buf[idx];
+  T[trace_at(row[k], v, col[k], Kt, NV, pm)] = buf[idx];
 }
 
 // ------------------------------------------------------------------------ host side
@@ -910,7 +916,7 @@ static void halo_pack(sdrt_ctx* c, int which, double* buf, cudaStream_t st) {
   if (n == 0) return;
   const int64_t tot = n * c->nv;
   k_halo_pack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(trace_buf(c, which), c->g.Kt, c->nv, c->h_srow,
-                                                              c->h_scol, n, buf);
+                                                              c->h_scol, n, buf, c->sfused);
   c->launches++;
 }
 
@@ -919,7 +925,7 @@ static void halo_unpack(sdrt_ctx* c, int which, const double* buf, cudaStream_t 
   if (n == 0) return;
   const int64_t tot = n * c->nv;
   k_halo_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(trace_buf(c, which), c->g.Kt, c->nv, c->h_rrow,
-                                                                c->h_rcol, n, buf);
+                                                                c->h_rcol, n, buf, c->sfused);
   c->launches++;
 }
 
@@ -936,7 +942,7 @@ static void halo_loopback(sdrt_ctx* c, int which, cudaStream_t st) {
     const int64_t tot = n * c->nv;
     k_halo_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
         trace_buf(c, which), c->g.Kt, c->nv, c->h_rrow + c->slab_off[i], c->h_rcol + c->slab_off[i], n,
-        c->h_stage + c->slab_off[j] * c->nv);
+        c->h_stage + c->slab_off[j] * c->nv, c->sfused);
     c->launches++;
   }
 }

@@ -18,7 +18,9 @@
 //   kernel B ("faces + update"): U_ext = M0 U, common fluxes D~ = +/- s F (l.312-340,
 //     canonical L/R), R~ = R_int + M14 D~ (l.2919-2925) [inviscid: U_u, F~ and M13 F~
 //     here too], -R~/detJ, RK4 update, new traces M0 U_new.
-// Tiles arrive by TMA; face values are exchanged only through double-buffered traces.
+// Tiles arrive by TMA; face values are exchanged only through double-buffered traces,
+// stored point-major [N_ext][K_t][N_V] (a neighbour's N_V values at one face point are
+// contiguous, so the scattered neighbour gathers touch 1-2 sectors instead of N_V).
 #include <cuda_runtime.h>
 
 #include <cstring>
@@ -147,7 +149,7 @@ struct Dmm {
 // Y = M X with the result rows written straight from the MMA fragments to global
 // memory, G[(r W + w) ld + e0 + el] (element-major ABI layout, 16-byte stores), for
 // e0 + el < K.  Saves the shared-memory round trip and a barrier for final products.
-template <int W, int KT, int E>
+template <int W, int KT, int E, bool POINT_MAJOR = false>
 __device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, double* __restrict__ Gout, int64_t ld,
                                             int64_t e0, int64_t K) {
   using DM = Dmm<W, E, KT>;
@@ -176,9 +178,15 @@ __device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, doub
       for (int q = 0; q < DM::NGR; ++q) {
         const int n = ng * DM::NGR * 8 + 8 * q + 2 * (lane & 3);  // column (w, el), el even
         const int w = n / E, el = n % E;
-        double* gp = Gout + ((int64_t)r * W + w) * ld + e0 + el;
-        if (e0 + el + 1 < K) *reinterpret_cast<double2*>(gp) = make_double2(c[q][0], c[q][1]);
-        else if (e0 + el < K) gp[0] = c[q][0];
+        if constexpr (POINT_MAJOR) {  // trace layout [row][element][w]
+          double* gp = Gout + ((int64_t)r * ld + e0 + el) * W + w;
+          if (e0 + el < K) gp[0] = c[q][0];
+          if (e0 + el + 1 < K) gp[W] = c[q][1];
+        } else {  // ABI layout [row][w][element]
+          double* gp = Gout + ((int64_t)r * W + w) * ld + e0 + el;
+          if (e0 + el + 1 < K) *reinterpret_cast<double2*>(gp) = make_double2(c[q][0], c[q][1]);
+          else if (e0 + el < K) gp[0] = c[q][0];
+        }
       }
     }
   }
@@ -269,7 +277,7 @@ struct NbGather {
       const int m = sNb[f][el];
       const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
 #pragma unroll
-      for (int v = 0; v < NV; ++v) nb[k][v] = Tu[(rho2 * NV + v) * Kp + m];
+      for (int v = 0; v < NV; ++v) nb[k][v] = Tu[((int64_t)rho2 * Kp + m) * NV + v];
     }
   }
 
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  dmm1_global<NV, S::kt_sol, E>(O.M0, sU, T, g.Kt, e0, g.K);
+  dmm1_global<NV, S::kt_sol, E, true>(O.M0, sU, T, g.Kt, e0, g.K);
 }
 
 // Kernel A.  Shared-memory regions (doubles per element) by liveness:
@@ -466,7 +474,7 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
     double gv[NV];
     Ph::visc_dir(ph, u, q, nl, gv);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) b.Tg[(rho * NV + v) * Kp + e] = gv[v];
+    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
   }
   __syncthreads();
   SPH(0, 6)
@@ -555,7 +563,7 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
     double uo[NV], un[NV], gsum[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      un[v] = b.Tu[(rho2 * NV + v) * Kp + m];
+      un[v] = b.Tu[((int64_t)rho2 * Kp + m) * NV + v];
       uo[v] = sUe[(rho * NV + v) * E + el];
       gsum[v] = 0.0;
     }
@@ -566,8 +574,8 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         double a = 0.0;
-        if (wl != 0.0) a = wl * b.Tg[(rL * NV + v) * Kp + eL];
-        if (wr != 0.0) a = fma(wr, b.Tg[(rR * NV + v) * Kp + eR], a);
+        if (wl != 0.0) a = wl * b.Tg[((int64_t)rL * Kp + eL) * NV + v];
+        if (wr != 0.0) a = fma(wr, b.Tg[((int64_t)rR * Kp + eR) * NV + v], a);
         gsum[v] = a;
       }
     }
@@ -640,7 +648,7 @@ __global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, Simplex
   if (stage < 0) return;
   __syncthreads();
   SPH(1, 5)
-  dmm1_global<NV, S::kt_sol, E>(O.M0, sU, b.Tu_next, g.Kt, e0, g.K);  // traces of the new state
+  dmm1_global<NV, S::kt_sol, E, true>(O.M0, sU, b.Tu_next, g.Kt, e0, g.K);  // traces of the new state
   SPH(1, 6)
   SPH(1, 7)
 }
