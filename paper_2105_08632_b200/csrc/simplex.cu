@@ -84,7 +84,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #define SDRT_SA_MINB 3
 #endif
 #ifndef SDRT_SB_MINB
-#define SDRT_SB_MINB 4
+#define SDRT_SB_MINB 5
+#endif
+#ifndef SDRT_SB_NT
+#define SDRT_SB_NT 160
+#endif
+#ifndef SDRT_SPLIT_INTFLUX
+#define SDRT_SPLIT_INTFLUX 0
 #endif
 __host__ __device__ constexpr int ngroup(int n) {
   return SDRT_NGR_MODE == 1   ? (n % 3 == 0 && n > 5 ? 3 : (n % 2 == 0 && n > 5 ? 2 : 1))
@@ -337,13 +343,15 @@ __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev&
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
   constexpr int NV = Ph::NV;
-  for (int item = threadIdx.x; item < S::nu * E; item += blockDim.x) {
-    const int el = item % E, u = item / E;
+  constexpr int ND = SDRT_SPLIT_INTFLUX ? D : 1;  // items per point: one per direction, or all
+  for (int item = threadIdx.x; item < S::nu * ND * E; item += blockDim.x) {
+    const int el = item % E, r = item / E, u = r % S::nu, dsel = r / S::nu;
     if (e0 + el >= g.K) {  // padding columns: finite zeros
 #pragma unroll
       for (int d = 0; d < D; ++d)
+        if (ND == 1 || d == dsel)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = 0.0;
+          for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = 0.0;
       continue;
     }
     const int s = sNb[D + 1][el];
@@ -356,6 +364,7 @@ __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev&
     }
 #pragma unroll
     for (int d = 0; d < D; ++d) {
+      if (ND != 1 && d != dsel) continue;
       double w[D], fo[NV];
 #pragma unroll
       for (int j = 0; j < D; ++j) w[j] = g.detJ[s] * g.Jinv[s][d * 3 + j];
@@ -503,7 +512,7 @@ struct SLayoutB {
 };
 
 template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256, SDRT_SB_MINB) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
+__global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
                                                 double dt, const __grid_constant__ STileMaps tm) {
   SPH_INIT
   using Ph = Phys<EQ, D>;
@@ -699,7 +708,7 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
   } else if (which == 1) {
     auto k = ks_stage<D, P, EQ, C::E>;
     sset_smem((const void*)k, C::SMEM_B);
-    k<<<grid, C::THREADS, C::SMEM_B, st>>>(g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true));
+    k<<<grid, SDRT_SB_NT, C::SMEM_B, st>>>(g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true));
   } else {
     auto k = ks_traces<D, P, EQ, C::E>;
     sset_smem((const void*)k, C::SMEM_T);
