@@ -86,6 +86,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SB_MINB
 #define SDRT_SB_MINB 5
 #endif
+#ifndef SDRT_SA_NT
+#define SDRT_SA_NT 256
+#endif
 #ifndef SDRT_SB_NT
 #define SDRT_SB_NT 160
 #endif
@@ -419,7 +422,7 @@ struct SLayoutA {
 };
 
 template <int D, int P, int EQ, int E>
-__global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
+__global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
                                                const __grid_constant__ STileMaps tm) {
   SPH_INIT
   using Ph = Phys<EQ, D>;
@@ -443,7 +446,7 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexO
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
   SPH(0, 0)
-  NbGather<D, P, NV, E, 256> gath;
+  NbGather<D, P, NV, E, SDRT_SA_NT> gath;
   gath.load(g, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
   // U_ext = M0 U, U_u = M12 U
@@ -703,7 +706,7 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
     if constexpr (Phys<EQ, D>::VISC) {
       auto k = ks_grad<D, P, EQ, C::E>;
       sset_smem((const void*)k, C::SMEM_A);
-      k<<<grid, C::THREADS, C::SMEM_A, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
+      k<<<grid, SDRT_SA_NT, C::SMEM_A, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
     }
   } else if (which == 1) {
     auto k = ks_stage<D, P, EQ, C::E>;

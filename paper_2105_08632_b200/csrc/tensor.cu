@@ -703,7 +703,10 @@ struct TCfg {
   // load / compute / store phases interleave
   static constexpr int E = NV > 1 ? 8 : (D == 3 ? 16 : 32);  // kernel B and traces
   static constexpr int EA = E;
-  static constexpr int NTB = 256;
+#ifndef SDRT_TB_NT
+#define SDRT_TB_NT 320
+#endif
+  static constexpr int NTB = SDRT_TB_NT;
 #ifndef SDRT_TA_NT
 #define SDRT_TA_NT 256
 #endif
