@@ -121,3 +121,35 @@ def integrate(L, u, dt, nsteps):
     for _ in range(nsteps):
         u = rk4_step(L, u, dt)
     return u
+
+
+# RK54: five stages, two registers, fourth order (Carpenter & Kennedy 1994, the paper's
+# "RK54 (five stages, two registers and fourth order)"; its stability
+# polynomial is P:1124's sum_{i<=4} z^i/i! + z^5/200).  2N-storage form:
+#   dU <- A_s dU + dt L(U);  U <- U + B_s dU,  s = 0..4 (A_0 = 0).
+# The semi-discrete SDRT operator is autonomous, so the stage times c_s are not needed.
+RK54_A = (0.0,
+          -567301805773.0 / 1357537059087.0,
+          -2404267990393.0 / 2016746695238.0,
+          -3550918686646.0 / 2091501179385.0,
+          -1275806237668.0 / 842570457699.0)
+RK54_B = (1432997174477.0 / 9575080441755.0,
+          5161836677717.0 / 13612068292357.0,
+          1720146321549.0 / 2090206949498.0,
+          3134564353537.0 / 4481467310338.0,
+          2277821191437.0 / 14882151754819.0)
+
+
+def rk54_step(L, u, dt):
+    """One RK54 step in the 2N-storage form above (two registers: u and du)."""
+    du = 0.0 * u
+    for a, b in zip(RK54_A, RK54_B):
+        du = a * du + dt * L(u)
+        u = u + b * du
+    return u
+
+
+def integrate_rk54(L, u, dt, nsteps):
+    for _ in range(nsteps):
+        u = rk54_step(L, u, dt)
+    return u

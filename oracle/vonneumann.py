@@ -64,11 +64,17 @@ def G_of_kappa(blocks, kappa):
 
 
 def rk_amplification(z, stages):
-    """Stability polynomial of classical RK3/RK4 (Eq. rk_exponential, l.1122-1126)."""
+    """Stability polynomial of classical RK3/RK4 (Eq. rk_exponential, l.1122-1126);
+    stages = "rk54": the amplification of one oracle RK54 step (residual.rk54_step)
+    applied to u' = z u, u(0) = 1 (evaluated from the scheme, not from a formula)."""
     if stages == 3:
         return 1 + z + z ** 2 / 2 + z ** 3 / 6
     if stages == 4:
         return 1 + z + z ** 2 / 2 + z ** 3 / 6 + z ** 4 / 24
+    if stages == "rk54":
+        from .residual import rk54_step
+        z = np.asarray(z, dtype=complex)
+        return rk54_step(lambda u: z * u, np.ones_like(z), 1.0)
     raise ValueError(stages)
 
 

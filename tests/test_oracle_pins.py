@@ -447,3 +447,61 @@ def test_design_order_linear_advection(etype, p):
     e2 = _advection_l2_error(etype, p, 16)
     order = math.log2(e1 / e2)
     assert abs(order - (p + 1)) < 0.35, (etype, p, e1, e2, order)
+
+
+# ----------------------------------------------------------------- RK54 (NEXT row N2)
+def test_rk54_stability_polynomial():
+    """The oracle's RK54 step applied to u' = z u reproduces the paper's RK54 stability
+    polynomial sum_{i<=4} z^i/i! + z^5/200 (Eq. rk_exponential) —
+    retyped here from the paper, evaluated against the 2N-storage scheme."""
+    z = np.array([0.3, -1.2, 0.5 + 1.1j, -2.0 + 0.7j, 1.5j])
+    ref = sum(z ** i / math.factorial(i) for i in range(5)) + z ** 5 / 200
+    assert np.abs(VN.rk_amplification(z, "rk54") - ref).max() <= 1e-14
+
+
+def test_rk54_nonlinear_order():
+    """Fourth order on a nonlinear autonomous ODE system ("fourth order")."""
+    from oracle.residual import rk54_step
+
+    def L(u):
+        return np.array([u[1], -np.sin(u[0]) - 0.1 * u[1] * u[0] ** 2])
+
+    def run(n):
+        u = np.array([1.0, 0.0])
+        for _ in range(n):
+            u = rk54_step(L, u, 2.0 / n)
+        return u
+
+    ref = run(4096)
+    e = [np.abs(run(n) - ref).max() for n in (16, 32, 64)]
+    orders = [math.log2(e[i] / e[i + 1]) for i in range(2)]
+    assert all(3.7 < o < 4.4 for o in orders), orders
+
+
+@pytest.mark.parametrize("etype,p", [(e, p) for e in ("quad", "tri") for p in range(1, 5)])
+def test_tau_max_diffusion_rk54(etype, p):
+    """RK54 column of the diffusion tau_MAX tables (l.1562-1565, l.1596-1599) with the
+    oracle's RK54 amplification; same protocol as the RK3/RK4 pin."""
+    B = VN.pattern_blocks(etype, p, VN.diffusion_physics(2), layers=2)
+    lam = VN.spectrum(B, [np.array([k, 0.0]) for k in np.linspace(0, 2 * np.pi, 361)])
+    ref = GOLD["tau_max_rk54"]["diffusion"][etype][str(p)]
+    assert abs(VN.tau_max(lam, "rk54") - ref) <= 1.5e-4, (VN.tau_max(lam, "rk54"), ref)
+
+
+@pytest.mark.parametrize("etype,p", [("quad", 1), ("quad", 2), ("quad", 3), ("quad", 4), ("hex", 1), ("hex", 3)])
+def test_tau_max_advection_rk54(etype, p):
+    """RK54 column of the advection tau_MAX tables (l.1219-1222, l.1294-1297); protocol
+    of test_tau_max_advection_rk4_table (kappa parallel to c), except quad p = 1 where the
+    paper's 0.695 is the full-Brillouin-zone value (the kappa-parallel sweep gives 0.718;
+    the paper does not state its sweep)."""
+    D = ND[etype]
+    ph = VN.advection_physics(D)
+    d = np.array(ph.c)
+    B = VN.pattern_blocks(etype, p, ph, layers=1)
+    if (etype, p) == ("quad", 1):
+        ks = np.linspace(-np.pi, np.pi, 41)
+        lam = VN.spectrum(B, [np.array([a, b]) for a in ks for b in ks])
+    else:
+        lam = VN.spectrum(B, [k * d for k in np.linspace(0, np.pi / np.abs(d).max(), 401)])
+    ref = GOLD["tau_max_rk54"]["advection"][etype][str(p)]
+    assert abs(VN.tau_max(lam, "rk54") - ref) <= 1e-2, (VN.tau_max(lam, "rk54"), ref)
