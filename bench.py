@@ -272,6 +272,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="sdrt", choices=["sdrt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--integrator", default="rk4", choices=["rk4", "rk54"],
+                    help="rk4: classical (BASELINE.json configs); rk54: the paper's PM protocol (N_RK = 5)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
@@ -315,7 +317,12 @@ def main():
         return bool(torch.isfinite(U[:, :, :K]).all().item())
 
     # ---------------------------------------------------------------- warm-up
-    S.rk_step(U, cfg.dt, args.warmup)
+    NST = 4 if args.integrator == "rk4" else 5  # stages per step
+
+    def step_fn(solver):
+        return solver.rk_step if args.integrator == "rk4" else solver.rk54_step
+
+    step_fn(S)(U, cfg.dt, args.warmup)
     torch.cuda.synchronize(dev)
     dbg = {"after_warmup": finite_now()}
     clocks = ClockSampler(local)
@@ -330,7 +337,7 @@ def main():
     e0.record(stream)
     launches = 0
     for _ in range(args.steps):
-        S.rk_step(U, cfg.dt, 1)
+        step_fn(S)(U, cfg.dt, 1)
         launches += S.last_launches()
     e1.record(stream)
     torch.cuda.synchronize(dev)
@@ -344,7 +351,7 @@ def main():
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
     for _ in range(args.steps):
-        S.rk_step(U, cfg.dt, 1)
+        step_fn(S)(U, cfg.dt, 1)
     e3.record(stream)
     torch.cuda.synchronize(dev)
     ms_clean = e2.elapsed_time(e3)
@@ -355,7 +362,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, ms_clean_max = float(t[0]), float(t[1])
-    total_dof_stages = dof * 4 * args.steps * world
+    total_dof_stages = dof * NST * args.steps * world
     value = total_dof_stages / (ms_max * 1e-3) / 1e9
 
     # ---------------------------------------------------------------- e2e (host buffers)
@@ -384,7 +391,7 @@ def main():
         k = i % 2 if world == 1 else 0
         with torch.cuda.stream(side[k]):
             bufs[k].copy_(pin, non_blocking=True)
-            solvers[k].rk_step(bufs[k], cfg.dt, 1)
+            step_fn(solvers[k])(bufs[k], cfg.dt, 1)
             outs[k].copy_(bufs[k], non_blocking=True)
     for sd in side:
         stream.wait_stream(sd)
@@ -435,8 +442,8 @@ def main():
                  "step_share": dom_ms / ms if dom else None})
     model_b = stage_model_bytes(cfg)
     stage_roof = {"model_bytes_per_dof_stage": model_b,
-                  "achieved_gbs": model_b * dof * 4 * args.steps / (ms_clean_max * 1e-3) / 1e9,
-                  "frac_of_hbm": model_b * dof * 4 * args.steps / (ms_clean_max * 1e-3) / 1e9 / hbm,
+                  "achieved_gbs": model_b * dof * NST * args.steps / (ms_clean_max * 1e-3) / 1e9,
+                  "frac_of_hbm": model_b * dof * NST * args.steps / (ms_clean_max * 1e-3) / 1e9 / hbm,
                   "ceiling_gdof_stage_s": hbm / model_b}
 
     # ---------------------------------------------------------------- cpu baseline
@@ -457,6 +464,7 @@ def main():
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": {"workload": WORKLOADS[cfg.name], "elements_per_gpu": K, "dof_per_gpu": dof,
                           "p": cfg.p, "dt": cfg.dt, "parallelism": parallelism,
+                          "integrator": "classical RK4 (4 stages)" if NST == 4 else "RK54 (5 stages, 2 registers)",
                           "l2": "working set > L2 (state 3 registers + traces >> 126 MB); no flush needed"
                           if dof * 8 * 3 > 126e6 else "working set fits L2 (small config)"},
                "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,

@@ -144,6 +144,11 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
  * stream every check_every steps and returns SDRT_E_DIVERGED (message names the
  * first non-finite / non-physical element and step) if the state went bad. */
 sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream);
+/* nsteps steps of RK54 (five stages, two registers, fourth order; PAPER.md l.1120,
+ * l.1200, stability polynomial l.1124; Carpenter & Kennedy 2N-storage coefficients),
+ * in place on d_U; the context's RK accumulator holds the second register.  Fused
+ * element paths only (SDRT_E_UNSUPPORTED otherwise).  check_every as sdrt_rk_step. */
+sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream);
 /* Per-kernel device timing (CUDA events recorded on the launching stream around each
  * kernel) for measurement: enable, run, then read per-kernel totals.  names receives
  * max_tags NUL-terminated strings of 64 bytes each (may be NULL); ms/counts get the
@@ -158,7 +163,8 @@ sdrt_status sdrt_ctx_kernel_times(sdrt_ctx* c, int max_tags, char* names, double
  *     sdrt_stage_grad(U, s)   (viscous only)   viscous traces       -> exchange which=1
  *     sdrt_stage_flux(U, s, dt, NULL)          RK stage, new traces -> exchange which=0
  * stage = -1 with d_out computes dU/dt into d_out instead (residual).  The stage input
- * is U for s <= 0 and the internal stage register otherwise. */
+ * is U for s <= 0 and the internal stage register otherwise.  RK54 stages are
+ * stage = 10 + s, s = 0..4 (stage input U, updated in place). */
 sdrt_status sdrt_stage_traces(sdrt_ctx* c, const double* d_U, void* stream);
 sdrt_status sdrt_stage_grad(sdrt_ctx* c, double* d_U, int stage, void* stream);
 sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, void* stream);

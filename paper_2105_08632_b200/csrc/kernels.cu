@@ -26,6 +26,7 @@
 #include "ctx.h"
 #include "tensor.cuh"
 #include "simplex.cuh"
+#include "rk.cuh"
 
 namespace sdrt {
 
@@ -1107,6 +1108,45 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
   })
 }
 
+sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream) {
+  if (!c || !d_U || nsteps < 0) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (!c->fused && !c->sfused) {
+    set_error("unsupported: RK54 needs a fused path (tensor or simplex kernels)");
+    return SDRT_E_UNSUPPORTED;
+  }
+  SDRT_TRY({
+    c->launches = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->needs_halo && !c->auto_halo) {
+      set_error("unsupported: multi-rank context; use the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
+      return SDRT_E_UNSUPPORTED;
+    }
+    if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
+    if (c->sfused && nsteps > 0) sfused_traces(c, d_U, st);
+    for (int step = 0; step < nsteps; ++step) {
+      for (int s = 0; s < 5; ++s) {
+        if (c->fused) fused_stage(c, d_U, d_U, RK54_STAGE0 + s, dt, nullptr, st);
+        else sfused_stage(c, d_U, d_U, RK54_STAGE0 + s, dt, nullptr, st);
+      }
+      CUDA_OK(cudaGetLastError());
+      if (check_every > 0 && (step + 1) % check_every == 0) {
+        int64_t bad;
+        if (!pick_chk(c->eq, c->nd)(c, d_U, st, &bad)) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "diverged: element %lld non-finite or non-physical after step %d",
+                   (long long)bad, step + 1);
+          set_error(buf);
+          return SDRT_E_DIVERGED;
+        }
+      }
+    }
+    return SDRT_OK;
+  })
+}
+
 sdrt_status sdrt_halo_info(const sdrt_ctx* c, int* nslab, int* peer, int* d, int* side, int64_t* offset) {
   if (!c || !nslab) {
     set_error("null argument");
@@ -1174,6 +1214,11 @@ sdrt_status sdrt_stage_flux(sdrt_ctx* c, double* d_U, int stage, double dt, doub
 
 }  // extern "C"
 
+// stage codes accepted by the staged API (rk.cuh): -1, RK4 0..3, RK54 10..14
+static bool stage_valid(int stage) {
+  return (stage >= -1 && stage <= 3) || (stage >= RK54_STAGE0 && stage < RK54_STAGE0 + 5);
+}
+
 // geometry restricted to a tile subset: part 0 = all tiles, 1 = interior, 2 = boundary
 static bool part_geom(sdrt_ctx* c, int part, TensorGeom* tg, GeomDev* g) {
   *tg = c->tg;
@@ -1193,14 +1238,14 @@ static bool part_geom(sdrt_ctx* c, int part, TensorGeom* tg, GeomDev* g) {
 extern "C" {
 
 sdrt_status sdrt_stage_grad_part(sdrt_ctx* c, double* d_U, int stage, int part, void* stream) {
-  if (!c || !d_U || stage < -1 || stage > 3 || part < 0 || part > 2 || (!c->fused && !c->sfused)) {
+  if (!c || !d_U || !stage_valid(stage) || part < 0 || part > 2 || (!c->fused && !c->sfused)) {
     set_error("invalid argument");
     return SDRT_E_INVALID_ARG;
   }
   if (!c->visc) return SDRT_OK;
   SDRT_TRY({
     cudaStream_t st = (cudaStream_t)stream;
-    const double* Uin = stage <= 0 ? d_U : c->Us;
+    const double* Uin = (stage <= 0 || stage >= RK54_STAGE0) ? d_U : c->Us;
     TensorGeom tgp;
     GeomDev gp;
     if (!part_geom(c, part, &tgp, &gp)) return SDRT_OK;
@@ -1229,14 +1274,14 @@ sdrt_status sdrt_stage_grad_part(sdrt_ctx* c, double* d_U, int stage, int part, 
 
 sdrt_status sdrt_stage_flux_part(sdrt_ctx* c, double* d_U, int stage, double dt, double* d_out, int part,
                                  void* stream) {
-  if (!c || !d_U || stage < -1 || stage > 3 || (stage == -1 && !d_out) || part < 0 || part > 2 ||
+  if (!c || !d_U || !stage_valid(stage) || (stage == -1 && !d_out) || part < 0 || part > 2 ||
       (!c->fused && !c->sfused)) {
     set_error("invalid argument");
     return SDRT_E_INVALID_ARG;
   }
   SDRT_TRY({
     cudaStream_t st = (cudaStream_t)stream;
-    const double* Uin = stage <= 0 ? d_U : c->Us;
+    const double* Uin = (stage <= 0 || stage >= RK54_STAGE0) ? d_U : c->Us;
     TensorGeom tgp;
     GeomDev gp;
     const bool any = part_geom(c, part, &tgp, &gp);

@@ -28,6 +28,7 @@
 #include <string>
 
 #include "simplex.cuh"
+#include "rk.cuh"
 #include "tma.cuh"
 
 namespace sdrt {
@@ -541,11 +542,11 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
     mbar_fence_init();
     mbar_expect_tx(&bar[0], TB);
     tma_tile<S::nsol * NV, E>(sU, &tm.uin, e0, &bar[0]);
-    const unsigned later = (INT ? 0 : TB) + ((stage == 1 || stage == 2) ? TB : 0) + (stage >= 1 ? TB : 0);
+    const unsigned later = (INT ? 0 : TB) + (stage_reads_un(stage) ? TB : 0) + (stage_reads_acc(stage) ? TB : 0);
     mbar_expect_tx(&bar[1], later);
     if constexpr (!INT) tma_tile<S::nsol * NV, E>(sR, &tm.rint, e0, &bar[1]);
-    if (stage == 1 || stage == 2) tma_tile<S::nsol * NV, E>(sUn, &tm.un, e0, &bar[1]);
-    if (stage >= 1) tma_tile<S::nsol * NV, E>(sAcc, &tm.acc, e0, &bar[1]);
+    if (stage_reads_un(stage)) tma_tile<S::nsol * NV, E>(sUn, &tm.un, e0, &bar[1]);
+    if (stage_reads_acc(stage)) tma_tile<S::nsol * NV, E>(sAcc, &tm.acc, e0, &bar[1]);
   }
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
@@ -650,10 +651,17 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
         nu = fma(dt, kk, sUn[idx]);
         b.Us[gi] = nu;
         break;
-      default:
+      case 3:
         nu = fma(dt / 6.0, kk, sAcc[idx]);
         b.U[gi] = nu;
         break;
+      default: {  // RK54 stage s (2N-storage, in place)
+        const int s5 = stage - RK54_STAGE0;
+        const double du = s5 == 0 ? dt * kk : fma(rk54_a(s5), sAcc[idx], dt * kk);
+        b.ACC[gi] = du;
+        nu = fma(rk54_b(s5), du, sU[idx]);
+        b.U[gi] = nu;
+      } break;
     }
     sU[idx] = nu;
   }

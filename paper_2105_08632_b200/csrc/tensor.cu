@@ -30,6 +30,7 @@
 #include <string>
 
 #include "tensor.cuh"
+#include "rk.cuh"
 #include "tma.cuh"
 
 namespace sdrt {
@@ -475,8 +476,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   double* sU = smem;
   double* sR = smem + NS * NV * E;    // R~ accumulator, starts as R_int (kernel A)
   double* sF = sR + NS * NV * E;      // [NL][NF][NV][E] flux-line values of one direction
-  double* sAcc = sF + NL * NF * NV * E;                             // RK accumulator (stages 1..3)
-  double* sUn = sAcc + (stage >= 1 ? NS * NV * E : 0);              // RK register u_n (stages 1, 2)
+  double* sAcc = sF + NL * NF * NV * E;                             // RK accumulator / RK54 dU
+  double* sUn = sAcc + (stage_reads_acc(stage) ? NS * NV * E : 0);  // RK register u_n (RK4 stages 1, 2)
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar[2];
   const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
@@ -490,11 +491,11 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
     mbar_fence_init();
     mbar_expect_tx(&bar[0], TB);
     tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar[0]);
-    const unsigned later = (Ph::VISC ? TB : 0) + ((stage == 1 || stage == 2) ? TB : 0) + (stage >= 1 ? TB : 0);
+    const unsigned later = (Ph::VISC ? TB : 0) + (stage_reads_un(stage) ? TB : 0) + (stage_reads_acc(stage) ? TB : 0);
     mbar_expect_tx(&bar[1], later);
     if constexpr (Ph::VISC) tma_tile<NS * NV, E>(sR, &tm.rv, e0, &bar[1]);
-    if (stage == 1 || stage == 2) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar[1]);
-    if (stage >= 1) tma_tile<NS * NV, E>(sAcc, &tm.acc, e0, &bar[1]);
+    if (stage_reads_un(stage)) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar[1]);
+    if (stage_reads_acc(stage)) tma_tile<NS * NV, E>(sAcc, &tm.acc, e0, &bar[1]);
   }
   fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();
@@ -660,10 +661,17 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
           nu = fma(dt, kk, sUn[idx]);
           b.Us[gi] = nu;
           break;
-        default:
+        case 3:
           nu = fma(dt / 6.0, kk, sAcc[idx]);
           b.U[gi] = nu;
           break;
+        default: {  // RK54 stage s (2N-storage, in place)
+          const int s5 = stage - RK54_STAGE0;
+          const double du = s5 == 0 ? dt * kk : fma(rk54_a(s5), sAcc[idx], dt * kk);
+          b.ACC[gi] = du;
+          nu = fma(rk54_b(s5), du, sU[idx]);
+          b.U[gi] = nu;
+        } break;
       }
       un[i] = nu;
       sU[idx] = nu;
@@ -724,7 +732,7 @@ struct TCfg {
   // 1..3, u_n: stages 1, 2)
   static constexpr size_t SMEM_B0 = TILE * 2 + (size_t)NL * (VISC ? 2 : P + 2) * NV * E * sizeof(double);
   static size_t smem_b(int stage) {
-    return SMEM_B0 + (stage >= 1 ? TILE : 0) + ((stage == 1 || stage == 2) ? TILE : 0);
+    return SMEM_B0 + (stage_reads_acc(stage) ? TILE : 0) + (stage_reads_un(stage) ? TILE : 0);
   }
   static constexpr size_t SMEM_T = TILE;
 };

@@ -112,8 +112,15 @@ class DistSolver(Solver):
         sdrt.stage_flux(self.ctx, U.data_ptr(), -1, 0.0, out.data_ptr(), st)
         return out
 
+    def rk54_step(self, U, dt, nsteps=1, check_every=0):
+        """RK54 over the same overlapped staged sequence (stage codes 10..14)."""
+        return self._steps(U, dt, nsteps, [sdrt.RK54_STAGE0 + s for s in range(5)])
+
     def rk_step(self, U, dt, nsteps=1, check_every=0):
-        """RK4 with the halo exchange overlapped with interior work: each
+        return self._steps(U, dt, nsteps, [0, 1, 2, 3])
+
+    def _steps(self, U, dt, nsteps, stages):
+        """Time steps with the halo exchange overlapped with interior work: each
         exchange is posted, the interior tiles (no ghost reads) run while it is in
         flight, then the boundary tiles after the unpack.  Same arithmetic per element
         as the unsplit stage, so the result is identical."""
@@ -122,7 +129,7 @@ class DistSolver(Solver):
         sdrt.stage_traces(self.ctx, U_ptr, st)
         h0 = self.start_exchange(0)
         for _ in range(nsteps):
-            for s in range(4):
+            for s in stages:
                 if self.visc:
                     sdrt.stage_grad_part(self.ctx, U_ptr, s, 1, st)
                     self.finish_exchange(h0)

@@ -69,6 +69,7 @@ lib.sdrt_ctx_workspace_bytes.restype = ctypes.c_size_t
 lib.sdrt_ctx_create.argtypes = [_vp, _vp, ctypes.POINTER(PhysicsT), _vp, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)]
 lib.sdrt_residual.argtypes = [_vp, _vp, _vp, _vp]
 lib.sdrt_rk_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
+lib.sdrt_rk54_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
 lib.sdrt_mesh_set_halo.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_mesh_halo_lists.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 lib.sdrt_mesh_neighbor.argtypes = [_vp, ctypes.c_int64, ctypes.c_int, _vp, _vp]
@@ -271,6 +272,13 @@ def halo_unpack(ctx, which, recv_ptr, stream):
 
 def stage_traces(ctx, U_ptr, stream):
     _check(lib.sdrt_stage_traces(ctx, _vp(U_ptr), _vp(stream)))
+
+
+def rk54_step(ctx, U_ptr, dt, nsteps, check_every, stream):
+    _check(lib.sdrt_rk54_step(ctx, _vp(U_ptr), float(dt), int(nsteps), int(check_every), _vp(stream)))
+
+
+RK54_STAGE0 = 10  # staged-API stage code of RK54 stage 0 (include/sdrt.h)
 
 
 def stage_grad(ctx, U_ptr, stage, stream):

@@ -67,6 +67,12 @@ class Solver:
                      torch.cuda.current_stream(self.device).cuda_stream)
         return U
 
+    def rk54_step(self, U, dt, nsteps=1, check_every=0):
+        """RK54 (five stages, two registers)."""
+        sdrt.rk54_step(self.ctx, U.data_ptr(), dt, nsteps, check_every,
+                       torch.cuda.current_stream(self.device).cuda_stream)
+        return U
+
     def set_timing(self, enable):
         sdrt.ctx_set_timing(self.ctx, enable)
 

@@ -143,3 +143,8 @@ def test_overlapped_stage_parts_bitwise(name, N, steps):
     a, b = S1.to_host(U1), S0.to_host(U2)
     assert S1.exchanges > 0
     assert np.array_equal(a, b), float(np.abs(a - b).max())
+    # the RK54 stages through the same overlapped sequence
+    S1.rk54_step(U1, cfg.dt, 1)
+    S0.rk54_step(U2, cfg.dt, 1)
+    a, b = S1.to_host(U1), S0.to_host(U2)
+    assert np.array_equal(a, b), float(np.abs(a - b).max())

@@ -142,3 +142,19 @@ def test_full_size_invariants(name):
     S.rk_step(Ud, cfg.dt, 1)
     assert np.isfinite(S.to_host(Ud)[:, :, :K]).all()
     S.close()
+
+
+@pytest.mark.parametrize("name,N,steps", [("c1", 8, 50), ("c2", 6, 20), ("c3", 3, 5), ("c4", 4, 5), ("c5", 3, 3)])
+def test_rk54_parity(name, N, steps):
+    """RK54 (NEXT row N2): the fused kernels' 2N-storage stages
+    against the oracle's rk54_step (itself pinned to the paper's stability polynomial and
+    tau_MAX RK54 columns)."""
+    from oracle.residual import integrate_rk54
+    cfg = CONFIGS[name]
+    m, R, S = _pair(cfg, N)
+    U0 = initial_state(cfg, m.sol_coords())
+    ref = integrate_rk54(R, U0, cfg.dt, steps)
+    Ud = S.to_device(U0)
+    S.rk54_step(Ud, cfg.dt, steps, check_every=steps)
+    got = S.to_host(Ud)
+    assert _rel(got, ref) <= TOL, _rel(got, ref)
