@@ -720,7 +720,7 @@ struct TCfg {
 #endif
   static constexpr int NTA = SDRT_TA_NT;
 #ifndef SDRT_TB_MINB
-#define SDRT_TB_MINB 3
+#define SDRT_TB_MINB 2
 #endif
   static constexpr int MINB_B = SDRT_TB_MINB;
   static constexpr int MINB_A = 2;
