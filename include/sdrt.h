@@ -149,6 +149,13 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
  * in place on d_U; the context's RK accumulator holds the second register.  Fused
  * element paths only (SDRT_E_UNSUPPORTED otherwise).  check_every as sdrt_rk_step. */
 sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream);
+/* Taylor-Green-vortex diagnostics of the device state d_U:
+ * d_out (3 device doubles) = { <E*> = <rho v.v>, eps2 = 2 mu <S^d : S^d>,
+ * eps3 = -<p div v> } with rho_inf = v_inf = L = t_c = 1, ensemble averages by the
+ * solution-point quadrature sum_e detJ_e sum_r w_r / |Omega| (DESIGN.md reading), grad v
+ * from the LDG gradient (l.295-302).  eps1 = -d<E*>/dt is left to the caller.  Single-rank
+ * 3-D NS contexts on a fused path; SDRT_E_UNSUPPORTED otherwise.  Enqueued on stream. */
+sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void* stream);
 /* Per-kernel device timing (CUDA events recorded on the launching stream around each
  * kernel) for measurement: enable, run, then read per-kernel totals.  names receives
  * max_tags NUL-terminated strings of 64 bytes each (may be NULL); ms/counts get the

@@ -292,6 +292,28 @@ __global__ void k_halo_unpack(double* __restrict__ T, int64_t Kt, int NV, const 
   T[trace_at(row[k], v, col[k], Kt, NV, pm)] = buf[idx];
 }
 
+// sum of the per-tile diagnostics partials in a fixed order (one block), scaled:
+// out = { <rho v.v>, 2 mu <S:S>, -<p div v> }
+__global__ void k_diag_final(const double* __restrict__ part, int64_t ntile, double inv_vol, double mu,
+                             double* __restrict__ out) {
+  __shared__ double red[3][256];
+  double a[3] = {0.0, 0.0, 0.0};
+  for (int64_t t = threadIdx.x; t < ntile; t += 256)
+    for (int k = 0; k < 3; ++k) a[k] += part[3 * t + k];
+  for (int k = 0; k < 3; ++k) red[k][threadIdx.x] = a[k];
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h)
+      for (int k = 0; k < 3; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = red[0][0] * inv_vol;
+    out[1] = 2.0 * mu * red[1][0] * inv_vol;
+    out[2] = -red[2][0] * inv_vol;
+  }
+}
+
 // ------------------------------------------------------------------------ host side
 struct OpHost {
   std::vector<int> ptr, col;
@@ -322,7 +344,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_tiles, total;
+      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_tiles, off_diag, total;
   size_t ops_bytes;
 };
 
@@ -388,6 +410,9 @@ struct sdrt_ctx {
   TensorTma tma;
   // interior / boundary tile lists (multi-rank overlap): tiles of tile_w elements
   int tile_w = 0, n_int = 0, n_bnd = 0;
+  double* d_part = nullptr;  // diagnostics partial sums
+  double* d_w = nullptr;     // solution-point quadrature weights w_r (App. B reading of l.2052)
+  double diag_vol = 0.0;     // sum_e detJ_e sum_r w_r
   const int* d_tiles = nullptr;  // [n_int interior tiles][n_bnd boundary tiles]
   double* Tu[2] = {nullptr, nullptr};
   double* Tg = nullptr;
@@ -507,6 +532,9 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   // interior / boundary tile lists of the fused paths (tiles of >= 8 elements)
   p.off_tiles = o;
   o += align256(((size_t)m.K / 8 + 2) * sizeof(int32_t));
+  // TGV diagnostics: per-tile partial sums (3 per tile of >= 8 elements) + weights w
+  p.off_diag = o;
+  o += align256((3 * ((size_t)m.K / 8 + 2) + r.nsol + 8) * sizeof(double));
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -734,6 +762,16 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tu[1] = (double*)(base + p.off_tu1);
       c->Tg = (double*)(base + p.off_tg);
       CUDA_OK(cudaStreamSynchronize(st));
+    }
+    // diagnostics buffers: weights w and the quadrature volume
+    c->d_w = (double*)(base + p.off_diag);
+    c->d_part = c->d_w + ((r.nsol + 7) / 8) * 8;
+    CUDA_OK(cudaMemcpyAsync(c->d_w, O.w.data(), r.nsol * sizeof(double), cudaMemcpyHostToDevice, st));
+    {
+      double sw = 0.0, sd = 0.0;
+      for (int i = 0; i < r.nsol; ++i) sw += O.w[i];
+      for (int64_t e = 0; e < m.K; ++e) sd += m.detJ[e % m.nsub];
+      c->diag_vol = sw * sd;
     }
     // interior / boundary tile lists for the overlapped multi-rank stage:
     // a tile is interior if none of its elements lies in a pattern layer next to a
@@ -1143,6 +1181,41 @@ sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int 
         }
       }
     }
+    return SDRT_OK;
+  })
+}
+
+sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void* stream) {
+  if (!c || !d_U || !d_out) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (c->eq != SDRT_EQ_NS || c->nd != 3 || (!c->fused && !c->sfused) || c->needs_halo) {
+    set_error("unsupported: TGV diagnostics need a single-rank 3-D Navier-Stokes context on a fused path");
+    return SDRT_E_UNSUPPORTED;
+  }
+  SDRT_TRY({
+    cudaStream_t st = (cudaStream_t)stream;
+    c->launches = 0;
+    int64_t ntile;
+    if (c->fused) {
+      fused_traces(c, d_U, st);
+      TensorBufs b{};
+      b.Uin = d_U;
+      b.Tu = c->Tu[c->cur];
+      tensor_launch_diag(c->nd, c->p, c->tg, c->line, c->ph, &c->tma, b, c->d_w, c->d_part, st);
+      ntile = (c->g.K + tensor_tile_width(c->nd, c->p, c->eq) - 1) / tensor_tile_width(c->nd, c->p, c->eq);
+    } else {
+      sfused_traces(c, d_U, st);
+      SimplexBufs b{};
+      b.Uin = d_U;
+      b.Tu = c->Tu[c->cur];
+      simplex_launch_diag(c->nd, c->p, c->g, c->sops, c->ph, &c->stma, b, c->d_w, c->d_part, st);
+      ntile = (c->g.K + 7) / 8;
+    }
+    k_diag_final<<<1, 256, 0, st>>>(c->d_part, ntile, 1.0 / c->diag_vol, c->ph.mu, d_out);
+    c->launches += 2;
+    CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })
 }

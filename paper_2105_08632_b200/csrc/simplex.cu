@@ -673,6 +673,95 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   SPH(1, 7)
 }
 
+// TGV diagnostics (NEXT row N4): per tile the solution-point
+// quadrature sums (w_r detJ_s) of E* = rho v.v, S^d : S^d and p div v, grad v from the
+// LDG gradient (the prologue of kernel A) by the chain rule (reading O20).
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256) ks_diag(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, const double* w,
+                                               double* part, const __grid_constant__ STileMaps tm) {
+  using Ph = Phys<EQ, D>;
+  using S = SDims<D, P>;
+  constexpr int NV = Ph::NV, NT = 256;
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;
+  double* sUe = sU + S::nsol * NV * E;
+  double* sUu = sUe + S::next * NV * E;
+  double* sC = sUu + S::nu * NV * E;
+  double* sQ = sC + S::next * NV * E;
+  __shared__ double red[3 * NT];
+  __shared__ int sNb[D + 2][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, S::nsol * NV * E * 8);
+    tma_tile<S::nsol * NV, E>(sU, &tm.uin, e0, &bar);
+  }
+  fill_neighbours<D, E>(g, sNb, e0);
+  __syncthreads();
+  NbGather<D, P, NV, E, NT> gath;
+  gath.load(g, b.Tu, sNb, e0);
+  mbar_wait(&bar, 0);
+  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, O.M12, sU, 1 << 30, sU, sUu);
+  __syncthreads();
+  gath.common_values(g, ph, sUe, sNb, sC, e0);
+  __syncthreads();
+  dmm1<NV, S::kt_G, E, false>(O.G, sC, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
+  __syncthreads();
+  metric_grad<D, P, NV, E>(g, sNb, sQ);
+  __syncthreads();
+  double acc[3] = {0.0, 0.0, 0.0};
+  if constexpr (NV == D + 2) {
+    for (int item = threadIdx.x; item < S::nsol * E; item += NT) {
+      const int el = item % E, sp = item / E;
+      if (e0 + el >= g.K) continue;
+      const int s = sNb[D + 1][el];
+      const double rho = sU[(sp * NV) * E + el];
+      double v[D], vv = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        v[i] = sU[(sp * NV + 1 + i) * E + el] / rho;
+        vv += v[i] * v[i];
+      }
+      const double pr = (ph.gamma - 1.0) * (sU[(sp * NV + D + 1) * E + el] - 0.5 * rho * vv);
+      double dv[D][D];  // dv[j][i] = d v_i / d x_j
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          dv[j][i] = (sQ[((sp * D + j) * NV + 1 + i) * E + el] - v[i] * sQ[((sp * D + j) * NV) * E + el]) / rho;
+      double div = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) div += dv[i][i];
+      double ss = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double sij = 0.5 * (dv[j][i] + dv[i][j]) - (i == j ? div / 3.0 : 0.0);
+          ss += sij * sij;
+        }
+      const double wr = w[sp] * g.detJ[s];
+      acc[0] += wr * rho * vv;
+      acc[1] += wr * ss;
+      acc[2] += wr * pr * div;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) red[k * NT + threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int h = NT / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) red[k * NT + threadIdx.x] += red[k * NT + threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) part[3 * blockIdx.x + k] = red[k * NT];
+}
+
 // ------------------------------------------------------------------ launchers
 template <int D, int P, int EQ>
 struct SCfg {
@@ -774,6 +863,22 @@ static SFn spick(int D, int P, int eq, STmaFn* m) {
 int simplex_tile_width(int D, int P, int eq) {
   (void)D; (void)P; (void)eq;
   return 8;  // SCfg<...>::E for every instantiation
+}
+
+void simplex_launch_diag(int D, int P, const GeomDev& g, const SimplexOps& O, const PhysDev& ph, SimplexTma* tma,
+                         const SimplexBufs& b, const double* w, double* part, cudaStream_t st) {
+  if (D != 3 || P < 1 || P > 3) throw std::runtime_error("unsupported: TGV diagnostics need a 3-D NS context");
+  auto launch = [&](auto kern, size_t per_el) {
+    const size_t sm = per_el * 8 * sizeof(double);
+    sset_smem((const void*)kern, sm);
+    const unsigned grid = (unsigned)((g.K + 7) / 8);
+    kern<<<grid, 256, sm, st>>>(g, O, ph, b, w, part, smaps(tma, b, b.Uin, false));
+  };
+  // regions per element: U, U_ext, U_u, C, Q  (N_V = 5)
+  auto per_el = [](int nsol, int next, int nu) { return (size_t)(4 * nsol + 2 * next + nu) * 5; };
+  if (P == 1) launch(ks_diag<3, 1, EQ_NS, 8>, per_el(SDims<3, 1>::nsol, SDims<3, 1>::next, SDims<3, 1>::nu));
+  else if (P == 2) launch(ks_diag<3, 2, EQ_NS, 8>, per_el(SDims<3, 2>::nsol, SDims<3, 2>::next, SDims<3, 2>::nu));
+  else launch(ks_diag<3, 3, EQ_NS, 8>, per_el(SDims<3, 3>::nsol, SDims<3, 3>::next, SDims<3, 3>::nu));
 }
 
 bool simplex_supported(int D, int P, int eq) {

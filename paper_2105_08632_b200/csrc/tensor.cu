@@ -699,6 +699,94 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   PH(1, 15)
 }
 
+// TGV diagnostics (NEXT row N4): per tile the solution-point
+// quadrature sums of E* = rho v.v, S^d : S^d and p div v, with grad v from the LDG
+// gradient (GradNb) by the chain rule (reading O20).  part[3 tile + k] (fixed-order
+// block reduction: deterministic).
+template <int NT>
+__device__ __forceinline__ void block_sum3(double (&a)[3], double* red, double* out) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) red[k * NT + threadIdx.x] = a[k];
+  __syncthreads();
+  for (int h = NT / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) red[k * NT + threadIdx.x] += red[k * NT + threadIdx.x + h];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out[k] = red[k * NT];
+}
+
+template <int D, int P, int EQ, int E, int NT>
+__global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, const double* w,
+                                              double* part, const __grid_constant__ TileMaps tm) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, NS = T::NS;
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;
+  double* sQ = smem + NS * NV * E;
+  __shared__ double red[3 * NT];
+  __shared__ int sNb[2 * D][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)blockIdx.x * E;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, NS * NV * E * 8);
+    tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar);
+  }
+  fill_nbrs<D, E>(g, sNb, e0);
+  __syncthreads();
+  {
+    GradNb<D, P, EQ, E, NT> gn;
+    gn.load(g, b.Tu, sNb, e0);
+    mbar_wait(&bar, 0);
+    __syncthreads();
+    gn.compute(g, L, ph, sU, sQ, e0);
+  }
+  __syncthreads();
+  double acc[3] = {0.0, 0.0, 0.0};
+  if constexpr (NV == D + 2) {
+    for (int item = threadIdx.x; item < NS * E; item += NT) {
+      const int el = item % E, sp = item / E;
+      if (e0 + el >= g.K) continue;
+      const double rho = sU[(sp * NV) * E + el];
+      double v[D], vv = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        v[i] = sU[(sp * NV + 1 + i) * E + el] / rho;
+        vv += v[i] * v[i];
+      }
+      const double pr = (ph.gamma - 1.0) * (sU[(sp * NV + D + 1) * E + el] - 0.5 * rho * vv);
+      double dv[D][D];  // dv[j][i] = d v_i / d x_j
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          dv[j][i] = (sQ[((j * NS + sp) * NV + 1 + i) * E + el] - v[i] * sQ[((j * NS + sp) * NV) * E + el]) / rho;
+      double div = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) div += dv[i][i];
+      double ss = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+          const double sij = 0.5 * (dv[j][i] + dv[i][j]) - (i == j ? div / 3.0 : 0.0);
+          ss += sij * sij;
+        }
+      const double wr = w[sp] * g.detJ;
+      acc[0] += wr * rho * vv;
+      acc[1] += wr * ss;
+      acc[2] += wr * pr * div;
+    }
+  }
+  block_sum3<NT>(acc, red, part + 3 * blockIdx.x);
+}
+
 // ------------------------------------------------------------------ launchers
 template <int D, int P, int EQ>
 struct TCfg {
@@ -790,6 +878,17 @@ static void run_traces(const TensorGeom& g, const Line1D& L, TensorTma* tma, con
   TensorBufs b{};
   b.Uin = U;
   k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, L, maps_for(tma, b, false), Tu);
+}
+
+template <int D, int P, int EQ>
+static void run_diag(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
+                     const double* w, double* part, cudaStream_t st) {
+  using C = TCfg<D, P, EQ>;
+  const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
+  auto k = kt_diag<D, P, EQ, C::E, 256>;
+  const size_t sm = C::TILE * (1 + D);
+  set_smem<D, P, EQ>((const void*)k, sm);
+  k<<<grid, 256, sm, st>>>(g, L, ph, b, w, part, maps_for(tma, b, false));
 }
 
 template <int D, int P, int EQ>
@@ -890,6 +989,17 @@ void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D&
   TmaFn m;
   pick_all(D, P, eq, &s, &t, &m);
   s(g, L, ph, tma, b, stage, dt, st, 1);
+}
+
+void tensor_launch_diag(int D, int P, const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
+                        const TensorBufs& b, const double* w, double* part, cudaStream_t st) {
+  if (D != 3) throw std::runtime_error("unsupported: TGV diagnostics need a 3-D NS context");
+  switch (P) {
+    case 1: run_diag<3, 1, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
+    case 2: run_diag<3, 2, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
+    case 3: run_diag<3, 3, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
+    default: run_diag<3, 4, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
+  }
 }
 
 void tensor_launch_traces(int D, int P, int eq, const TensorGeom& g, const Line1D& L, TensorTma* tma,

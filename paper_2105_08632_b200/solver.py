@@ -73,6 +73,12 @@ class Solver:
                        torch.cuda.current_stream(self.device).cuda_stream)
         return U
 
+    def diagnostics(self, U):
+        """TGV ensemble averages (<E*>, eps2, eps3), PAPER.md l.2052-2080 (3-D NS)."""
+        out = torch.empty(3, dtype=torch.float64, device=self.device)
+        sdrt.diagnostics(self.ctx, U.data_ptr(), out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
+        return out.cpu().numpy()
+
     def set_timing(self, enable):
         sdrt.ctx_set_timing(self.ctx, enable)
 

@@ -158,3 +158,17 @@ def test_rk54_parity(name, N, steps):
     S.rk54_step(Ud, cfg.dt, steps, check_every=steps)
     got = S.to_host(Ud)
     assert _rel(got, ref) <= TOL, _rel(got, ref)
+
+
+@pytest.mark.parametrize("name,N", [("c4", 4), ("c5", 3)])
+@pytest.mark.parametrize("state", ["ic", "random"])
+def test_tgv_diagnostics_parity(name, N, state):
+    """sdrt_diagnostics (NEXT row N4) against the oracle's tgv_diagnostics."""
+    from oracle.diagnostics import tgv_diagnostics
+    cfg = CONFIGS[name]
+    m, R, S = _pair(cfg, N)
+    U = initial_state(cfg, m.sol_coords()) if state == "ic" else random_state(cfg, R.ops.nsol, m.K, seed=3, amp=0.2)
+    ref = np.array(tgv_diagnostics(R, U))
+    got = S.diagnostics(S.to_device(U))
+    scale = np.array([abs(ref[0]), abs(ref[1]), max(abs(ref[1]), abs(ref[2]))])
+    assert (np.abs(got - ref) <= 1e-11 * scale).all(), (got, ref)
