@@ -24,13 +24,14 @@ from .physics import Physics
 from .residual import Residual
 
 
-def pattern_blocks(etype, p, ph, layers=1):
-    """Responses Resp_b (dict offset -> (n, n) matrix, n = N_p * N_sol) with h = 1."""
+def pattern_blocks(etype, p, ph, layers=1, residual=Residual):
+    """Responses Resp_b (dict offset -> (n, n) matrix, n = N_p * N_sol) with h = 1;
+    residual: the residual class (SDRT, or fr.FRResidual partial for FR schemes)."""
     D = 2 if etype in ("quad", "tri") else 3
     N = 2 * layers + 3
     m = build_mesh(etype, p, N, [0.0] * D, [float(N)] * D)
     o = build_operators(etype, p)
-    R = Residual(m, ph)
+    R = residual(m, ph)
     nsub, nsol = m.nsub, o.nsol
     root = sum((N // 2) * N ** d for d in range(D))
     nprobe = nsub * nsol

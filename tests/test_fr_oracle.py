@@ -1,0 +1,83 @@
+"""Pins of the oracle FR-SDRT / FR-DG residuals (NEXT row N1; no GPU).
+
+* FR-SDRT == SDRT for linear flux on constant-metric elements (§2.3,
+  Eq. divergence_equivalence l.414-419 and the gradient remark l.429-434; the paper's
+  runs agree to 6.11e-16, Tables l.1855, l.1866), on every element type.
+* FR-DG on quadrilaterals reproduces the paper's FR-DG tau_MAX tables (advection
+  l.1236-1243, diffusion l.1576-1585) with the oracle's Von Neumann harness.
+* freestream and discrete conservation for both schemes (l.170-172, l.312-318).
+"""
+import functools
+
+import numpy as np
+import pytest
+
+from oracle import vonneumann as VN
+from oracle.fr import FRResidual
+from oracle.mesh import build_mesh
+from oracle.operators import build_operators
+from oracle.physics import Physics
+from oracle.residual import Residual
+from sdrt_inputs import CONFIGS, random_state
+
+import json
+import os
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_tables.json")))
+ND = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}
+
+
+@pytest.mark.parametrize("etype,p,N", [("quad", 3, 4), ("tri", 3, 3), ("hex", 2, 2), ("tet", 2, 2), ("tet", 3, 2)])
+def test_frsdrt_equals_sdrt_linear(etype, p, N):
+    D = ND[etype]
+    m = build_mesh(etype, p, N, [0.0] * D, [1.0] * D)
+    ph = Physics("linadvdiff", D, c=tuple([1.0, 0.6, 0.3][:D]), mu=0.05)
+    U = np.random.default_rng(1).uniform(-1, 1, (build_operators(etype, p).nsol, 1, m.K))
+    a, b = Residual(m, ph)(U), FRResidual(m, ph, "frsdrt")(U)
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+
+
+def test_frsdrt_differs_from_sdrt_nonlinear():
+    """Non-linear flux: the schemes differ (aliasing, l.386-389) - the equivalence above is
+    not a tautology of the implementation."""
+    cfg = CONFIGS["c2"]
+    m = build_mesh("tri", 3, 3, cfg.lo, cfg.hi)
+    ph = Physics("euler", 2, **cfg.physics_kwargs())
+    U = random_state(cfg, build_operators("tri", 3).nsol, m.K, seed=5, amp=0.3)
+    a, b = Residual(m, ph)(U), FRResidual(m, ph, "frsdrt")(U)
+    assert np.abs(a - b).max() > 1e-8 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_frdg_quad_tau_max_tables(p):
+    res = functools.partial(FRResidual, scheme="frdg")
+    B = VN.pattern_blocks("quad", p, VN.diffusion_physics(2), layers=2, residual=res)
+    lam = VN.spectrum(B, [np.array([k, 0.0]) for k in np.linspace(0, 2 * np.pi, 361)])
+    assert lam.real.max() < 1e-10
+    ref = GOLD["tau_max_frdg_quad"]["diffusion"][str(p)]
+    for stages, r in zip((3, 4, "rk54"), ref):
+        assert abs(VN.tau_max(lam, stages) - r) <= 1.5e-4, (stages, VN.tau_max(lam, stages), r)
+    ph = VN.advection_physics(2)
+    d = np.array(ph.c)
+    B = VN.pattern_blocks("quad", p, ph, layers=1, residual=res)
+    lam = VN.spectrum(B, [k * d for k in np.linspace(0, np.pi / np.abs(d).max(), 401)])
+    assert abs(VN.tau_max(lam, 4) - GOLD["tau_max_frdg_quad"]["advection"][str(p)][1]) <= 2.5e-3
+
+
+@pytest.mark.parametrize("scheme,etype,p", [("frsdrt", "tri", 3), ("frsdrt", "tet", 2), ("frsdrt", "hex", 2),
+                                            ("frdg", "quad", 3), ("frdg", "hex", 2)])
+def test_fr_freestream_and_conservation(scheme, etype, p):
+    D = ND[etype]
+    cfg = CONFIGS["c4" if D == 3 else "c2"]
+    eq = "ns" if D == 3 else "euler"
+    m = build_mesh(etype, p, 3, cfg.lo, cfg.hi)
+    ph = Physics(eq, D, **cfg.physics_kwargs())
+    R = FRResidual(m, ph, scheme)
+    o = build_operators(etype, p)
+    U = random_state(cfg, o.nsol, m.K, seed=2, amp=0.2)
+    const = np.broadcast_to(U.mean(axis=(0, 2))[None, :, None], U.shape).copy()
+    assert np.abs(R(const)).max() <= 1e-10 * np.abs(const).max()
+    r = R(U)
+    tot = np.einsum("r,rvk,k->v", o.w, r, m.detJ)
+    mag = np.einsum("r,rvk,k->v", o.w, np.abs(r), m.detJ)
+    assert (np.abs(tot) <= 1e-12 * mag).all(), (tot, mag)
