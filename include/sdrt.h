@@ -47,7 +47,10 @@ typedef enum {
 
 /* element types (App. A); N_p = 1, 2, 1, 6 sub-cells per pattern (l.499) */
 typedef enum { SDRT_QUAD = 0, SDRT_TRI = 1, SDRT_HEX = 2, SDRT_TET = 3 } sdrt_etype;
-typedef enum { SDRT_SCHEME_SDRT = 0 } sdrt_scheme;
+/* schemes: SDRT (the path); FR-SDRT and FR-DG flux reconstruction on the same data
+ * (NEXT row N1): no internal flux points, solution-point fluxes
+ * with the SDRT (FR-SDRT) or DG/Radau (FR-DG, tensor elements) corrections */
+typedef enum { SDRT_SCHEME_SDRT = 0, SDRT_SCHEME_FRSDRT = 1, SDRT_SCHEME_FRDG = 2 } sdrt_scheme;
 /* equations: linear advection, linear advection-diffusion (l.1658), Euler
  * (l.1909-1935), compressible Navier-Stokes (l.2012-2030) */
 typedef enum { SDRT_EQ_LINADV = 0, SDRT_EQ_LINADVDIFF = 1, SDRT_EQ_EULER = 2, SDRT_EQ_NS = 3 } sdrt_eq;

@@ -231,8 +231,8 @@ sdrt_status sdrt_operators_build(int etype, int p, int scheme, sdrt_operators** 
     sdrt::set_error("null argument");
     return SDRT_E_INVALID_ARG;
   }
-  if (scheme != SDRT_SCHEME_SDRT) {
-    sdrt::set_error("unsupported scheme (only SDRT)");
+  if (scheme < SDRT_SCHEME_SDRT || scheme > SDRT_SCHEME_FRDG) {
+    sdrt::set_error("unsupported scheme");
     return SDRT_E_UNSUPPORTED;
   }
   if (etype < 0 || etype > 3) {
@@ -242,7 +242,7 @@ sdrt_status sdrt_operators_build(int etype, int p, int scheme, sdrt_operators** 
   SDRT_TRY({
     auto* o = new sdrt_operators;
     try {
-      o->o = sdrt::build_operators(etype, p);
+      o->o = sdrt::build_operators(etype, p, scheme);
     } catch (...) {
       delete o;
       throw;

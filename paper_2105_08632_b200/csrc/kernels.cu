@@ -726,13 +726,31 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       Line1D& L = c->line;
       std::memset(&L, 0, sizeof(L));
       int n = m.p + 1;
-      for (int i = 0; i < n; ++i) {
-        L.Iend[0][i] = O.M0(0 * r.nfp + 0, i);
-        L.Iend[1][i] = O.M0(1 * r.nfp + 0, i);
-        for (int a = 0; a < m.p; ++a) L.Iint[a][i] = O.M12(a, i);
-        L.Dfl[i][0] = -O.M14(i, 0 * r.nfp + 0);
-        L.Dfl[i][m.p + 1] = O.M14(i, 1 * r.nfp + 0);
-        for (int a = 0; a < m.p; ++a) L.Dfl[i][a + 1] = O.M13(i, a);
+      if (O.scheme == 0) {
+        for (int i = 0; i < n; ++i) {
+          L.Iend[0][i] = O.M0(0 * r.nfp + 0, i);
+          L.Iend[1][i] = O.M0(1 * r.nfp + 0, i);
+          for (int a = 0; a < m.p; ++a) L.Iint[a][i] = O.M12(a, i);
+          L.Dfl[i][0] = -O.M14(i, 0 * r.nfp + 0);
+          L.Dfl[i][m.p + 1] = O.M14(i, 1 * r.nfp + 0);
+          for (int a = 0; a < m.p; ++a) L.Dfl[i][a + 1] = O.M13(i, a);
+        }
+      } else {
+        // FR on the first x-line: the "internal points" are the n solution points
+        // (Iint = I); end coefficients -div g of the x = -1 face and div g of x = +1
+        // (signs as the SDRT M14 columns); interior coefficients Dsol - end x Iend
+        L.fr = 1;
+        for (int i = 0; i < n; ++i) {
+          L.Iend[0][i] = O.M0(0 * r.nfp + 0, i);
+          L.Iend[1][i] = O.M0(1 * r.nfp + 0, i);
+          L.Iint[i][i] = 1.0;
+        }
+        for (int i = 0; i < n; ++i) {
+          const double e0 = -O.Mc(i, 0 * r.nfp + 0), e1 = O.Mc(i, 1 * r.nfp + 0);
+          L.Dfl[i][0] = e0;
+          L.Dfl[i][n + 1] = e1;
+          for (int j = 0; j < n; ++j) L.Dfl[i][j + 1] = O.Dsol[0](i, j) - e0 * L.Iend[0][j] - e1 * L.Iend[1][j];
+        }
       }
       tensor_tma_init(&c->tma, m.nd, m.p, ph->eq, m.K_pad);
       c->Tu[0] = (double*)(base + p.off_tu0);
@@ -740,6 +758,11 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tg = (double*)(base + p.off_tg);
     }
     c->sfused = !etype_tensor(m.etype) && !(fg && fg[0] == '1') && simplex_supported(m.nd, m.p, ph->eq);
+    if (O.scheme != 0 && !c->fused) {
+      delete c;
+      set_error("unsupported: FR schemes run on the fused tensor-element kernels");
+      return SDRT_E_UNSUPPORTED;
+    }
     if (m.slabs.size() > 0 && !c->fused && !c->sfused) {
       delete c;
       set_error("unsupported: halo exchange is implemented for the fused paths only");

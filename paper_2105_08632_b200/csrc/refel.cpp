@@ -595,6 +595,37 @@ static Operators tensor_operators(int etype, int p) {
   }
   O.cond_flux = 0.0;
   finish_gradient_ops(O);
+  // FR data: solution-basis derivatives along each axis (1D Lagrange on the GL nodes)
+  // and the FR-DG correction divergence (Radau polynomials of degree p+1 along the
+  // face normal: g_L = (-1)^{p+1}/2 (P_{p+1} - P_p), g_R(x) = g_L(-x))
+  O.Dsol.assign(D, Mat(ns, ns));
+  for (int d = 0; d < D; ++d)
+    for (int s = 0; s < ns; ++s)
+      for (int q = 0; q < ns; ++q) {
+        bool tang = true;
+        for (int c = 0; c < D; ++c)
+          if (c != d && sidx(s, c) != sidx(q, c)) tang = false;
+        if (tang) O.Dsol[d](s, q) = (double)lag_d(g, sidx(q, d), g[sidx(s, d)]);
+      }
+  auto legd = [](int n, qd x) {  // P_n'(x) for |x| < 1
+    qd pn, pm;
+    legendre_pair(n, x, pn, pm);
+    return n == 0 ? (qd)0 : (qd)n * (x * pn - pm) / (x * x - 1);
+  };
+  const qd sg = (p + 1) % 2 ? -1 : 1;  // (-1)^{p+1}
+  O.Mc = Mat(ns, r.next);
+  for (int e = 0; e < r.next; ++e) {
+    int f = r.ext_face[e], d = f / 2, side = f % 2;
+    for (int s = 0; s < ns; ++s) {
+      bool tang = true;
+      for (int c = 0; c < D; ++c)
+        if (c != d && qabs(R.xext[e][c] - g[sidx(s, c)]) > 1e-25Q) tang = false;
+      if (!tang) continue;
+      const qd xi = g[sidx(s, d)];
+      if (side == 0) O.Mc(s, e) = (double)(-(sg / 2) * (legd(p + 1, xi) - legd(p, xi)));     // div(-e_d g_L)
+      else O.Mc(s, e) = (double)(-(sg / 2) * (legd(p + 1, -xi) - legd(p, -xi)));            // div(+e_d g_R)
+    }
+  }
   return O;
 }
 
@@ -724,6 +755,15 @@ static Operators simplex_operators(int etype, int p) {
   };
   interp(R.xext, O.M0);
   interp(R.xu, O.M12);
+  // FR data: solution-basis derivatives (FR-DG correction not built for simplices)
+  O.Dsol.assign(D, Mat(ns, ns));
+  for (int d = 0; d < D; ++d)
+    for (int s = 0; s < ns; ++s)
+      for (int rr = 0; rr < ns; ++rr) {
+        qd v = 0;
+        for (int k = 0; k < ns; ++k) v += Y[(size_t)k * ns + rr] * mono_dx(Ptot[k], R.xsol[s], d);
+        O.Dsol[d](s, rr) = (double)v;
+      }
   // weights: int over reference simplex of xi^e = 2^D prod e_i! / (|e|+D)!
   O.w.assign(ns, 0.0);
   for (int rr = 0; rr < ns; ++rr) {
@@ -746,10 +786,16 @@ static Operators simplex_operators(int etype, int p) {
   return O;
 }
 
-Operators build_operators(int etype, int p) {
-  if (etype_tensor(etype)) return tensor_operators(etype, p);
-  if (etype == TRI || etype == TET) return simplex_operators(etype, p);
-  throw std::runtime_error("unknown element type");
+Operators build_operators(int etype, int p, int scheme) {
+  Operators O;
+  if (etype_tensor(etype)) O = tensor_operators(etype, p);
+  else if (etype == TRI || etype == TET) O = simplex_operators(etype, p);
+  else throw std::runtime_error("unknown element type");
+  if (scheme < 0 || scheme > 2) throw std::runtime_error("unsupported scheme");
+  if (scheme == 2 && !etype_tensor(etype)) throw std::runtime_error("unsupported: FR-DG is built for tensor elements only");
+  O.scheme = scheme;
+  if (scheme == 1) O.Mc = O.M14;  // FR-SDRT: div g_nu = div psi_nu (l.407-413)
+  return O;
 }
 
 }  // namespace sdrt

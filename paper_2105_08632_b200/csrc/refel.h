@@ -39,11 +39,16 @@ struct Operators {
   Mat M0, M12, M13, M14, M15, M16, P, M19P2;
   std::vector<double> w;  // int of the solution nodal basis over the reference element
   double cond_flux = 0.0;
+  // flux reconstruction (NEXT row N1): scheme 0 SDRT, 1 FR-SDRT,
+  // 2 FR-DG; Dsol[d](s, r) = d l_r / d x~_d (x~_s); Mc(s, nu) = div g_nu (x~_s)
+  int scheme = 0;
+  std::vector<Mat> Dsol;
+  Mat Mc;
 };
 
 // Build; throws std::runtime_error with a message on failure.
 RefElement build_reference(int etype, int p);
-Operators build_operators(int etype, int p);
+Operators build_operators(int etype, int p, int scheme = 0);
 
 // Reference vertices of the simplices (x~ of vertex k), used by mesh code.
 void simplex_ref_vertices(int etype, std::vector<std::array<double, 3>>& V);

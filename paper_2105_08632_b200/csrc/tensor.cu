@@ -170,7 +170,7 @@ __device__ __forceinline__ void prefetch_rows(const double* __restrict__ A, int6
 // mapped: thread tid owns items tid + k THREADS.  The neighbour traces of all its items
 // are loaded into registers first (GradNb::load, issued before the tile wait), so their
 // latency overlaps the tile load.
-template <int D, int P, int EQ, int E, int THREADS>
+template <int D, int P, int EQ, int E, int THREADS, int NI = P>
 struct GradNb {
   using T = TDims<D, P>;
   static constexpr int NV = Phys<EQ, D>::NV;
@@ -214,9 +214,9 @@ struct GradNb {
       const double own0 = interp_end<n>(L.Iend[0], u), own1 = interp_end<n>(L.Iend[1], u);
       const double c0 = wl * nb[k][0] + wr * own0;  // face x_d = -1: this element is RIGHT
       const double c1 = wl * own1 + wr * nb[k][1];  // face x_d = +1: this element is LEFT
-      double ui[P];
+      double ui[NI];
 #pragma unroll
-      for (int a = 0; a < P; ++a) {
+      for (int a = 0; a < NI; ++a) {
         double s = 0.0;
 #pragma unroll
         for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i], s);
@@ -227,8 +227,8 @@ struct GradNb {
       for (int i = 0; i < n; ++i) {
         double q = L.Dfl[i][0] * c0;
 #pragma unroll
-        for (int a = 0; a < P; ++a) q = fma(L.Dfl[i][a + 1], ui[a], q);
-        q = fma(L.Dfl[i][P + 1], c1, q);
+        for (int a = 0; a < NI; ++a) q = fma(L.Dfl[i][a + 1], ui[a], q);
+        q = fma(L.Dfl[i][NI + 1], c1, q);
         sQ[((d * NS + (lb + i * ls)) * NV + v) * E + el] = jd * q;
       }
     }
@@ -312,7 +312,7 @@ __device__ __forceinline__ void publish_g(const TensorGeom& g, const Line1D& L, 
 
 // internal transformed flux F~ = detJ (J^-1 (f^c - f^v))_d at internal point a of d-line t
 // (one normal component, B7; l.305-311) -> sF[t][a][v][el]
-template <int D, int P, int EQ, int E, int d>
+template <int D, int P, int EQ, int E, int d, int NI>
 __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
                                               const double* sU, const double* sQ, double* sF, int t, int a, int el) {
   using Ph = Phys<EQ, D>;
@@ -341,7 +341,7 @@ __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D&
   Ph::conv_dir(ph, ua, w, fc);
   Ph::visc_dir(ph, ua, qa, w, fv);
 #pragma unroll
-  for (int v = 0; v < NV; ++v) sF[((t * P + a) * NV + v) * E + el] = fc[v] + fv[v];
+  for (int v = 0; v < NV; ++v) sF[((t * NI + a) * NV + v) * E + el] = fc[v] + fv[v];
 }
 
 // Kernel A (viscous equations) = the element-local "volume" work: gradient, published
@@ -351,14 +351,14 @@ __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D&
 // Phases after the gradient: [publish g + F_v(d=0)] [div(0) + F_v(1)] [div(1) + F_v(2)]
 // [div(2)], with the internal-flux buffer double-buffered so each phase has work for
 // every thread.
-template <int D, int P, int EQ, int E, int NT, int MINB>
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
 __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
                                                     const __grid_constant__ TileMaps tm) {
   PH_INIT
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, NL = T::NL, NS = T::NS;
-  constexpr int NFB = NL * P * NV * E;  // one internal-flux buffer
+  constexpr int NFB = NL * NI * NV * E;  // one internal-flux buffer
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;
   double* sQ = smem + NS * NV * E;
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   __syncthreads();
   PH(0, 0)
   {
-    GradNb<D, P, EQ, E, NT> gn;
+    GradNb<D, P, EQ, E, NT, NI> gn;
     gn.load(g, b.Tu, sNb, e0);
     mbar_wait(&bar, 0);
     __syncthreads();
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   const bool pub1 = (0.5 + ph.beta) != 0.0, pub0 = (0.5 - ph.beta) != 0.0;
   const int nsides = (pub0 ? 1 : 0) + (pub1 ? 1 : 0);
   const int npub = D * nsides * NL * E;
-  constexpr int NFI = NL * P * E;   // internal-flux items per direction
+  constexpr int NFI = NL * NI * E;   // internal-flux items per direction
   constexpr int NDI = NL * NV * E;  // divergence items per direction
 #pragma unroll 1
   for (int ph_ = 0; ph_ <= D; ++ph_) {
@@ -424,11 +424,11 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         else if (d == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
         else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
       } else {
-        const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % P, t = r / P;
+        const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % NI, t = r / NI;
         double* f1 = sF + (ph_ & 1) * NFB;
-        if (ph_ == 0) visc_internal<D, P, EQ, E, 0>(g, L, ph, sU, sQ, f1, t, a, el);
-        else if (ph_ == 1) visc_internal<D, P, EQ, E, 1>(g, L, ph, sU, sQ, f1, t, a, el);
-        else if constexpr (D == 3) visc_internal<D, P, EQ, E, 2>(g, L, ph, sU, sQ, f1, t, a, el);
+        if (ph_ == 0) visc_internal<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if (ph_ == 1) visc_internal<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if constexpr (D == 3) visc_internal<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, t, a, el);
       }
     }
     if (ph_ >= 1) {
@@ -439,15 +439,15 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         const int el = item % E, r = item / E, v = r % NV, t = r / NV;
         if (item >= NDI || e0 + el >= g.K) continue;
         const int lb = lbase<D, P>(dd, t), ls = lstr<D, P>(dd);
-        double f[P];
+        double f[NI];
 #pragma unroll
-        for (int a = 0; a < P; ++a) f[a] = f0[((t * P + a) * NV + v) * E + el];
+        for (int a = 0; a < NI; ++a) f[a] = f0[((t * NI + a) * NV + v) * E + el];
         double* dst = b.Rv + (int64_t)(lb * NV + v) * g.Kp + e0 + el;
 #pragma unroll
         for (int i = 0; i <= P; ++i) {
           double acc = ph_ >= 2 ? prev[k][i] : 0.0;
 #pragma unroll
-          for (int a = 0; a < P; ++a) acc = fma(L.Dfl[i][a + 1], f[a], acc);
+          for (int a = 0; a < NI; ++a) acc = fma(L.Dfl[i][a + 1], f[a], acc);
           dst[(int64_t)i * ls * NV * g.Kp] = acc;
         }
       }
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
 // traces + LDG jump, l.312-340), the face part of the divergence M14 D~ (l.2919-2925),
 // [inviscid equations: also the internal fluxes and M13 F~, which kernel A does
 // otherwise], R~ = sum + R_int, -R~/detJ, RK4 update, new traces.
-template <int D, int P, int EQ, int E, int NT, int MINB>
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
 __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
                                                    double dt, const __grid_constant__ TileMaps tm) {
   PH_INIT
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
   constexpr bool INT = !Ph::VISC;     // internal fluxes evaluated here (inviscid only)
-  constexpr int NF = INT ? P + 2 : 2;  // flux-line slots per line held in sF
+  constexpr int NF = INT ? NI + 2 : 2;  // flux-line slots per line held in sF
   extern __shared__ __align__(128) double smem[];
   // regions allocated per stage (the launcher sizes dynamic smem the same way):
   // sU, sR, sF always; u_n for stages 1, 2; ACC for stages 1..3
@@ -539,8 +539,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
     double nL[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
-    for (int item = threadIdx.x; item < (INT ? NL * P * E : 0); item += blockDim.x) {
-      const int el = item % E, r = item / E, a = r % P, t = r / P;
+    for (int item = threadIdx.x; item < (INT ? NL * NI * E : 0); item += blockDim.x) {
+      const int el = item % E, r = item / E, a = r % NI, t = r / NI;
       const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
       double ua[NV];
 #pragma unroll
@@ -609,7 +609,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
           for (int k = 0; k < NF; ++k) acc = fma(L.Dfl[i][k], f[k], acc);
         } else {
           acc = fma(L.Dfl[i][0], f[0], acc);
-          acc = fma(L.Dfl[i][P + 1], f[1], acc);
+          acc = fma(L.Dfl[i][NI + 1], f[1], acc);
         }
         *dst = acc;
       }
@@ -719,7 +719,7 @@ __device__ __forceinline__ void block_sum3(double (&a)[3], double* red, double* 
     for (int k = 0; k < 3; ++k) out[k] = red[k * NT];
 }
 
-template <int D, int P, int EQ, int E, int NT>
+template <int D, int P, int EQ, int E, int NT, int NI>
 __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, const double* w,
                                               double* part, const __grid_constant__ TileMaps tm) {
   using Ph = Phys<EQ, D>;
@@ -741,7 +741,7 @@ __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph
   fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();
   {
-    GradNb<D, P, EQ, E, NT> gn;
+    GradNb<D, P, EQ, E, NT, NI> gn;
     gn.load(g, b.Tu, sNb, e0);
     mbar_wait(&bar, 0);
     __syncthreads();
@@ -815,12 +815,18 @@ struct TCfg {
   static constexpr int THREADS = 256;
   static constexpr size_t TILE = (size_t)NS * NV * E * sizeof(double);
   static constexpr size_t TILEA = (size_t)NS * NV * EA * sizeof(double);
-  static constexpr size_t SMEM_A = TILEA * (1 + D) + 2 * (size_t)NL * P * NV * EA * sizeof(double);
+  // kernel A: tile, gradient, two internal-flux buffers of NI points per line (NI = p
+  // for SDRT, p+1 solution points for FR)
+  static constexpr size_t smem_a(int ni) {
+    return TILEA * (1 + D) + 2 * (size_t)NL * ni * NV * EA * sizeof(double);
+  }
   // kernel B: sU, sR, flux-line slots, + the RK registers the stage reads (ACC: stages
   // 1..3, u_n: stages 1, 2)
-  static constexpr size_t SMEM_B0 = TILE * 2 + (size_t)NL * (VISC ? 2 : P + 2) * NV * E * sizeof(double);
-  static size_t smem_b(int stage) {
-    return SMEM_B0 + (stage_reads_acc(stage) ? TILE : 0) + (stage_reads_un(stage) ? TILE : 0);
+  static constexpr size_t smem_b0(int ni) {
+    return TILE * 2 + (size_t)NL * (VISC ? 2 : ni + 2) * NV * E * sizeof(double);
+  }
+  static size_t smem_b(int stage, int ni) {
+    return smem_b0(ni) + (stage_reads_acc(stage) ? TILE : 0) + (stage_reads_un(stage) ? TILE : 0);
   }
   static constexpr size_t SMEM_T = TILE;
 };
@@ -847,25 +853,33 @@ static TileMaps maps_for(TensorTma* t, const TensorBufs& b, bool full) {
   return m;
 }
 
-template <int D, int P, int EQ>
-static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
-                      int stage, double dt, cudaStream_t st, int which) {
+template <int D, int P, int EQ, int NI>
+static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
+                         const TensorBufs& b, int stage, double dt, cudaStream_t st, int which) {
   using C = TCfg<D, P, EQ>;
   if (which == 0) {
     if constexpr (Phys<EQ, D>::VISC) {
       const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::EA - 1) / C::EA);
       if (grid == 0) return;
-      auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A>;
-      set_smem<D, P, EQ>((const void*)ka, C::SMEM_A);
-      ka<<<grid, C::NTA, C::SMEM_A, st>>>(g, L, ph, b, maps_for(tma, b, false));
+      auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A, NI>;
+      set_smem<D, P, EQ>((const void*)ka, C::smem_a(NI));
+      ka<<<grid, C::NTA, C::smem_a(NI), st>>>(g, L, ph, b, maps_for(tma, b, false));
     }
   } else {
     const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::E - 1) / C::E);
     if (grid == 0) return;
-    auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B>;
-    set_smem<D, P, EQ>((const void*)kb, C::smem_b(2));
-    kb<<<grid, C::NTB, C::smem_b(stage), st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
+    auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI>;
+    set_smem<D, P, EQ>((const void*)kb, C::smem_b(2, NI));
+    kb<<<grid, C::NTB, C::smem_b(stage, NI), st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
   }
+}
+
+// SDRT: P internal flux points per line; FR (L.fr): the P+1 solution points
+template <int D, int P, int EQ>
+static void run_stage(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
+                      int stage, double dt, cudaStream_t st, int which) {
+  if (L.fr) run_stage_ni<D, P, EQ, P + 1>(g, L, ph, tma, b, stage, dt, st, which);
+  else run_stage_ni<D, P, EQ, P>(g, L, ph, tma, b, stage, dt, st, which);
 }
 
 template <int D, int P, int EQ>
@@ -885,7 +899,7 @@ static void run_diag(const TensorGeom& g, const Line1D& L, const PhysDev& ph, Te
                      const double* w, double* part, cudaStream_t st) {
   using C = TCfg<D, P, EQ>;
   const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
-  auto k = kt_diag<D, P, EQ, C::E, 256>;
+  auto k = L.fr ? kt_diag<D, P, EQ, C::E, 256, P + 1> : kt_diag<D, P, EQ, C::E, 256, P>;
   const size_t sm = C::TILE * (1 + D);
   set_smem<D, P, EQ>((const void*)k, sm);
   k<<<grid, 256, sm, st>>>(g, L, ph, b, w, part, maps_for(tma, b, false));

@@ -18,10 +18,16 @@ constexpr int TMAXP = 4;  // max degree of the fused tensor path
 //   Dfl[i][f]  = L_f'(g_i), f over the flux line {-1, zeta_1..zeta_p, +1}
 //                (M13 columns are Dfl[.][1..p]; M14 = -Dfl[.][0] (x=-1), +Dfl[.][p+1] (x=+1);
 //                 M16 = n . M14 = Dfl[.][0] / Dfl[.][p+1] for both ends)
+//   FR schemes (Line1D::fr = 1): the "internal points" are the p+1
+//   solution points (Iint = I), Dfl[.][1..p+1] = Dsol - Dfl[.][0] Iend[0] - Dfl[.][p+2]
+//   Iend[1] (discontinuous-flux derivative minus its end values times the correction
+//   derivatives), Dfl[.][0] / Dfl[.][p+2] = the correction derivatives -g_L', g_R'
+//   (FR-SDRT: the SDRT end values; FR-DG: Radau).
 struct Line1D {
   double Iend[2][TMAXP + 1];
-  double Iint[TMAXP][TMAXP + 1];
-  double Dfl[TMAXP + 1][TMAXP + 2];
+  double Iint[TMAXP + 1][TMAXP + 1];
+  double Dfl[TMAXP + 1][TMAXP + 3];
+  int fr;  // 0: SDRT (p internal flux points), 1: FR (p+1 solution points)
 };
 
 struct TensorGeom {

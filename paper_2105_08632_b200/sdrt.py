@@ -191,7 +191,11 @@ def mesh_destroy(m):
 
 
 # ------------------------------------------------------------------ operators
+SCHEMES = {"sdrt": 0, "frsdrt": 1, "frdg": 2}
+
+
 def operators_build(etype, p, scheme=0):
+    scheme = SCHEMES[scheme] if isinstance(scheme, str) else int(scheme)
     et = ETYPES[etype] if isinstance(etype, str) else int(etype)
     out = _vp()
     _check(lib.sdrt_operators_build(et, p, scheme, ctypes.byref(out)))

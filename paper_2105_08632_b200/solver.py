@@ -13,7 +13,7 @@ from . import sdrt
 
 class Solver:
     def __init__(self, etype, p, N, lo, hi, eq, device="cuda", rank=0, nranks=1, pgrid=None, _pre_ctx=None,
-                 force_self_halo=False, **phys):
+                 force_self_halo=False, scheme="sdrt", **phys):
         D = 2 if etype in ("quad", "tri") else 3
         Nl = list(N) if np.ndim(N) else [int(N)] * D
         self.mesh = sdrt.mesh_create(etype, p, Nl, lo, hi, rank=rank, nranks=nranks, pgrid=pgrid)
@@ -21,7 +21,7 @@ class Solver:
             _pre_ctx(self.mesh)
         elif force_self_halo:
             sdrt.mesh_set_halo(self.mesh, True)   # loopback halo: the library exchanges itself
-        self.ops = sdrt.operators_build(etype, p)
+        self.ops = sdrt.operators_build(etype, p, scheme)
         self.info = sdrt.mesh_info(self.mesh)
         self.phys = sdrt.physics(eq, **phys)
         self.nv = 1 if eq in ("linadv", "linadvdiff") else D + 2

@@ -172,3 +172,31 @@ def test_tgv_diagnostics_parity(name, N, state):
     got = S.diagnostics(S.to_device(U))
     scale = np.array([abs(ref[0]), abs(ref[1]), max(abs(ref[1]), abs(ref[2]))])
     assert (np.abs(got - ref) <= 1e-11 * scale).all(), (got, ref)
+
+
+@pytest.mark.parametrize("scheme", ["frsdrt", "frdg"])
+@pytest.mark.parametrize("name,N,steps", [("c1", 5, 20), ("c3", 3, 3), ("c4", (3, 4, 3), 3), ("c4", 4, 2)])
+def test_fr_parity(scheme, name, N, steps):
+    """FR-SDRT / FR-DG (NEXT row N1) on the fused tensor kernels against the oracle's
+    FRResidual (pinned to the paper's FR-DG tau_MAX tables and the FR-SDRT == SDRT
+    equivalence): residual on a random state and RK4 steps of the configuration."""
+    from oracle.fr import FRResidual
+    from oracle.mesh import build_mesh
+    from oracle.physics import Physics
+    from oracle.residual import integrate
+    from paper_2105_08632_b200.solver import Solver
+    cfg = CONFIGS[name]
+    D = cfg.nd
+    Nt = tuple(N) if isinstance(N, (tuple, list)) else (N,) * D
+    m = build_mesh(cfg.etype, cfg.p, Nt, cfg.lo, cfg.hi)
+    R = FRResidual(m, Physics(cfg.eq, D, **cfg.physics_kwargs()), scheme)
+    S = Solver(cfg.etype, cfg.p, list(Nt), cfg.lo, cfg.hi, cfg.eq, device="cuda", scheme=scheme,
+               **cfg.physics_kwargs())
+    U = random_state(cfg, R.ops.nsol, m.K, seed=11, amp=0.3)
+    got = S.to_host(S.residual(S.to_device(U)))
+    assert _rel(got, R(U)) <= TOL, _rel(got, R(U))
+    U0 = initial_state(cfg, m.sol_coords())
+    ref = integrate(R, U0, cfg.dt, steps)
+    Ud = S.to_device(U0)
+    S.rk_step(Ud, cfg.dt, steps)
+    assert _rel(S.to_host(Ud), ref) <= TOL, _rel(S.to_host(Ud), ref)

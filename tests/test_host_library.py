@@ -90,3 +90,16 @@ def test_errors_are_reported(sdrt):
     with pytest.raises(sdrt.SdrtError) as e:
         sdrt.operators_build("quad", 0)
     assert e.value.code == -2
+
+
+def test_fr_schemes_build(sdrt):
+    """FR-SDRT builds for every element type, FR-DG for tensor elements only."""
+    for et in ("quad", "tri", "hex", "tet"):
+        o = sdrt.operators_build(et, 2, "frsdrt")
+        sdrt.operators_destroy(o)
+    for et in ("quad", "hex"):
+        o = sdrt.operators_build(et, 3, "frdg")
+        sdrt.operators_destroy(o)
+    with pytest.raises(sdrt.SdrtError) as e:
+        sdrt.operators_build("tet", 2, "frdg")
+    assert e.value.code == -2
