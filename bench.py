@@ -272,6 +272,9 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="sdrt", choices=["sdrt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scheme", default="sdrt", choices=["sdrt", "frsdrt", "frdg"],
+                    help="sdrt: the path; frsdrt/frdg: flux reconstruction on the same kernels (tensor "
+                         "elements; the paper's SDRT-vs-FR-DG cost comparison, Table perfo_tgv)")
     ap.add_argument("--integrator", default="rk4", choices=["rk4", "rk54"],
                     help="rk4: classical (BASELINE.json configs); rk54: the paper's PM protocol (N_RK = 5)")
     args = ap.parse_args()
@@ -300,10 +303,12 @@ def main():
         pgrid = default_pgrid(world, cfg.nd)
         Ng = [cfg.N * g for g in pgrid]
         hi = [l + (h - l) * g for l, h, g in zip(cfg.lo, cfg.hi, pgrid)]
-        S = DistSolver(cfg.etype, cfg.p, Ng, cfg.lo, hi, cfg.eq, device=dev, pgrid=pgrid, **cfg.physics_kwargs())
+        S = DistSolver(cfg.etype, cfg.p, Ng, cfg.lo, hi, cfg.eq, device=dev, pgrid=pgrid, scheme=args.scheme,
+                       **cfg.physics_kwargs())
         parallelism = f"element partition {'x'.join(map(str, pgrid))}, NCCL halo"
     else:
-        S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, **cfg.physics_kwargs())
+        S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, scheme=args.scheme,
+                   **cfg.physics_kwargs())
         parallelism = "single"
     U0 = initial_state(cfg, S.sol_coords())
     U = S.to_device(U0)
@@ -377,7 +382,8 @@ def main():
         S2 = None
         solvers, bufs = [S, S], [U, U]
     else:
-        S2 = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, **cfg.physics_kwargs())
+        S2 = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, scheme=args.scheme,
+                    **cfg.physics_kwargs())
         solvers, bufs = [S, S2], [U, torch.empty_like(U)]
     side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     torch.cuda.synchronize(dev)
@@ -465,6 +471,7 @@ def main():
                "config": {"workload": WORKLOADS[cfg.name], "elements_per_gpu": K, "dof_per_gpu": dof,
                           "p": cfg.p, "dt": cfg.dt, "parallelism": parallelism,
                           "integrator": "classical RK4 (4 stages)" if NST == 4 else "RK54 (5 stages, 2 registers)",
+                          "scheme": args.scheme,
                           "l2": "working set > L2 (state 3 registers + traces >> 126 MB); no flush needed"
                           if dof * 8 * 3 > 126e6 else "working set fits L2 (small config)"},
                "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,

@@ -217,10 +217,14 @@ struct GradNb {
       double ui[NI];
 #pragma unroll
       for (int a = 0; a < NI; ++a) {
-        double s = 0.0;
+        if constexpr (NI == n) {  // FR: the flux points are the solution points (Iint = I)
+          ui[a] = u[a];
+        } else {
+          double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i], s);
-        ui[a] = s;
+          for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[i], s);
+          ui[a] = s;
+        }
       }
       const double jd = g.jinv[d];
 #pragma unroll
@@ -273,6 +277,11 @@ __global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const _
   write_traces<D, P, NV, E>(g, L, smem, T, e0);
 }
 
+// kernel A keeps two internal-flux buffers when both fit two CTAs per SM
+__host__ __device__ constexpr bool tensor_a_dbuf(int D, int NS, int NL, int NV, int E, int NI) {
+  return (size_t)(NS * NV * E * (1 + D) + 2 * NL * NI * NV * E) * sizeof(double) <= 112 * 1024;
+}
+
 // Kernel A phase helpers -----------------------------------------------------------
 // publish g = n_L . f^v(u, q) at the face point (d, side, t) of element slot el
 template <int D, int P, int EQ, int E, int d>
@@ -320,18 +329,27 @@ __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D&
   constexpr int NV = Ph::NV, n = T::n, NS = T::NS;
   const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
   double ua[NV], qa[D * NV];
+  if constexpr (NI == n) {  // FR: the flux points are the solution points (Iint = I)
 #pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double s = 0.0;
+    for (int v = 0; v < NV; ++v) {
+      ua[v] = sU[((lb + a * ls) * NV + v) * E + el];
 #pragma unroll
-    for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], sU[((lb + i * ls) * NV + v) * E + el], s);
-    ua[v] = s;
+      for (int dd = 0; dd < D; ++dd) qa[dd * NV + v] = sQ[((dd * NS + (lb + a * ls)) * NV + v) * E + el];
+    }
+  } else {
 #pragma unroll
-    for (int dd = 0; dd < D; ++dd) {
-      double s2 = 0.0;
+    for (int v = 0; v < NV; ++v) {
+      double s = 0.0;
 #pragma unroll
-      for (int i = 0; i < n; ++i) s2 = fma(L.Iint[a][i], sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el], s2);
-      qa[dd * NV + v] = s2;
+      for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], sU[((lb + i * ls) * NV + v) * E + el], s);
+      ua[v] = s;
+#pragma unroll
+      for (int dd = 0; dd < D; ++dd) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) s2 = fma(L.Iint[a][i], sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el], s2);
+        qa[dd * NV + v] = s2;
+      }
     }
   }
   double w[D], fc[NV], fv[NV];
@@ -359,6 +377,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, NL = T::NL, NS = T::NS;
   constexpr int NFB = NL * NI * NV * E;  // one internal-flux buffer
+  constexpr bool DBUF = tensor_a_dbuf(D, NS, NL, NV, E, NI);
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;
   double* sQ = smem + NS * NV * E;
@@ -415,24 +434,10 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
     }
     const int nA = ph_ == 0 ? npub : 0;
     const int nB = ph_ < D ? NFI : 0;
-    for (int item = threadIdx.x; item < nA + nB; item += blockDim.x) {
-      if (item < nA) {
-        const int el = item % E, r = item / E;
-        const int t = r % NL, r2 = r / NL, k = r2 % nsides, d = r2 / nsides;
-        const int side = (nsides == 2) ? k : (pub1 ? 1 : 0);
-        if (d == 0) publish_g<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
-        else if (d == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
-        else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
-      } else {
-        const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % NI, t = r / NI;
-        double* f1 = sF + (ph_ & 1) * NFB;
-        if (ph_ == 0) visc_internal<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, t, a, el);
-        else if (ph_ == 1) visc_internal<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, t, a, el);
-        else if constexpr (D == 3) visc_internal<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, t, a, el);
-      }
-    }
-    if (ph_ >= 1) {
-      const double* f0 = sF + (dd & 1) * NFB;
+    // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
+    // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
+    auto divergence = [&]() {
+      const double* f0 = sF + (DBUF ? (dd & 1) * NFB : 0);
 #pragma unroll
       for (int k = 0; k < CD; ++k) {
         const int item = threadIdx.x + k * NT;
@@ -451,6 +456,29 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
           dst[(int64_t)i * ls * NV * g.Kp] = acc;
         }
       }
+    };
+    if constexpr (!DBUF) {
+      if (ph_ >= 1) divergence();
+      __syncthreads();
+    }
+    for (int item = threadIdx.x; item < nA + nB; item += blockDim.x) {
+      if (item < nA) {
+        const int el = item % E, r = item / E;
+        const int t = r % NL, r2 = r / NL, k = r2 % nsides, d = r2 / nsides;
+        const int side = (nsides == 2) ? k : (pub1 ? 1 : 0);
+        if (d == 0) publish_g<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+        else if (d == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+        else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+      } else {
+        const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % NI, t = r / NI;
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        if (ph_ == 0) visc_internal<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if (ph_ == 1) visc_internal<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if constexpr (D == 3) visc_internal<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+      }
+    }
+    if constexpr (DBUF) {
+      if (ph_ >= 1) divergence();
     }
     __syncthreads();
   PH(0, 3 + ph_)
@@ -545,10 +573,14 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
       double ua[NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        double s = 0.0;
+        if constexpr (NI == n) {  // FR: solution points
+          ua[v] = sU[((lb + a * ls) * NV + v) * E + el];
+        } else {
+          double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], sU[((lb + i * ls) * NV + v) * E + el], s);
-        ua[v] = s;
+          for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], sU[((lb + i * ls) * NV + v) * E + el], s);
+          ua[v] = s;
+        }
       }
       double w[D], f[NV];
 #pragma unroll
@@ -818,7 +850,7 @@ struct TCfg {
   // kernel A: tile, gradient, two internal-flux buffers of NI points per line (NI = p
   // for SDRT, p+1 solution points for FR)
   static constexpr size_t smem_a(int ni) {
-    return TILEA * (1 + D) + 2 * (size_t)NL * ni * NV * EA * sizeof(double);
+    return TILEA * (1 + D) + (tensor_a_dbuf(D, NS, NL, NV, EA, ni) ? 2 : 1) * (size_t)NL * ni * NV * EA * sizeof(double);
   }
   // kernel B: sU, sR, flux-line slots, + the RK registers the stage reads (ACC: stages
   // 1..3, u_n: stages 1, 2)
