@@ -473,6 +473,25 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
       double v = O.M13(s2, i);
       if (v != 0.0) M13F(s2, r.int_dir[i] * r.nu + r.int_u[i]) += v;
     }
+  if (O.scheme != 0) {
+    // FR-SDRT (l.400-413): gradient [M16 | Dsol - M16 M0] on [C; U] with rows (s, d); the
+    // divergence Dsol - M14 (n^ . M0) on the solution-point fluxes F[s][d] (columns (s, d))
+    G = Mat(ns * D, r.next + ns);
+    M13F = Mat(ns, ns * D);
+    for (int s2 = 0; s2 < ns; ++s2)
+      for (int d = 0; d < D; ++d) {
+        for (int e = 0; e < r.next; ++e) G(s2 * D + d, e) = O.M16(d * ns + s2, e);
+        for (int q = 0; q < ns; ++q) {
+          double gc = O.Dsol[d](s2, q), dv = O.Dsol[d](s2, q);
+          for (int e = 0; e < r.next; ++e) {
+            gc -= O.M16(d * ns + s2, e) * O.M0(e, q);
+            dv -= O.Mc(s2, e) * r.ext_normal[e][d] * O.M0(e, q);
+          }
+          G(s2 * D + d, r.next + q) = gc;
+          M13F(s2, q * D + d) = dv;
+        }
+      }
+  }
   out->clear();
   out->push_back(pack_frag(O.M0));
   out->push_back(pack_frag(O.M12));
@@ -758,11 +777,12 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tg = (double*)(base + p.off_tg);
     }
     c->sfused = !etype_tensor(m.etype) && !(fg && fg[0] == '1') && simplex_supported(m.nd, m.p, ph->eq);
-    if (O.scheme != 0 && !c->fused) {
+    if (O.scheme != 0 && !c->fused && !c->sfused) {
       delete c;
-      set_error("unsupported: FR schemes run on the fused tensor-element kernels");
+      set_error("unsupported: FR schemes run on the fused element kernels");
       return SDRT_E_UNSUPPORTED;
     }
+    c->sops.fr = O.scheme != 0;
     if (m.slabs.size() > 0 && !c->fused && !c->sfused) {
       delete c;
       set_error("unsupported: halo exchange is implemented for the fused paths only");

@@ -60,6 +60,8 @@ struct SDims {
   static constexpr int kt_G = (next + nu + 3) / 4;       // [M16 | M15 P]
   static constexpr int kt_ext = (next + 3) / 4;          // M14
   static constexpr int kt_F = (D * nu + 3) / 4;          // M13 M19 P2
+  static constexpr int kt_GF = (next + nsol + 3) / 4;    // FR-SDRT [M16 | Dsol - M16 M0]
+  static constexpr int kt_FF = (D * nsol + 3) / 4;       // FR-SDRT divergence on F[s][d]
 };
 
 template <typename T>
@@ -220,6 +222,11 @@ __device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split,
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nj = Dmm<W, E, KT>::jobs(M);
   for (int j = warp; j < nj; j += nw) Dmm<W, E, KT>::template job<ACC>(M, j, X0, split, X1, Y);
+}
+
+// entry M[r][c] of a fragment-packed operator
+__device__ __forceinline__ double sop_at(const SOpF& M, int r, int c) {
+  return __ldg(M.frag + ((int64_t)(r / 8) * M.kt + c / 4) * 32 + (r % 8) * 4 + c % 4);
 }
 
 // ---------------------------------------------------------------- tile helpers
@@ -502,6 +509,104 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   SPH(0, 10)
 }
 
+// Kernel A for FR-SDRT (NEXT row N1): no internal flux points.
+//   U_ext = M0 U;  C in place;  Q~ = [M16 | Dsol - M16 M0][C; U]  (gradient with the SDRT
+//   correction, remark l.429-434);  Q = J^-T Q~;  Q_ext = M0 Q;  published g;  fluxes at the
+//   solution points F[s][d] = detJ (J^-1 (f^c - f^v))_d (in place of Q);
+//   R_int = [Dsol - M14 (n^ . M0)] F  (Eq. divergence_fr l.400-405 without the common flux).
+// Regions (doubles per element): U [nsol NV] | W [next D NV] (U_ext -> C -> Q_ext) |
+// Q [nsol D NV] (Q -> F).
+template <int D, int P, int EQ, int E>
+__global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad_fr(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
+                                                               const __grid_constant__ STileMaps tm) {
+  using Ph = Phys<EQ, D>;
+  using S = SDims<D, P>;
+  constexpr int NV = Ph::NV;
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;
+  double* sW = sU + S::nsol * NV * E;
+  double* sQ = sW + S::next * D * NV * E;
+  __shared__ int sNb[D + 2][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, S::nsol * NV * E * 8);
+    tma_tile<S::nsol * NV, E>(sU, &tm.uin, e0, &bar);
+  }
+  fill_neighbours<D, E>(g, sNb, e0);
+  __syncthreads();
+  NbGather<D, P, NV, E, 256> gath;
+  gath.load(g, b.Tu, sNb, e0);
+  mbar_wait(&bar, 0);
+  dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sW);  // U_ext
+  __syncthreads();
+  gath.common_values(g, ph, sW, sNb, sW, e0);  // C in place of U_ext (same entries per item)
+  __syncthreads();
+  dmm1<NV, S::kt_GF, E, false>(O.G, sW, S::next, sU, sQ);  // rows (s, d) -> [s][d][v]
+  __syncthreads();
+  metric_grad<D, P, NV, E>(g, sNb, sQ);
+  __syncthreads();
+  dmm1<D * NV, S::kt_sol, E, false>(O.M0, sQ, 1 << 30, sQ, sW);  // Q_ext [next][D NV]
+  __syncthreads();
+  // publish g at the face points of the LDG-weighted side (u_ext recomputed from U)
+  const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
+  const int Kp = (int)g.Kt;
+  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
+    const int el = item % E, rho = item / E;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int s = sNb[D + 1][el], f = rho / S::nfp;
+    const bool left = g.left[s][f];
+    if ((left && !pub_left) || (!left && !pub_right)) continue;
+    double u[NV], q[D * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) u[v] = 0.0;
+    for (int sp = 0; sp < S::nsol; ++sp) {
+      const double mv = sop_at(O.M0, rho, sp);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) u[v] = fma(mv, sU[(sp * NV + v) * E + el], u[v]);
+    }
+#pragma unroll
+    for (int k = 0; k < D * NV; ++k) q[k] = sW[(rho * D * NV + k) * E + el];
+    const ExtMetric mt = b.xm[s * S::next + rho];
+    const double nl[3] = {mt.n0, mt.n1, mt.n2};
+    double gv[NV];
+    Ph::visc_dir(ph, u, q, nl, gv);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
+  }
+  // fluxes at the solution points, F[s][d][v] in place of Q[s][d][v] (each item reads its
+  // point's gradient before writing the same entries)
+  for (int item = threadIdx.x; item < S::nsol * E; item += blockDim.x) {
+    const int el = item % E, sp = item / E;
+    const int s = sNb[D + 1][el];
+    double uu[NV], qq[D * NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uu[v] = sU[(sp * NV + v) * E + el];
+#pragma unroll
+    for (int k = 0; k < D * NV; ++k) qq[k] = sQ[(sp * D * NV + k) * E + el];
+    double fo[D][NV];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      double w[D], fv[NV];
+#pragma unroll
+      for (int j = 0; j < D; ++j) w[j] = g.detJ[s] * g.Jinv[s][d * 3 + j];
+      Ph::conv_dir(ph, uu, w, fo[d]);
+      Ph::visc_dir(ph, uu, qq, w, fv);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) fo[d][v] = e0 + el < g.K ? fo[d][v] + fv[v] : 0.0;
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sQ[((sp * D + d) * NV + v) * E + el] = fo[d][v];
+  }
+  __syncthreads();
+  dmm1_global<NV, S::kt_FF, E>(O.M13F, sQ, b.Rint, g.Kp, e0, g.K);  // R_int -> HBM
+}
+
 // Kernel B.  Regions (doubles per element): U [nsol NV] (stage input), R [nsol NV]
 // (R_int, accumulated), UN, ACC [nsol NV] (RK registers), UE [next NV] (own traces,
 // then D~, then the new traces); inviscid: UU [nu NV], F [D nu NV].
@@ -511,7 +616,7 @@ struct SLayoutB {
   static constexpr int U = S::nsol * NV;
   static constexpr int UE = S::next * NV;
   static constexpr int UU = INT ? S::nu * NV : 0;
-  static constexpr int F = INT ? D * S::nu * NV : 0;
+  static constexpr int F = INT ? D * (S::nsol > S::nu ? S::nsol : S::nu) * NV : 0;  // SDRT or FR
   static constexpr int TOTAL = 4 * U + UE + UU + F;
 };
 
@@ -554,8 +659,8 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   mbar_wait(&bar[0], 0);
   // own traces (and, inviscid, U_u)
   const SOpF none{0, 0, 0, 0, nullptr};
-  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, INT ? O.M12 : none, sU, 1 << 30,
-                                                        sU, sUu);
+  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, (INT && !O.fr) ? O.M12 : none, sU,
+                                                        1 << 30, sU, sUu);
   __syncthreads();
   SPH(1, 1)
   // common fluxes D~ = +/- s F at external points, in place over the own traces
@@ -606,7 +711,28 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
       sUe[(rho * NV + v) * E + el] = sc * Fv;
     }
   }
-  if constexpr (INT) internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, nullptr, sF, e0);
+  if constexpr (INT) {
+    if (O.fr) {  // FR-SDRT: fluxes at the solution points, F[s][d][v]
+      for (int item = threadIdx.x; item < S::nsol * E; item += blockDim.x) {
+        const int el = item % E, sp = item / E;
+        const int s = sNb[D + 1][el];
+        double uu[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) uu[v] = sU[(sp * NV + v) * E + el];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double w[D], fo[NV];
+#pragma unroll
+          for (int j = 0; j < D; ++j) w[j] = g.detJ[s] * g.Jinv[s][d * 3 + j];
+          Ph::conv_dir(ph, uu, w, fo);
+#pragma unroll
+          for (int v = 0; v < NV; ++v) sF[((sp * D + d) * NV + v) * E + el] = e0 + el < g.K ? fo[v] : 0.0;
+        }
+      }
+    } else {
+      internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, nullptr, sF, e0);
+    }
+  }
   mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed
   __syncthreads();
   SPH(1, 2)
@@ -615,7 +741,8 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
     dmm1<NV, S::kt_ext, E, false>(O.M14, sUe, 1 << 30, sUe, sR);
     __syncthreads();
   SPH(1, 3)
-    dmm1<NV, S::kt_F, E, true>(O.M13F, sF, 1 << 30, sF, sR);
+    if (O.fr) dmm1<NV, S::kt_FF, E, true>(O.M13F, sF, 1 << 30, sF, sR);
+    else dmm1<NV, S::kt_F, E, true>(O.M13F, sF, 1 << 30, sF, sR);
   } else {
     dmm1<NV, S::kt_ext, E, true>(O.M14, sUe, 1 << 30, sUe, sR);
   }
@@ -801,9 +928,16 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
   if (grid == 0) return;
   if (which == 0) {
     if constexpr (Phys<EQ, D>::VISC) {
-      auto k = ks_grad<D, P, EQ, C::E>;
-      sset_smem((const void*)k, C::SMEM_A);
-      k<<<grid, SDRT_SA_NT, C::SMEM_A, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
+      if (O.fr) {
+        auto k = ks_grad_fr<D, P, EQ, C::E>;
+        const size_t sm = (size_t)(SDims<D, P>::nsol * (1 + D) + SDims<D, P>::next * D) * C::NV * C::E * sizeof(double);
+        sset_smem((const void*)k, sm);
+        k<<<grid, 256, sm, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
+      } else {
+        auto k = ks_grad<D, P, EQ, C::E>;
+        sset_smem((const void*)k, C::SMEM_A);
+        k<<<grid, SDRT_SA_NT, C::SMEM_A, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
+      }
     }
   } else if (which == 1) {
     auto k = ks_stage<D, P, EQ, C::E>;
