@@ -435,6 +435,7 @@ struct sdrt_ctx {
 // to 4, frag[(m * kt + k) * 32 + lane] = M[8 m + lane / 4][4 k + lane % 4].
 struct OpHostF {
   std::vector<double> frag;
+  std::vector<unsigned> kmask;  // per m-tile, bit k: block (m, k) has a non-zero
   int rows, cols, mt, kt;
 };
 
@@ -444,12 +445,17 @@ static OpHostF pack_frag(const Mat& M) {
   o.cols = M.cols;
   o.mt = (M.rows + 7) / 8;
   o.kt = (M.cols + 3) / 4;
+  if (o.kt > 32) throw std::runtime_error("internal: operator too wide for the k-step mask");
   o.frag.assign((size_t)o.mt * o.kt * 32, 0.0);
+  o.kmask.assign(o.mt, 0u);
   for (int m = 0; m < o.mt; ++m)
     for (int k = 0; k < o.kt; ++k)
       for (int lane = 0; lane < 32; ++lane) {
         const int r = 8 * m + lane / 4, c = 4 * k + lane % 4;
-        if (r < M.rows && c < M.cols) o.frag[((size_t)m * o.kt + k) * 32 + lane] = M(r, c);
+        if (r < M.rows && c < M.cols) {
+          o.frag[((size_t)m * o.kt + k) * 32 + lane] = M(r, c);
+          if (M(r, c) != 0.0) o.kmask[m] |= 1u << k;
+        }
       }
   return o;
 }
@@ -458,13 +464,13 @@ static OpHostF pack_frag(const Mat& M) {
 static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
   const RefElement& r = O.ref;
   int ns = r.nsol;
-  Mat G(ns * D, r.next + r.nu);
+  Mat G(ns * D, r.next + r.nu);  // rows (d, s)
   for (int s2 = 0; s2 < ns; ++s2)
     for (int d = 0; d < D; ++d) {
-      for (int e = 0; e < r.next; ++e) G(s2 * D + d, e) = O.M16(d * ns + s2, e);
+      for (int e = 0; e < r.next; ++e) G(d * ns + s2, e) = O.M16(d * ns + s2, e);
       for (int i = 0; i < r.nint; ++i) {
         double v = O.M15(d * ns + s2, i);
-        if (v != 0.0) G(s2 * D + d, r.next + r.int_u[i]) += v;
+        if (v != 0.0) G(d * ns + s2, r.next + r.int_u[i]) += v;
       }
     }
   Mat M13F(ns, D * r.nu);
@@ -480,15 +486,15 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
     M13F = Mat(ns, ns * D);
     for (int s2 = 0; s2 < ns; ++s2)
       for (int d = 0; d < D; ++d) {
-        for (int e = 0; e < r.next; ++e) G(s2 * D + d, e) = O.M16(d * ns + s2, e);
+        for (int e = 0; e < r.next; ++e) G(d * ns + s2, e) = O.M16(d * ns + s2, e);
         for (int q = 0; q < ns; ++q) {
           double gc = O.Dsol[d](s2, q), dv = O.Dsol[d](s2, q);
           for (int e = 0; e < r.next; ++e) {
             gc -= O.M16(d * ns + s2, e) * O.M0(e, q);
             dv -= O.Mc(s2, e) * r.ext_normal[e][d] * O.M0(e, q);
           }
-          G(s2 * D + d, r.next + q) = gc;
-          M13F(s2, q * D + d) = dv;
+          G(d * ns + s2, r.next + q) = gc;
+          M13F(s2, d * ns + q) = dv;
         }
       }
   }
@@ -539,7 +545,7 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   if (!etype_tensor(m.etype)) {
     std::vector<OpHostF> s4;
     simplex_pack(O, D, &s4);
-    for (auto& h : s4) o += align256(h.frag.size() * sizeof(double));
+    for (auto& h : s4) o += align256(h.frag.size() * sizeof(double)) + align256(h.kmask.size() * sizeof(unsigned) + 4);
   }
   // halo lists: send (row, col) and recv (row, col) int32 for all slabs, + a loopback
   // staging buffer of the same number of values
@@ -798,7 +804,13 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         double* dval = (double*)(base + so);
         CUDA_OK(cudaMemcpyAsync(dval, h.frag.data(), h.frag.size() * sizeof(double), cudaMemcpyHostToDevice, st));
         so += align256(h.frag.size() * sizeof(double));
-        *dst[i] = SOpF{h.rows, h.cols, h.mt, h.kt, dval};
+        unsigned* dmask = (unsigned*)(base + so);
+        CUDA_OK(cudaMemcpyAsync(dmask, h.kmask.data(), h.kmask.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st));
+        so += align256(h.kmask.size() * sizeof(unsigned) + 4);
+        const unsigned full = h.kt >= 32 ? ~0u : (1u << h.kt) - 1u;
+        bool dense = true;
+        for (unsigned mk : h.kmask) dense = dense && mk == full;
+        *dst[i] = SOpF{h.rows, h.cols, h.mt, h.kt, dval, dense ? nullptr : dmask};  // dense: no mask reads
       }
       simplex_tma_init(&c->stma, m.nd, m.p, ph->eq, m.K_pad);
       c->Tu[0] = (double*)(base + p.off_tu0);

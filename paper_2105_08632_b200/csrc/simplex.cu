@@ -108,31 +108,35 @@ __host__ __device__ constexpr int ngroup(int n) {
 // from X1 (row stride N = W E doubles); Y rows r < M.rows.  Warp jobs = (m-tile,
 // group of NGR n-tiles).  KT (k steps) is a compile-time constant: all A fragments
 // of a job are requested at once (one L1/L2 round trip per job), then the MMAs run.
-template <int W, int E, int KT>
+template <int W, int E, int KT, int YS = W * E>
 struct Dmm {
   static constexpr int N = W * E;
   static_assert(N % 8 == 0, "tile columns must be a multiple of 8");
+  static_assert(KT <= 32, "k-step mask");
   static constexpr int NT8 = N / 8;
   static constexpr int NGR = ngroup(NT8);
   static constexpr int NG = NT8 / NGR;
 
   __device__ __forceinline__ static int jobs(const SOpF& M) { return M.mt * NG; }
 
+  // Y rows at stride YS doubles (YS > N: interleaved outputs of several products)
   template <bool ACCUM>
   __device__ __forceinline__ static void job(const SOpF& M, int j, const double* X0, int split, const double* X1,
                                              double* Y) {
     const int lane = threadIdx.x & 31;
     const int m = j / NG, ng = j % NG;
     const int n0 = ng * NGR * 8 + (lane >> 2);
+    const unsigned km = M.kmask ? __ldg(M.kmask + m) : 0xffffffffu;  // structurally zero blocks skipped
     const double* af = M.frag + (int64_t)m * KT * 32 + lane;
     double a[KT];
 #pragma unroll
-    for (int k = 0; k < KT; ++k) a[k] = __ldg(af + k * 32);
+    for (int k = 0; k < KT; ++k) a[k] = (km >> k & 1u) ? __ldg(af + k * 32) : 0.0;
     double c[NGR][2];
 #pragma unroll
     for (int q = 0; q < NGR; ++q) c[q][0] = c[q][1] = 0.0;
 #pragma unroll
     for (int k = 0; k < KT; ++k) {
+      if (!(km >> k & 1u)) continue;
       const int col = 4 * k + (lane & 3);
       const double* xr = col < split ? X0 + col * N : X1 + (col - split) * N;
       const bool ok = col < M.cols;
@@ -146,7 +150,7 @@ struct Dmm {
     if (r < M.rows) {
 #pragma unroll
       for (int q = 0; q < NGR; ++q) {
-        double2* y = reinterpret_cast<double2*>(Y + r * N + ng * NGR * 8 + 8 * q + 2 * (lane & 3));
+        double2* y = reinterpret_cast<double2*>(Y + r * YS + ng * NGR * 8 + 8 * q + 2 * (lane & 3));
         if (ACCUM) {
           const double2 o = *y;
           *y = make_double2(o.x + c[q][0], o.y + c[q][1]);
@@ -157,6 +161,39 @@ struct Dmm {
     }
   }
 };
+
+// Y1 = M1 X1 (W1 per row, KT1 k steps) and Y2 = M2 X2 (W2, KT2) in one phase
+// (independent products; M2.frag == nullptr skips the second)
+template <int W1, int KT1, int W2, int KT2, int E, bool ACC1, bool ACC2>
+__device__ __forceinline__ void dmm2(const SOpF& M1, const double* X1a, int s1, const double* X1b, double* Y1,
+                                     const SOpF& M2, const double* X2a, int s2, const double* X2b, double* Y2) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int j1 = Dmm<W1, E, KT1>::jobs(M1), j2 = M2.frag ? Dmm<W2, E, KT2>::jobs(M2) : 0;
+  for (int j = warp; j < j1 + j2; j += nw) {
+    if (j < j1) Dmm<W1, E, KT1>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
+    else Dmm<W2, E, KT2>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
+  }
+}
+
+template <int W, int KT, int E, bool ACC>
+__device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split, const double* X1, double* Y) {
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nj = Dmm<W, E, KT>::jobs(M);
+  for (int j = warp; j < nj; j += nw) Dmm<W, E, KT>::template job<ACC>(M, j, X0, split, X1, Y);
+}
+
+// the same operator on the ND row blocks of a [nd][rows][W][E] tile (block stride XS
+// doubles), written interleaved as Y[r][nd][W][E]: one job pool for all blocks
+template <int W, int KT, int E, int ND>
+__device__ __forceinline__ void dmm_blocks(const SOpF& M, const double* X, int XS, double* Y) {
+  using DM = Dmm<W, E, KT, ND * W * E>;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nj = DM::jobs(M);
+  for (int j = warp; j < ND * nj; j += nw) {
+    const int d = j / nj;
+    DM::template job<false>(M, j % nj, X + d * XS, 1 << 30, X + d * XS, Y + d * W * E);
+  }
+}
 
 // Y = M X with the result rows written straight from the MMA fragments to global
 // memory, G[(r W + w) ld + e0 + el] (element-major ABI layout, 16-byte stores), for
@@ -171,14 +208,16 @@ __device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, doub
     const int m = j / DM::NG, ng = j % DM::NG;
     const int n0 = ng * DM::NGR * 8 + (lane >> 2);
     const double* af = M.frag + (int64_t)m * KT * 32 + lane;
+    const unsigned km = M.kmask ? __ldg(M.kmask + m) : 0xffffffffu;
     double a[KT];
 #pragma unroll
-    for (int k = 0; k < KT; ++k) a[k] = __ldg(af + k * 32);
+    for (int k = 0; k < KT; ++k) a[k] = (km >> k & 1u) ? __ldg(af + k * 32) : 0.0;
     double c[DM::NGR][2];
 #pragma unroll
     for (int q = 0; q < DM::NGR; ++q) c[q][0] = c[q][1] = 0.0;
 #pragma unroll
     for (int k = 0; k < KT; ++k) {
+      if (!(km >> k & 1u)) continue;
       const int col = 4 * k + (lane & 3);
       const bool ok = col < M.cols;
 #pragma unroll
@@ -202,26 +241,6 @@ __device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, doub
       }
     }
   }
-}
-
-// Y1 = M1 X1 (W1 per row, KT1 k steps) and Y2 = M2 X2 (W2, KT2) in one phase
-// (independent products; M2.frag == nullptr skips the second)
-template <int W1, int KT1, int W2, int KT2, int E, bool ACC1, bool ACC2>
-__device__ __forceinline__ void dmm2(const SOpF& M1, const double* X1a, int s1, const double* X1b, double* Y1,
-                                     const SOpF& M2, const double* X2a, int s2, const double* X2b, double* Y2) {
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int j1 = Dmm<W1, E, KT1>::jobs(M1), j2 = M2.frag ? Dmm<W2, E, KT2>::jobs(M2) : 0;
-  for (int j = warp; j < j1 + j2; j += nw) {
-    if (j < j1) Dmm<W1, E, KT1>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
-    else Dmm<W2, E, KT2>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
-  }
-}
-
-template <int W, int KT, int E, bool ACC>
-__device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split, const double* X1, double* Y) {
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nj = Dmm<W, E, KT>::jobs(M);
-  for (int j = warp; j < nj; j += nw) Dmm<W, E, KT>::template job<ACC>(M, j, X0, split, X1, Y);
 }
 
 // entry M[r][c] of a fragment-packed operator
@@ -323,7 +342,7 @@ struct NbGather {
   }
 };
 
-// Q = J^-T Q~ in place on sQ [nsol][D][NV][E]
+// Q = J^-T Q~ in place on sQ [D][nsol][NV][E]
 template <int D, int P, int NV, int E>
 __device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E], double* sQ) {
   using S = SDims<D, P>;
@@ -334,13 +353,13 @@ __device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E
     for (int v = 0; v < NV; ++v) {
       double qt[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) qt[d] = sQ[((sp * D + d) * NV + v) * E + el];
+      for (int d = 0; d < D; ++d) qt[d] = sQ[((d * S::nsol + sp) * NV + v) * E + el];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j) acc = fma(g.Jinv[s][j * 3 + i], qt[j], acc);
-        sQ[((sp * D + i) * NV + v) * E + el] = acc;
+        sQ[((i * S::nsol + sp) * NV + v) * E + el] = acc;
       }
     }
   }
@@ -464,14 +483,14 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   gath.common_values(g, ph, sUe, sNb, sX, e0);  // C into X (U is dead)
   __syncthreads();
   SPH(0, 2)
-  dmm1<NV, S::kt_G, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
+  dmm1<NV, S::kt_G, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (d, s) -> [d][s][v]
   __syncthreads();
   SPH(0, 3)
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
   SPH(0, 4)
   // gradient at the external points (M0 on each of the D NV gradient rows) into X
-  dmm1<D * NV, S::kt_sol, E, false>(O.M0, sQ, 1 << 30, sQ, sX);
+  dmm_blocks<NV, S::kt_sol, E, D>(O.M0, sQ, S::nsol * NV * E, sX);  // Q_ext [next][d][v]
   __syncthreads();
   SPH(0, 5)
   // publish g at the face points of the LDG-weighted side
@@ -498,7 +517,7 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   }
   __syncthreads();
   SPH(0, 6)
-  dmm1<D * NV, S::kt_sol, E, false>(O.M12, sQ, 1 << 30, sQ, sUe);  // Q_u = M18 Q [nu][D NV] into UE
+  dmm_blocks<NV, S::kt_sol, E, D>(O.M12, sQ, S::nsol * NV * E, sUe);  // Q_u = M18 Q [nu][d][v] into UE
   __syncthreads();
   SPH(0, 7)
   internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
@@ -544,11 +563,11 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad_fr(GeomDev g, Simpl
   __syncthreads();
   gath.common_values(g, ph, sW, sNb, sW, e0);  // C in place of U_ext (same entries per item)
   __syncthreads();
-  dmm1<NV, S::kt_GF, E, false>(O.G, sW, S::next, sU, sQ);  // rows (s, d) -> [s][d][v]
+  dmm1<NV, S::kt_GF, E, false>(O.G, sW, S::next, sU, sQ);  // rows (d, s) -> [d][s][v]
   __syncthreads();
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
-  dmm1<D * NV, S::kt_sol, E, false>(O.M0, sQ, 1 << 30, sQ, sW);  // Q_ext [next][D NV]
+  dmm_blocks<NV, S::kt_sol, E, D>(O.M0, sQ, S::nsol * NV * E, sW);  // Q_ext [next][d][v]
   __syncthreads();
   // publish g at the face points of the LDG-weighted side (u_ext recomputed from U)
   const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
@@ -586,7 +605,10 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad_fr(GeomDev g, Simpl
 #pragma unroll
     for (int v = 0; v < NV; ++v) uu[v] = sU[(sp * NV + v) * E + el];
 #pragma unroll
-    for (int k = 0; k < D * NV; ++k) qq[k] = sQ[(sp * D * NV + k) * E + el];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) qq[d * NV + v] = sQ[((d * S::nsol + sp) * NV + v) * E + el];
     double fo[D][NV];
 #pragma unroll
     for (int d = 0; d < D; ++d) {
@@ -601,10 +623,10 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad_fr(GeomDev g, Simpl
 #pragma unroll
     for (int d = 0; d < D; ++d)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) sQ[((sp * D + d) * NV + v) * E + el] = fo[d][v];
+      for (int v = 0; v < NV; ++v) sQ[((d * S::nsol + sp) * NV + v) * E + el] = fo[d][v];
   }
   __syncthreads();
-  dmm1_global<NV, S::kt_FF, E>(O.M13F, sQ, b.Rint, g.Kp, e0, g.K);  // R_int -> HBM
+  dmm1_global<NV, S::kt_FF, E>(O.M13F, sQ, b.Rint, g.Kp, e0, g.K);  // R_int -> HBM (columns (d, s))
 }
 
 // Kernel B.  Regions (doubles per element): U [nsol NV] (stage input), R [nsol NV]
@@ -658,7 +680,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   SPH(1, 0)
   mbar_wait(&bar[0], 0);
   // own traces (and, inviscid, U_u)
-  const SOpF none{0, 0, 0, 0, nullptr};
+  const SOpF none{0, 0, 0, 0, nullptr, nullptr};
   dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, (INT && !O.fr) ? O.M12 : none, sU,
                                                         1 << 30, sU, sUu);
   __syncthreads();
@@ -726,7 +748,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
           for (int j = 0; j < D; ++j) w[j] = g.detJ[s] * g.Jinv[s][d * 3 + j];
           Ph::conv_dir(ph, uu, w, fo);
 #pragma unroll
-          for (int v = 0; v < NV; ++v) sF[((sp * D + d) * NV + v) * E + el] = e0 + el < g.K ? fo[v] : 0.0;
+          for (int v = 0; v < NV; ++v) sF[((d * S::nsol + sp) * NV + v) * E + el] = e0 + el < g.K ? fo[v] : 0.0;
         }
       }
     } else {
@@ -834,7 +856,7 @@ __global__ void __launch_bounds__(256) ks_diag(GeomDev g, SimplexOps O, PhysDev 
   __syncthreads();
   gath.common_values(g, ph, sUe, sNb, sC, e0);
   __syncthreads();
-  dmm1<NV, S::kt_G, E, false>(O.G, sC, S::next, sUu, sQ);  // rows (s, d) -> [s][d][v]
+  dmm1<NV, S::kt_G, E, false>(O.G, sC, S::next, sUu, sQ);  // rows (d, s) -> [d][s][v]
   __syncthreads();
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
@@ -857,7 +879,7 @@ __global__ void __launch_bounds__(256) ks_diag(GeomDev g, SimplexOps O, PhysDev 
       for (int j = 0; j < D; ++j)
 #pragma unroll
         for (int i = 0; i < D; ++i)
-          dv[j][i] = (sQ[((sp * D + j) * NV + 1 + i) * E + el] - v[i] * sQ[((sp * D + j) * NV) * E + el]) / rho;
+          dv[j][i] = (sQ[((j * S::nsol + sp) * NV + 1 + i) * E + el] - v[i] * sQ[((j * S::nsol + sp) * NV) * E + el]) / rho;
       double div = 0.0;
 #pragma unroll
       for (int i = 0; i < D; ++i) div += dv[i][i];

@@ -17,16 +17,18 @@ namespace sdrt {
 struct SOpF {
   int rows, cols, mt, kt;
   const double* frag;
+  const unsigned* kmask;  // per m-tile: bit k set if the 8x4 block (m, k) has a non-zero
 };
 
 struct SimplexOps {
   SOpF M0;    // N_ext x N_sol
   SOpF M12;   // N_u x N_sol
-  SOpF G;     // (N_sol*D) x (N_ext + N_u): rows (s, d), [M16 | M15 P]
-              //   FR-SDRT: (N_sol*D) x (N_ext + N_sol), [M16 | Dsol - M16 M0] on [C; U]
+  SOpF G;     // (D*N_sol) x (N_ext + N_u): rows (d, s), [M16 | M15 P]; the face blocks of
+              //   M16 whose normal lacks a d component are zero 8x4 blocks (skipped)
+              //   FR-SDRT: (D*N_sol) x (N_ext + N_sol), [M16 | Dsol - M16 M0] on [C; U]
   SOpF M14;   // N_sol x N_ext
   SOpF M13F;  // N_sol x (D N_u): M13 M19 P2, columns (d, u)
-              //   FR-SDRT: N_sol x (N_sol D), Dsol - M14 (n^ . M0), columns (s, d)
+              //   FR-SDRT: N_sol x (D N_sol), Dsol - M14 (n^ . M0), columns (d, s)
   int fr;     // 1: FR-SDRT (NEXT row N1), fluxes at the solution points
 };
 
