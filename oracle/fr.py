@@ -8,9 +8,14 @@ solution points plus corrections at the external points,
                    + sum_nu [ D~_nu - (sum_r f~_r l_r(x_nu)) . n^_nu ] div g_nu (x_s)
 (Eq. divergence_fr, l.400-405), with D~ the scaled common normal flux of the SDRT path.
     FR-SDRT: div g_nu = div psi_nu, the SDRT external RT basis  ->  M14     (l.407-413)
-    FR-DG:   g_nu = the DG correction; for tensor elements the 1D right/left Radau
-             polynomials of degree p+1 along the face normal (Huynh's g_DG), i.e.
-             div g_nu (x_s) = -/+ g_L/R'(xi_{s,d}) delta_tangential(s, nu)
+    FR-DG:   g_nu = the correction that recovers nodal DG (l.371-373); for tensor
+             elements the 1D right/left Radau polynomials of degree p+1 along the face
+             normal (Huynh's g_DG), i.e.
+             div g_nu (x_s) = -/+ g_L/R'(xi_{s,d}) delta_tangential(s, nu);
+             for simplices the DG lifting  div g_nu (x_s) = (M^-1 L)_{s nu},
+             M_rs = int l_r l_s,  L_{r nu} = int_{face(nu)} l_r ell_nu dS~, with ell_nu
+             the degree-p Lagrange basis of the face's flux points (dg_lift; reading in
+             DESIGN.md).  For tensor elements dg_lift equals the Radau form (test pin).
 The auxiliary gradient uses the same corrections (remark l.429-434):
     q~_d = sum_r u_r d_d l_r + sum_nu n^_nu,d (C_nu - u_h(x_nu)) div g_nu.
 Everything else (C, common fluxes, metric terms, dU/dt = -R~/detJ) is the SDRT
@@ -18,13 +23,16 @@ residual's (residual.py).
 """
 from __future__ import annotations
 
+import itertools
+import math
+from fractions import Fraction
 from functools import lru_cache
 
 import numpy as np
 
 from . import physics as phys
-from .operators import _decpts, _f64, _inverse, _mono, build_operators, sol_span
-from .points import reference_element
+from .operators import _decpts, _exps_total, _f64, _inverse, _mono, _mono_integral, build_operators, sol_span
+from .points import TET_FACES, TET_V, TRI_FACES, TRI_V, reference_element
 from .residual import Residual
 
 
@@ -101,6 +109,120 @@ def dg_correction_tensor(etype, p):
     return Mc
 
 
+def _pmul(a, b):
+    """Product of polynomials held as {exponent tuple: coefficient}."""
+    out = {}
+    for ea, ca in a.items():
+        for eb, cb in b.items():
+            e = tuple(x + y for x, y in zip(ea, eb))
+            out[e] = out.get(e, 0) + ca * cb
+    return out
+
+
+@lru_cache(maxsize=None)
+def _unit_integral(e, simplex):
+    """Exact int of t^e over the unit simplex (Dirichlet: prod e_i! / (|e| + m)!) or the
+    unit box [0, 1]^m (prod 1 / (e_i + 1)), as Decimal."""
+    from decimal import Decimal
+    if simplex:
+        num = 1
+        for k in e:
+            num *= math.factorial(k)
+        v = Fraction(num, math.factorial(sum(e) + len(e)))
+    else:
+        v = Fraction(1)
+        for k in e:
+            v /= k + 1
+    return Decimal(v.numerator) / Decimal(v.denominator)
+
+
+def _faces(etype, D):
+    """Per reference face: (origin x0, edge vectors T (columns), simplex parameter domain?)
+    in exact integers.  Simplex faces from the vertex lists; tensor face 2d+s is x_d = 2s-1
+    with the other coordinates spanning [-1, 1]."""
+    if etype in ("tri", "tet"):
+        V, F = (TRI_V, TRI_FACES) if etype == "tri" else (TET_V, TET_FACES)
+        out = []
+        for f in F:
+            x0 = V[f[0]]
+            T = [tuple(V[f[k]][c] - x0[c] for c in range(D)) for k in range(1, len(f))]
+            out.append((x0, T, True))
+        return out
+    out = []
+    for d in range(D):
+        for sd in range(2):
+            x0 = tuple((2 * sd - 1) if c == d else -1 for c in range(D))
+            T = [tuple(2 if c == a else 0 for c in range(D)) for a in range(D) if a != d]
+            out.append((x0, T, False))
+    return out
+
+
+@lru_cache(maxsize=None)
+def dg_lift(etype, p):
+    """Mc[s, nu] = (M^-1 L)[s, nu]: the DG lifting of the face-point values (FR-DG on any
+    element type), with exact integrals (monomials over the reference element, and over
+    each face in its affine parametrisation x = x0 + T t), 40-digit decimal arithmetic,
+    rounded once."""
+    from decimal import Decimal
+    o = build_operators(etype, p)
+    ref = reference_element(etype, p)
+    D = o.nd
+    sspan = sol_span(etype, p, D)
+    xsol = _decpts(ref.xsol)
+    xext = _decpts(ref.xext)
+    Cu = _inverse(np.array([[_mono(e, x) for x in xsol] for e in sspan], dtype=object))
+    n = len(sspan)
+    # mass matrix M = Cu I Cu^T, I_km = int phi_k phi_m
+    I = np.array([[_mono_integral(etype, tuple(a + b for a, b in zip(ek, em))) for em in sspan] for ek in sspan],
+                 dtype=object)
+    M = Cu.dot(I).dot(Cu.T)
+    L = np.empty((n, o.next), dtype=object)
+    L[:, :] = Decimal(0)
+    for f, (x0, T, simp) in enumerate(_faces(etype, D)):
+        m = len(T)
+        nus = [nu for nu in range(o.next) if ref.ext_face[nu] == f]
+        # face parameters of the face points: t = (T^T T)^-1 T^T (x - x0)
+        G = np.array([[Decimal(sum(T[a][c] * T[b][c] for c in range(D))) for b in range(m)] for a in range(m)],
+                     dtype=object)
+        Gi = _inverse(G)
+        ts = []
+        for nu in nus:
+            rhs = [sum(Decimal(T[a][c]) * (xext[nu][c] - Decimal(x0[c])) for c in range(D)) for a in range(m)]
+            ts.append(tuple(sum(Gi[a, b] * rhs[b] for b in range(m)) for a in range(m)))
+        fspan = _exps_total(m, p) if simp else list(itertools.product(range(p + 1), repeat=m))
+        Cl = _inverse(np.array([[_mono(e, t) for t in ts] for e in fspan], dtype=object))  # ell_j = sum Cl[j,k] t^e_k
+        scale = np.linalg.det(np.array([[float(G[a, b]) for b in range(m)] for a in range(m)]))
+        scale = Decimal(int(round(scale))).sqrt()   # Gram determinants are integers here
+        # x_c(t) = x0_c + sum_a T[a][c] t_a as polynomials in t
+        xc = []
+        for c in range(D):
+            poly = {tuple([0] * m): Decimal(x0[c])}
+            for a in range(m):
+                if T[a][c]:
+                    e = [0] * m
+                    e[a] = 1
+                    poly[tuple(e)] = poly.get(tuple(e), 0) + Decimal(T[a][c])
+            xc.append(poly)
+        for k, ek in enumerate(sspan):
+            phi = {tuple([0] * m): Decimal(1)}
+            for c in range(D):
+                for _ in range(ek[c]):
+                    phi = _pmul(phi, xc[c])
+            # int_face phi_k ell_j dS = scale * sum Cl[j, i] int t^(e + f_i)
+            for j, nu in enumerate(nus):
+                v = Decimal(0)
+                for i, fi in enumerate(fspan):
+                    if Cl[j, i] == 0:
+                        continue
+                    acc = Decimal(0)
+                    for te, cf in phi.items():
+                        acc += cf * _unit_integral(tuple(a + b for a, b in zip(te, fi)), simp)
+                    v += Cl[j, i] * acc
+                for r in range(n):
+                    L[r, nu] += Cu[r, k] * v * scale
+    return _f64(_inverse(M).dot(L))
+
+
 class FRResidual(Residual):
     """dU/dt of the FR-SDRT or FR-DG scheme on the same mesh, points and common fluxes."""
 
@@ -109,7 +231,12 @@ class FRResidual(Residual):
         o = self.ops
         self.scheme = scheme
         self.Dsol = sol_derivatives(mesh.etype, mesh.p)
-        self.Mc = o.M14 if scheme == "frsdrt" else dg_correction_tensor(mesh.etype, mesh.p)
+        if scheme == "frsdrt":
+            self.Mc = o.M14
+        elif mesh.etype in ("quad", "hex"):
+            self.Mc = dg_correction_tensor(mesh.etype, mesh.p)
+        else:
+            self.Mc = dg_lift(mesh.etype, mesh.p)
         # gradient correction per direction: (Mc_d)[s, nu] = n^_nu,d Mc[s, nu]
         self.Mcd = [self.Mc * o.ext_normal[None, :, d] for d in range(o.nd)]
 

@@ -5,6 +5,11 @@
   runs agree to 6.11e-16, Tables l.1855, l.1866), on every element type.
 * FR-DG on quadrilaterals reproduces the paper's FR-DG tau_MAX tables (advection
   l.1236-1243, diffusion l.1576-1585) with the oracle's Von Neumann harness.
+* FR-DG on simplices (the DG lifting, oracle.fr.dg_lift): equals the Radau form on
+  tensor elements (two independent constructions of the same correction), integrates
+  to the face measure, and reproduces the paper's FR-DG triangle tau_MAX tables
+  (diffusion l.1612-1618; advection l.1255, l.1272 through the FR-DG/SDRT ratio, since the
+  simplex advection length scale differs by a constant factor).
 * freestream and discrete conservation for both schemes (l.170-172, l.312-318).
 """
 import functools
@@ -13,7 +18,7 @@ import numpy as np
 import pytest
 
 from oracle import vonneumann as VN
-from oracle.fr import FRResidual
+from oracle.fr import FRResidual, dg_correction_tensor, dg_lift
 from oracle.mesh import build_mesh
 from oracle.operators import build_operators
 from oracle.physics import Physics
@@ -64,8 +69,56 @@ def test_frdg_quad_tau_max_tables(p):
     assert abs(VN.tau_max(lam, 4) - GOLD["tau_max_frdg_quad"]["advection"][str(p)][1]) <= 2.5e-3
 
 
+@pytest.mark.parametrize("etype,p", [("quad", 1), ("quad", 2), ("quad", 3), ("quad", 4), ("hex", 1), ("hex", 2)])
+def test_dg_lift_equals_radau_on_tensor(etype, p):
+    """The generic DG lifting (mass matrix + face integrals) and Huynh's Radau g_DG are
+    built by unrelated formulas; on tensor elements they are the same correction."""
+    a, b = dg_lift(etype, p), dg_correction_tensor(etype, p)
+    assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("etype,p", [("tri", 1), ("tri", 2), ("tri", 3), ("tri", 4), ("tet", 1), ("tet", 2)])
+def test_dg_lift_face_measure(etype, p):
+    """sum_s w_s div g_nu(x_s) = int div g_nu = int_face ell_nu dS: the face weights, which
+    sum to the face measure (tri: 2, 2 sqrt2, 2; tet: 2, 2, 2 sqrt3, 2), and the lifted
+    correction of a face's constant is the same for every point ordering."""
+    o = build_operators(etype, p)
+    fw = o.w @ dg_lift(etype, p)
+    area = {"tri": [2, 2 * np.sqrt(2), 2], "tet": [2, 2, 2 * np.sqrt(3), 2]}[etype]
+    for f in range(o.nfaces):
+        assert abs(fw[o.ext_face == f].sum() - area[f]) <= 1e-13
+    assert (fw > 0).all()
+
+
+GOLD_FRDG_TRI = {  # FR-DG Triangles, diffusion tau_MAX (RK3, RK4, RK54), PAPER.md l.1612-1618
+    1: [0.0418, 0.0464, 0.0776], 2: [0.0144, 0.0160, 0.0267], 3: [0.0054, 0.0060, 0.0101], 4: [0.0027, 0.0030, 0.0050]}
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_frdg_tri_tau_max_tables(p):
+    res = functools.partial(FRResidual, scheme="frdg")
+    B = VN.pattern_blocks("tri", p, VN.diffusion_physics(2), layers=2, residual=res)
+    lam = VN.spectrum(B, [np.array([k, 0.0]) for k in np.linspace(0, 2 * np.pi, 361)])
+    assert lam.real.max() < 1e-10
+    for stages, r in zip((3, 4, "rk54"), GOLD_FRDG_TRI[p]):
+        assert abs(VN.tau_max(lam, stages) - r) <= 1.2e-4, (stages, VN.tau_max(lam, stages), r)
+
+
+def test_frdg_tri_advection_ratio():
+    """Advection, triangles p=2, RK4: FR-DG / SDRT = 0.140 / 0.198 (l.1272, l.1255)."""
+    ph = VN.advection_physics(2)
+    d = np.array(ph.c)
+    ks = [k * d for k in np.linspace(0, np.pi / np.abs(d).max(), 401)]
+    t = {}
+    for name, res in (("sdrt", Residual), ("frdg", functools.partial(FRResidual, scheme="frdg"))):
+        lam = VN.spectrum(VN.pattern_blocks("tri", 2, ph, layers=1, residual=res), ks)
+        t[name] = VN.tau_max(lam, 4)
+    assert abs(t["frdg"] / t["sdrt"] - 0.140 / 0.198) <= 0.01, t
+
+
 @pytest.mark.parametrize("scheme,etype,p", [("frsdrt", "tri", 3), ("frsdrt", "tet", 2), ("frsdrt", "hex", 2),
-                                            ("frdg", "quad", 3), ("frdg", "hex", 2)])
+                                            ("frdg", "quad", 3), ("frdg", "hex", 2), ("frdg", "tri", 3),
+                                            ("frdg", "tet", 2)])
 def test_fr_freestream_and_conservation(scheme, etype, p):
     D = ND[etype]
     cfg = CONFIGS["c4" if D == 3 else "c2"]
