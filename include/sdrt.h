@@ -49,7 +49,8 @@ typedef enum {
 typedef enum { SDRT_QUAD = 0, SDRT_TRI = 1, SDRT_HEX = 2, SDRT_TET = 3 } sdrt_etype;
 /* schemes: SDRT (the path); FR-SDRT and FR-DG flux reconstruction on the same data
  * (NEXT row N1): no internal flux points, solution-point fluxes
- * with the SDRT (FR-SDRT) or DG/Radau (FR-DG, tensor elements) corrections */
+ * with the SDRT (FR-SDRT) or DG (FR-DG: Radau on tensor elements, DG lifting on
+ * simplices) corrections */
 typedef enum { SDRT_SCHEME_SDRT = 0, SDRT_SCHEME_FRSDRT = 1, SDRT_SCHEME_FRDG = 2 } sdrt_scheme;
 /* equations: linear advection, linear advection-diffusion (l.1658), Euler
  * (l.1909-1935), compressible Navier-Stokes (l.2012-2030) */
@@ -128,8 +129,11 @@ sdrt_status sdrt_mesh_neighbor(const sdrt_mesh* m, int64_t e, int f, int64_t* co
 /* Appendix-B operators for (etype, p), built in __float128 and rounded once.
  * Errors: SDRT_E_UNSUPPORTED, SDRT_E_ILL_CONDITIONED (cond(V^f) > 1e12). */
 sdrt_status sdrt_operators_build(int etype, int p, int scheme, sdrt_operators** out);
-/* name in {"M0","M12","M13","M14","M15","M16","P","M19P2","w","xsol","xext","xu"};
- * dst == NULL queries the shape. Row-major doubles, host memory. */
+/* name in {"M0","M12","M13","M14","M15","M16","P","M19P2","w","xsol","xext","xu"}, and for
+ * the FR schemes "Mc" (N_sol x N_ext, div g_nu at the solution points: M14 for FR-SDRT,
+ * l.407-413; FR-DG: Radau g_DG on tensor elements, the DG lifting M^-1 L on simplices,
+ * l.371-373). dst == NULL queries the shape. Row-major doubles, host memory.
+ * Errors: SDRT_E_INVALID_ARG for an unknown name. */
 sdrt_status sdrt_operators_get(const sdrt_operators* o, const char* name, double* dst, int* rows,
                                int* cols);
 void sdrt_operators_destroy(sdrt_operators* o);

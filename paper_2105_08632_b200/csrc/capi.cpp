@@ -269,6 +269,7 @@ sdrt_status sdrt_operators_get(const sdrt_operators* oo, const char* name, doubl
   else if (n == "M16") M = &o.M16;
   else if (n == "P") M = &o.P;
   else if (n == "M19P2") M = &o.M19P2;
+  else if (n == "Mc" && o.scheme != 0) M = &o.Mc;
   if (M) {
     if (rows) *rows = M->rows;
     if (cols) *cols = M->cols;

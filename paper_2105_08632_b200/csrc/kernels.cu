@@ -480,17 +480,19 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
       if (v != 0.0) M13F(s2, r.int_dir[i] * r.nu + r.int_u[i]) += v;
     }
   if (O.scheme != 0) {
-    // FR-SDRT (l.400-413): gradient [M16 | Dsol - M16 M0] on [C; U] with rows (s, d); the
-    // divergence Dsol - M14 (n^ . M0) on the solution-point fluxes F[s][d] (columns (s, d))
+    // FR (l.400-413, gradient remark l.429-434): with Mc = div g (FR-SDRT: M14, FR-DG: the
+    // DG lifting) and Mc_d = Mc n^_d, the gradient [Mc_d | Dsol_d - Mc_d M0] on [C; U] with
+    // rows (d, s); the divergence Dsol - Mc (n^ . M0) on the solution-point fluxes F[d][s]
+    // (columns (d, s)); the face lift Mc (kernel B)
     G = Mat(ns * D, r.next + ns);
     M13F = Mat(ns, ns * D);
     for (int s2 = 0; s2 < ns; ++s2)
       for (int d = 0; d < D; ++d) {
-        for (int e = 0; e < r.next; ++e) G(d * ns + s2, e) = O.M16(d * ns + s2, e);
+        for (int e = 0; e < r.next; ++e) G(d * ns + s2, e) = O.Mc(s2, e) * r.ext_normal[e][d];
         for (int q = 0; q < ns; ++q) {
           double gc = O.Dsol[d](s2, q), dv = O.Dsol[d](s2, q);
           for (int e = 0; e < r.next; ++e) {
-            gc -= O.M16(d * ns + s2, e) * O.M0(e, q);
+            gc -= O.Mc(s2, e) * r.ext_normal[e][d] * O.M0(e, q);
             dv -= O.Mc(s2, e) * r.ext_normal[e][d] * O.M0(e, q);
           }
           G(d * ns + s2, r.next + q) = gc;
@@ -502,7 +504,7 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
   out->push_back(pack_frag(O.M0));
   out->push_back(pack_frag(O.M12));
   out->push_back(pack_frag(G));
-  out->push_back(pack_frag(O.M14));
+  out->push_back(pack_frag(O.scheme != 0 ? O.Mc : O.M14));
   out->push_back(pack_frag(M13F));
 }
 

@@ -654,6 +654,134 @@ static void exps_total(int D, int p, std::vector<std::vector<int>>& out) {
   }
 }
 
+// Quadrature on the unit m-simplex {t >= 0, sum t <= 1} (m = 1, 2, 3) by the collapsed
+// (Duffy) product of nq-point Gauss-Legendre rules: exact for degree <= 2 nq - m.
+static void unit_simplex_rule(int m, int nq, std::vector<std::array<qd, 3>>& pts, std::vector<qd>& wts) {
+  std::vector<qd> g, gw;
+  gauss_legendre(nq, g, gw);
+  pts.clear();
+  wts.clear();
+  for (int i = 0; i < nq; ++i) {
+    const qd a = (g[i] + 1) / 2, wa = gw[i] / 2;
+    if (m == 1) {
+      pts.push_back({a, 0, 0});
+      wts.push_back(wa);
+      continue;
+    }
+    for (int j = 0; j < nq; ++j) {
+      const qd b = (g[j] + 1) / 2, wb = gw[j] / 2;
+      if (m == 2) {
+        pts.push_back({a, (1 - a) * b, 0});
+        wts.push_back(wa * wb * (1 - a));
+        continue;
+      }
+      for (int k = 0; k < nq; ++k) {
+        const qd c = (g[k] + 1) / 2, wc = gw[k] / 2;
+        pts.push_back({a, (1 - a) * b, (1 - a) * (1 - b) * c});
+        wts.push_back(wa * wb * wc * (1 - a) * (1 - a) * (1 - b));
+      }
+    }
+  }
+}
+
+// FR-DG correction on simplices (l.371-373: the correction functions that recover nodal
+// DG): the DG lifting Mc = M^-1 L with M_rs = int l_r l_s over the reference simplex and
+// L_{r nu} = int_{face(nu)} l_r ell_nu dS~, ell_nu the degree-p Lagrange basis of the
+// face's flux points in the face parameters; integrals by collapsed Gauss rules.
+// Y: solution basis coefficients (l_r = sum_k Y[k][r] mono(Ptot[k], x)).
+static Mat simplex_dg_lift(const RefQ& R, const std::vector<qd>& Y, const std::vector<std::vector<int>>& Ptot) {
+  const RefElement& r = R.r;
+  const int D = r.nd, ns = r.nsol, nq = r.p + 3;
+  std::vector<P3> V;
+  if (D == 2)
+    for (auto& v : TRI_V) V.push_back({(qd)v[0], (qd)v[1], 0});
+  else
+    for (auto& v : TET_V) V.push_back({(qd)v[0], (qd)v[1], (qd)v[2]});
+  auto lval = [&](const P3& x, std::vector<qd>& out) {
+    out.assign(ns, 0);
+    for (int k = 0; k < ns; ++k) {
+      const qd m = mono(Ptot[k], x);
+      for (int rr = 0; rr < ns; ++rr) out[rr] += Y[(size_t)k * ns + rr] * m;
+    }
+  };
+  auto affine = [&](const std::vector<P3>& verts, const std::array<qd, 3>& t) {
+    P3 x = verts[0];
+    for (size_t i = 1; i < verts.size(); ++i)
+      for (int c = 0; c < 3; ++c) x[c] += t[i - 1] * (verts[i][c] - verts[0][c]);
+    return x;
+  };
+  std::vector<std::array<qd, 3>> pts;
+  std::vector<qd> wts, lv;
+  // mass matrix (|det J| of the unit-simplex map: 4 tri, 8 tet)
+  std::vector<qd> M((size_t)ns * ns, 0);
+  unit_simplex_rule(D, nq, pts, wts);
+  const qd vdet = D == 2 ? 4 : 8;
+  for (size_t q = 0; q < pts.size(); ++q) {
+    lval(affine(V, pts[q]), lv);
+    for (int a = 0; a < ns; ++a)
+      for (int b = 0; b < ns; ++b) M[(size_t)a * ns + b] += wts[q] * vdet * lv[a] * lv[b];
+  }
+  // face lifts
+  std::vector<qd> L((size_t)ns * r.next, 0);
+  std::vector<std::vector<int>> fsp;
+  exps_total(D - 1, r.p, fsp);
+  const int nfp = (int)fsp.size();
+  unit_simplex_rule(D - 1, nq, pts, wts);
+  for (int f = 0; f < r.nfaces; ++f) {
+    std::vector<P3> fv;
+    for (int k = 0; k < D; ++k) fv.push_back(V[D == 2 ? TRI_F[f][k] : TET_F[f][k]]);
+    // Gram matrix of the edge vectors, face measure scale sqrt(det G)
+    qd G[2][2] = {{0, 0}, {0, 0}};
+    for (int a = 0; a < D - 1; ++a)
+      for (int b = 0; b < D - 1; ++b)
+        for (int c = 0; c < 3; ++c) G[a][b] += (fv[a + 1][c] - fv[0][c]) * (fv[b + 1][c] - fv[0][c]);
+    const qd gdet = D == 2 ? G[0][0] : G[0][0] * G[1][1] - G[0][1] * G[1][0];
+    const qd scale = sqrtq(gdet);
+    std::vector<int> nus;
+    for (int nu = 0; nu < r.next; ++nu)
+      if (r.ext_face[nu] == f) nus.push_back(nu);
+    if ((int)nus.size() != nfp) throw std::runtime_error("face point count != dim P_p(face)");
+    // face parameters of the face points: G t = T^T (x - x0)
+    std::vector<std::array<qd, 3>> tf;
+    for (int nu : nus) {
+      qd rhs[2] = {0, 0};
+      for (int a = 0; a < D - 1; ++a)
+        for (int c = 0; c < 3; ++c) rhs[a] += (fv[a + 1][c] - fv[0][c]) * (R.xext[nu][c] - fv[0][c]);
+      if (D == 2) tf.push_back({rhs[0] / G[0][0], 0, 0});
+      else
+        tf.push_back({(rhs[0] * G[1][1] - G[0][1] * rhs[1]) / gdet, (G[0][0] * rhs[1] - G[1][0] * rhs[0]) / gdet, 0});
+    }
+    auto tmono = [&](const std::vector<int>& e, const std::array<qd, 3>& t) {
+      qd v = 1;
+      for (size_t c = 0; c < e.size(); ++c)
+        for (int k = 0; k < e[c]; ++k) v *= t[c];
+      return v;
+    };
+    // face Lagrange basis: B = V^T (B[j][i] = t_j^e_i), Z = B^-1, ell_j = sum_i Z[i][j] t^e_i
+    std::vector<qd> B((size_t)nfp * nfp), Z((size_t)nfp * nfp, 0);
+    for (int j = 0; j < nfp; ++j)
+      for (int i = 0; i < nfp; ++i) B[(size_t)j * nfp + i] = tmono(fsp[i], tf[j]);
+    for (int i = 0; i < nfp; ++i) Z[(size_t)i * nfp + i] = 1;
+    gj_solve(B, nfp, Z, nfp);
+    for (size_t q = 0; q < pts.size(); ++q) {
+      lval(affine(fv, pts[q]), lv);
+      std::vector<qd> tm(nfp);
+      for (int i = 0; i < nfp; ++i) tm[i] = tmono(fsp[i], pts[q]);
+      for (int j = 0; j < nfp; ++j) {
+        qd ell = 0;
+        for (int i = 0; i < nfp; ++i) ell += Z[(size_t)i * nfp + j] * tm[i];
+        const qd w = wts[q] * scale * ell;
+        for (int a = 0; a < ns; ++a) L[(size_t)a * r.next + nus[j]] += w * lv[a];
+      }
+    }
+  }
+  gj_solve(M, ns, L, r.next);  // L <- M^-1 L
+  Mat Mc(ns, r.next);
+  for (int a = 0; a < ns; ++a)
+    for (int nu = 0; nu < r.next; ++nu) Mc(a, nu) = (double)L[(size_t)a * r.next + nu];
+  return Mc;
+}
+
 static Operators simplex_operators(int etype, int p) {
   RefQ R = build_ref_q(etype, p);
   Operators O;
@@ -755,7 +883,7 @@ static Operators simplex_operators(int etype, int p) {
   };
   interp(R.xext, O.M0);
   interp(R.xu, O.M12);
-  // FR data: solution-basis derivatives (FR-DG correction not built for simplices)
+  // FR data: solution-basis derivatives and the FR-DG correction (DG lifting)
   O.Dsol.assign(D, Mat(ns, ns));
   for (int d = 0; d < D; ++d)
     for (int s = 0; s < ns; ++s)
@@ -782,6 +910,7 @@ static Operators simplex_operators(int etype, int p) {
     }
     O.w[rr] = (double)v;
   }
+  O.Mc = simplex_dg_lift(R, Y, Ptot);
   finish_gradient_ops(O);
   return O;
 }
@@ -792,7 +921,6 @@ Operators build_operators(int etype, int p, int scheme) {
   else if (etype == TRI || etype == TET) O = simplex_operators(etype, p);
   else throw std::runtime_error("unknown element type");
   if (scheme < 0 || scheme > 2) throw std::runtime_error("unsupported scheme");
-  if (scheme == 2 && !etype_tensor(etype)) throw std::runtime_error("unsupported: FR-DG is built for tensor elements only");
   O.scheme = scheme;
   if (scheme == 1) O.Mc = O.M14;  // FR-SDRT: div g_nu = div psi_nu (l.407-413)
   return O;

@@ -176,14 +176,15 @@ def test_tgv_diagnostics_parity(name, N, state):
 
 FR_CASES = [(sch, n, N, st) for sch in ("frsdrt", "frdg")
             for (n, N, st) in [("c1", 5, 20), ("c3", 3, 3), ("c4", (3, 4, 3), 3), ("c4", 4, 2)]] + \
-           [("frsdrt", "c2", 5, 10), ("frsdrt", "c5", 3, 2), ("frsdrt", "c5", (3, 4, 3), 1)]
+           [(sch, n, N, st) for sch in ("frsdrt", "frdg")
+            for (n, N, st) in [("c2", 5, 10), ("c5", 3, 2), ("c5", (3, 4, 3), 1)]]
 
 
 @pytest.mark.parametrize("scheme,name,N,steps", FR_CASES)
 def test_fr_parity(scheme, name, N, steps):
-    """FR-SDRT / FR-DG (NEXT row N1) on the fused tensor kernels against the oracle's
-    FRResidual (pinned to the paper's FR-DG tau_MAX tables and the FR-SDRT == SDRT
-    equivalence): residual on a random state and RK4 steps of the configuration."""
+    """FR-SDRT / FR-DG (NEXT row N1) on the fused tensor and simplex kernels against the
+    oracle's FRResidual (pinned to the paper's FR-DG quad/tri tau_MAX tables and the
+    FR-SDRT == SDRT equivalence): residual on a random state and RK4 steps."""
     from oracle.fr import FRResidual
     from oracle.mesh import build_mesh
     from oracle.physics import Physics

@@ -93,13 +93,28 @@ def test_errors_are_reported(sdrt):
 
 
 def test_fr_schemes_build(sdrt):
-    """FR-SDRT builds for every element type, FR-DG for tensor elements only."""
-    for et in ("quad", "tri", "hex", "tet"):
-        o = sdrt.operators_build(et, 2, "frsdrt")
-        sdrt.operators_destroy(o)
-    for et in ("quad", "hex"):
-        o = sdrt.operators_build(et, 3, "frdg")
-        sdrt.operators_destroy(o)
-    with pytest.raises(sdrt.SdrtError) as e:
-        sdrt.operators_build("tet", 2, "frdg")
-    assert e.value.code == -2
+    """FR-SDRT and FR-DG build for every element type; the SDRT scheme has no "Mc"."""
+    for sch in ("frsdrt", "frdg"):
+        for et in ("quad", "tri", "hex", "tet"):
+            o = sdrt.operators_build(et, 2, sch)
+            assert sdrt.operators_get(o, "Mc").shape == sdrt.operators_get(o, "M14").shape
+            sdrt.operators_destroy(o)
+    o = sdrt.operators_build("tri", 2)
+    with pytest.raises(sdrt.SdrtError):
+        sdrt.operators_get(o, "Mc")
+    sdrt.operators_destroy(o)
+
+
+@pytest.mark.parametrize("etype,p", CASES)
+def test_fr_corrections_match_oracle(sdrt, etype, p):
+    """Mc of the library (collapsed Gauss quadrature in __float128 for the simplex DG
+    lifting) against the oracle (exact monomial integrals; Radau on tensor elements)."""
+    from oracle.fr import dg_correction_tensor, dg_lift
+    for sch, ref in (("frsdrt", build_operators(etype, p).M14),
+                     ("frdg", dg_correction_tensor(etype, p) if etype in ("quad", "hex") else dg_lift(etype, p))):
+        o = sdrt.operators_build(etype, p, sch)
+        try:
+            A = sdrt.operators_get(o, "Mc")
+            assert np.abs(A - ref).max() <= 1e-14 * np.abs(ref).max(), (sch, np.abs(A - ref).max())
+        finally:
+            sdrt.operators_destroy(o)
