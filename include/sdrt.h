@@ -158,11 +158,18 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
 sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream);
 /* Taylor-Green-vortex diagnostics of the device state d_U:
  * d_out (3 device doubles) = { <E*> = <rho v.v>, eps2 = 2 mu <S^d : S^d>,
- * eps3 = -<p div v> } with rho_inf = v_inf = L = t_c = 1, ensemble averages by the
- * solution-point quadrature sum_e detJ_e sum_r w_r / |Omega| (DESIGN.md reading), grad v
- * from the LDG gradient (l.295-302).  eps1 = -d<E*>/dt is left to the caller.  Single-rank
- * 3-D NS contexts on a fused path; SDRT_E_UNSUPPORTED otherwise.  Enqueued on stream. */
+ * eps3 = -<p div v> } with rho_inf = v_inf = L = t_c = 1.  Ensemble averages by the
+ * context's rule (sdrt_diagnostics_rule): by default the paper's degree-10 quadrature
+ * (l.2075) of the solution polynomial u_h and of the LDG-gradient polynomial Q_h
+ * (l.295-302), grad v by the chain rule (DESIGN.md readings).  eps1 = -d<E*>/dt is left
+ * to the caller.  Single-rank 3-D NS contexts on a fused path; SDRT_E_UNSUPPORTED
+ * otherwise.  Enqueued on stream. */
 sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void* stream);
+/* Quadrature of sdrt_diagnostics: degree 1..10 = a rule exact to that degree on the
+ * reference element (Gauss-Legendre products on quad/hex, collapsed Gauss-Legendre
+ * products on tri/tet; default 10), 0 = the solution points with weights w_r = int l_r.
+ * Synchronous host->device upload.  SDRT_E_INVALID_ARG outside 0..10. */
+sdrt_status sdrt_diagnostics_rule(sdrt_ctx* c, int degree);
 /* Per-kernel device timing (CUDA events recorded on the launching stream around each
  * kernel) for measurement: enable, run, then read per-kernel totals.  names receives
  * max_tags NUL-terminated strings of 64 bytes each (may be NULL); ms/counts get the

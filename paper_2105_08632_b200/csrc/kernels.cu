@@ -344,7 +344,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_tiles, off_diag, total;
+      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_tiles, off_diag, off_cub, total;
   size_t ops_bytes;
 };
 
@@ -413,6 +413,9 @@ struct sdrt_ctx {
   double* d_part = nullptr;  // diagnostics partial sums
   double* d_w = nullptr;     // solution-point quadrature weights w_r (App. B reading of l.2052)
   double diag_vol = 0.0;     // sum_e detJ_e sum_r w_r
+  double* d_cub = nullptr;   // cubature of the diagnostics: B [ncub][nsol], then weights [ncub]
+  int ncub = 0;              // 0: solution-point quadrature
+  int cub_cap = 0;           // points reserved (the degree-10 rule)
   const int* d_tiles = nullptr;  // [n_int interior tiles][n_bnd boundary tiles]
   double* Tu[2] = {nullptr, nullptr};
   double* Tg = nullptr;
@@ -510,6 +513,12 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
 
 static int nvars(int eq, int D) { return (eq == SDRT_EQ_LINADV || eq == SDRT_EQ_LINADVDIFF) ? 1 : D + 2; }
 
+// points of the diagnostics cubature exact to `degree` (refel.cpp cubature_interp)
+static int cub_points(int etype, int D, int degree) {
+  const int n = etype_tensor(etype) ? degree / 2 + 1 : (degree + D - 1) / 2 + 1;
+  return D == 2 ? n * n : n * n * n;
+}
+
 static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph, std::vector<OpHost>* packed) {
   const RefElement& r = O.ref;
   int D = m.nd, NV = nvars(ph->eq, D);
@@ -562,9 +571,28 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   // TGV diagnostics: per-tile partial sums (3 per tile of >= 8 elements) + weights w
   p.off_diag = o;
   o += align256((3 * ((size_t)m.K / 8 + 2) + r.nsol + 8) * sizeof(double));
+  // degree-10 cubature of the diagnostics (l.2075): interpolation matrix + weights
+  p.off_cub = o;
+  o += align256((size_t)cub_points(r.etype, r.nd, 10) * (r.nsol + 1) * sizeof(double));
   p.total = o;
   if (packed) *packed = pk;
   return p;
+}
+
+// Diagnostics rule: degree 0 = the solution points (weights w), else the cubature exact
+// to `degree` (refel.cpp cubature_interp) uploaded into the reserved area (synchronous).
+static void set_diag_rule(sdrt_ctx* c, int etype, int degree) {
+  if (degree == 0) {
+    c->ncub = 0;
+    return;
+  }
+  std::vector<double> w;
+  Mat B;
+  cubature_interp(etype, c->p, degree, w, B);
+  if ((int)w.size() > c->cub_cap || B.cols != c->nsol) throw std::runtime_error("cubature larger than reserved");
+  CUDA_OK(cudaMemcpy(c->d_cub, B.a.data(), B.a.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_OK(cudaMemcpy(c->d_cub + B.a.size(), w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
+  c->ncub = (int)w.size();
 }
 
 extern "C" {
@@ -830,6 +858,10 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       for (int64_t e = 0; e < m.K; ++e) sd += m.detJ[e % m.nsub];
       c->diag_vol = sw * sd;
     }
+    c->d_cub = (double*)(base + p.off_cub);
+    c->cub_cap = cub_points(r.etype, r.nd, 10);
+    CUDA_OK(cudaStreamSynchronize(st));
+    set_diag_rule(c, r.etype, 10);
     // interior / boundary tile lists for the overlapped multi-rank stage:
     // a tile is interior if none of its elements lies in a pattern layer next to a
     // partition face (ghost neighbours only occur there)
@@ -1242,6 +1274,17 @@ sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int 
   })
 }
 
+sdrt_status sdrt_diagnostics_rule(sdrt_ctx* c, int degree) {
+  if (!c || degree < 0 || degree > 10) {
+    set_error("invalid argument: degree must be 0 (solution points) or 1..10");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    set_diag_rule(c, c->etype, degree);
+    return SDRT_OK;
+  })
+}
+
 sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void* stream) {
   if (!c || !d_U || !d_out) {
     set_error("invalid argument");
@@ -1260,14 +1303,17 @@ sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void
       TensorBufs b{};
       b.Uin = d_U;
       b.Tu = c->Tu[c->cur];
-      tensor_launch_diag(c->nd, c->p, c->tg, c->line, c->ph, &c->tma, b, c->d_w, c->d_part, st);
+      tensor_launch_diag(c->nd, c->p, c->tg, c->line, c->ph, &c->tma, b, c->ncub ? c->d_cub + (size_t)c->ncub * c->nsol : c->d_w,
+                         c->ncub ? c->d_cub : nullptr, c->ncub, c->d_part, st);
       ntile = (c->g.K + tensor_tile_width(c->nd, c->p, c->eq) - 1) / tensor_tile_width(c->nd, c->p, c->eq);
     } else {
       sfused_traces(c, d_U, st);
       SimplexBufs b{};
       b.Uin = d_U;
       b.Tu = c->Tu[c->cur];
-      simplex_launch_diag(c->nd, c->p, c->g, c->sops, c->ph, &c->stma, b, c->d_w, c->d_part, st);
+      simplex_launch_diag(c->nd, c->p, c->g, c->sops, c->ph, &c->stma, b,
+                          c->ncub ? c->d_cub + (size_t)c->ncub * c->nsol : c->d_w, c->ncub ? c->d_cub : nullptr, c->ncub,
+                          c->d_part, st);
       ntile = (c->g.K + 7) / 8;
     }
     k_diag_final<<<1, 256, 0, st>>>(c->d_part, ntile, 1.0 / c->diag_vol, c->ph.mu, d_out);

@@ -915,6 +915,71 @@ static Operators simplex_operators(int etype, int p) {
   return O;
 }
 
+// Degree-`degree` cubature of the reference element (TGV ensemble averages, l.2075) and
+// the solution-basis interpolation B(q, r) = l_r(x_q).  Tensor: Gauss-Legendre products
+// with degree/2 + 1 points per axis; simplex: collapsed (Duffy) Gauss-Legendre products
+// with (degree + D - 1)/2 + 1 points per direction, mapped affinely (|det| 4 tri, 8 tet).
+void cubature_interp(int etype, int p, int degree, std::vector<double>& w, Mat& B) {
+  RefQ R = build_ref_q(etype, p);
+  const RefElement& r = R.r;
+  const int D = r.nd, ns = r.nsol;
+  std::vector<P3> xq;
+  std::vector<qd> wq;
+  if (etype_tensor(etype)) {
+    std::vector<qd> g, gw;
+    gauss_legendre(degree / 2 + 1, g, gw);
+    const int nq = (int)g.size();
+    const int tot = D == 2 ? nq * nq : nq * nq * nq;
+    for (int q = 0; q < tot; ++q) {
+      const int i = q % nq, j = (q / nq) % nq, k = q / (nq * nq);
+      xq.push_back({g[i], g[j], D == 3 ? g[k] : (qd)0});
+      wq.push_back(gw[i] * gw[j] * (D == 3 ? gw[k] : (qd)1));
+    }
+    std::vector<qd> gs, gsw;
+    gauss_legendre(p + 1, gs, gsw);
+    const int n = p + 1;
+    B = Mat((int)xq.size(), ns);
+    for (size_t q = 0; q < xq.size(); ++q)
+      for (int s = 0; s < ns; ++s) {
+        qd v = 1;
+        int t = s;
+        for (int c = 0; c < D; ++c, t /= n) v *= lag(gs, t % n, xq[q][c]);
+        B((int)q, s) = (double)v;
+      }
+  } else {
+    std::vector<std::array<qd, 3>> tp;
+    unit_simplex_rule(D, (degree + D - 1) / 2 + 1, tp, wq);
+    std::vector<P3> V;
+    if (D == 2)
+      for (auto& v : TRI_V) V.push_back({(qd)v[0], (qd)v[1], 0});
+    else
+      for (auto& v : TET_V) V.push_back({(qd)v[0], (qd)v[1], (qd)v[2]});
+    for (size_t q = 0; q < tp.size(); ++q) {
+      P3 x = V[0];
+      for (int i = 0; i < D; ++i)
+        for (int c = 0; c < 3; ++c) x[c] += tp[q][i] * (V[i + 1][c] - V[0][c]);
+      xq.push_back(x);
+      wq[q] *= D == 2 ? 4 : 8;
+    }
+    std::vector<std::vector<int>> Ptot;
+    exps_total(D, p, Ptot);
+    std::vector<qd> A((size_t)ns * ns), Y((size_t)ns * ns, 0);
+    for (int k = 0; k < ns; ++k)
+      for (int s = 0; s < ns; ++s) A[(size_t)s * ns + k] = mono(Ptot[k], R.xsol[s]);
+    for (int i = 0; i < ns; ++i) Y[(size_t)i * ns + i] = 1;
+    gj_solve(A, ns, Y, ns);  // l_r = sum_k Y[k][r] phi_k
+    B = Mat((int)xq.size(), ns);
+    for (size_t q = 0; q < xq.size(); ++q)
+      for (int rr = 0; rr < ns; ++rr) {
+        qd v = 0;
+        for (int k = 0; k < ns; ++k) v += Y[(size_t)k * ns + rr] * mono(Ptot[k], xq[q]);
+        B((int)q, rr) = (double)v;
+      }
+  }
+  w.assign(wq.size(), 0.0);
+  for (size_t q = 0; q < wq.size(); ++q) w[q] = (double)wq[q];
+}
+
 Operators build_operators(int etype, int p, int scheme) {
   Operators O;
   if (etype_tensor(etype)) O = tensor_operators(etype, p);

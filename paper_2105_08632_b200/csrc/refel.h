@@ -50,6 +50,10 @@ struct Operators {
 RefElement build_reference(int etype, int p);
 Operators build_operators(int etype, int p, int scheme = 0);
 
+// Cubature exact to `degree` on the reference element (weights w) and the solution-basis
+// interpolation B(q, r) = l_r(x_q) (TGV diagnostics, l.2075).
+void cubature_interp(int etype, int p, int degree, std::vector<double>& w, Mat& B);
+
 // Reference vertices of the simplices (x~ of vertex k), used by mesh code.
 void simplex_ref_vertices(int etype, std::vector<std::array<double, 3>>& V);
 

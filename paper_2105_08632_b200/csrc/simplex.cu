@@ -30,6 +30,7 @@
 #include "simplex.cuh"
 #include "rk.cuh"
 #include "tma.cuh"
+#include "diag.cuh"
 
 namespace sdrt {
 
@@ -827,7 +828,8 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
 // LDG gradient (the prologue of kernel A) by the chain rule (reading O20).
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256) ks_diag(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, const double* w,
-                                               double* part, const __grid_constant__ STileMaps tm) {
+                                               const double* Bq, int nq, double* part,
+                                               const __grid_constant__ STileMaps tm) {
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
   constexpr int NV = Ph::NV, NT = 256;
@@ -861,42 +863,8 @@ __global__ void __launch_bounds__(256) ks_diag(GeomDev g, SimplexOps O, PhysDev 
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
-  if constexpr (NV == D + 2) {
-    for (int item = threadIdx.x; item < S::nsol * E; item += NT) {
-      const int el = item % E, sp = item / E;
-      if (e0 + el >= g.K) continue;
-      const int s = sNb[D + 1][el];
-      const double rho = sU[(sp * NV) * E + el];
-      double v[D], vv = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        v[i] = sU[(sp * NV + 1 + i) * E + el] / rho;
-        vv += v[i] * v[i];
-      }
-      const double pr = (ph.gamma - 1.0) * (sU[(sp * NV + D + 1) * E + el] - 0.5 * rho * vv);
-      double dv[D][D];  // dv[j][i] = d v_i / d x_j
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-          dv[j][i] = (sQ[((j * S::nsol + sp) * NV + 1 + i) * E + el] - v[i] * sQ[((j * S::nsol + sp) * NV) * E + el]) / rho;
-      double div = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) div += dv[i][i];
-      double ss = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const double sij = 0.5 * (dv[j][i] + dv[i][j]) - (i == j ? div / 3.0 : 0.0);
-          ss += sij * sij;
-        }
-      const double wr = w[sp] * g.detJ[s];
-      acc[0] += wr * rho * vv;
-      acc[1] += wr * ss;
-      acc[2] += wr * pr * div;
-    }
-  }
+  if constexpr (NV == D + 2)
+    tgv_tile<D, NV, E, S::nsol>(ph, sU, sQ, w, Bq, nq, e0, g.K, [&](int el) { return g.detJ[sNb[D + 1][el]]; }, acc);
 #pragma unroll
   for (int k = 0; k < 3; ++k) red[k * NT + threadIdx.x] = acc[k];
   __syncthreads();
@@ -1022,13 +990,14 @@ int simplex_tile_width(int D, int P, int eq) {
 }
 
 void simplex_launch_diag(int D, int P, const GeomDev& g, const SimplexOps& O, const PhysDev& ph, SimplexTma* tma,
-                         const SimplexBufs& b, const double* w, double* part, cudaStream_t st) {
+                         const SimplexBufs& b, const double* w, const double* Bq, int nq, double* part,
+                         cudaStream_t st) {
   if (D != 3 || P < 1 || P > 3) throw std::runtime_error("unsupported: TGV diagnostics need a 3-D NS context");
   auto launch = [&](auto kern, size_t per_el) {
     const size_t sm = per_el * 8 * sizeof(double);
     sset_smem((const void*)kern, sm);
     const unsigned grid = (unsigned)((g.K + 7) / 8);
-    kern<<<grid, 256, sm, st>>>(g, O, ph, b, w, part, smaps(tma, b, b.Uin, false));
+    kern<<<grid, 256, sm, st>>>(g, O, ph, b, w, Bq, nq, part, smaps(tma, b, b.Uin, false));
   };
   // regions per element: U, U_ext, U_u, C, Q  (N_V = 5)
   auto per_el = [](int nsol, int next, int nu) { return (size_t)(4 * nsol + 2 * next + nu) * 5; };

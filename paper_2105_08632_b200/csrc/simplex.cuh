@@ -57,7 +57,8 @@ struct SimplexTma {
 bool simplex_supported(int D, int P, int eq);
 // TGV diagnostics partial sums (3 per tile of 8 elements); NS only
 void simplex_launch_diag(int D, int P, const GeomDev& g, const SimplexOps& O, const PhysDev& ph, SimplexTma* tma,
-                         const SimplexBufs& b, const double* w, double* part, cudaStream_t st);
+                         const SimplexBufs& b, const double* w, const double* Bq, int nq, double* part,
+                         cudaStream_t st);
 int simplex_tile_width(int D, int P, int eq);
 void simplex_tma_init(SimplexTma* t, int D, int P, int eq, int64_t Kp);
 void simplex_launch_traces(int D, int P, int eq, const GeomDev& g, const SimplexOps& O, SimplexTma* tma,

@@ -32,6 +32,7 @@
 #include "tensor.cuh"
 #include "rk.cuh"
 #include "tma.cuh"
+#include "diag.cuh"
 
 namespace sdrt {
 
@@ -753,7 +754,8 @@ __device__ __forceinline__ void block_sum3(double (&a)[3], double* red, double* 
 
 template <int D, int P, int EQ, int E, int NT, int NI>
 __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, const double* w,
-                                              double* part, const __grid_constant__ TileMaps tm) {
+                                              const double* Bq, int nq, double* part,
+                                              const __grid_constant__ TileMaps tm) {
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, NS = T::NS;
@@ -781,41 +783,8 @@ __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph
   }
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
-  if constexpr (NV == D + 2) {
-    for (int item = threadIdx.x; item < NS * E; item += NT) {
-      const int el = item % E, sp = item / E;
-      if (e0 + el >= g.K) continue;
-      const double rho = sU[(sp * NV) * E + el];
-      double v[D], vv = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        v[i] = sU[(sp * NV + 1 + i) * E + el] / rho;
-        vv += v[i] * v[i];
-      }
-      const double pr = (ph.gamma - 1.0) * (sU[(sp * NV + D + 1) * E + el] - 0.5 * rho * vv);
-      double dv[D][D];  // dv[j][i] = d v_i / d x_j
-#pragma unroll
-      for (int j = 0; j < D; ++j)
-#pragma unroll
-        for (int i = 0; i < D; ++i)
-          dv[j][i] = (sQ[((j * NS + sp) * NV + 1 + i) * E + el] - v[i] * sQ[((j * NS + sp) * NV) * E + el]) / rho;
-      double div = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) div += dv[i][i];
-      double ss = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-          const double sij = 0.5 * (dv[j][i] + dv[i][j]) - (i == j ? div / 3.0 : 0.0);
-          ss += sij * sij;
-        }
-      const double wr = w[sp] * g.detJ;
-      acc[0] += wr * rho * vv;
-      acc[1] += wr * ss;
-      acc[2] += wr * pr * div;
-    }
-  }
+  if constexpr (NV == D + 2)
+    tgv_tile<D, NV, E, NS>(ph, sU, sQ, w, Bq, nq, e0, g.K, [&](int) { return g.detJ; }, acc);
   block_sum3<NT>(acc, red, part + 3 * blockIdx.x);
 }
 
@@ -928,13 +897,13 @@ static void run_traces(const TensorGeom& g, const Line1D& L, TensorTma* tma, con
 
 template <int D, int P, int EQ>
 static void run_diag(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
-                     const double* w, double* part, cudaStream_t st) {
+                     const double* w, const double* Bq, int nq, double* part, cudaStream_t st) {
   using C = TCfg<D, P, EQ>;
   const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
   auto k = L.fr ? kt_diag<D, P, EQ, C::E, 256, P + 1> : kt_diag<D, P, EQ, C::E, 256, P>;
   const size_t sm = C::TILE * (1 + D);
   set_smem<D, P, EQ>((const void*)k, sm);
-  k<<<grid, 256, sm, st>>>(g, L, ph, b, w, part, maps_for(tma, b, false));
+  k<<<grid, 256, sm, st>>>(g, L, ph, b, w, Bq, nq, part, maps_for(tma, b, false));
 }
 
 template <int D, int P, int EQ>
@@ -1038,13 +1007,14 @@ void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D&
 }
 
 void tensor_launch_diag(int D, int P, const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
-                        const TensorBufs& b, const double* w, double* part, cudaStream_t st) {
+                        const TensorBufs& b, const double* w, const double* Bq, int nq, double* part,
+                        cudaStream_t st) {
   if (D != 3) throw std::runtime_error("unsupported: TGV diagnostics need a 3-D NS context");
   switch (P) {
-    case 1: run_diag<3, 1, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
-    case 2: run_diag<3, 2, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
-    case 3: run_diag<3, 3, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
-    default: run_diag<3, 4, EQ_NS>(g, L, ph, tma, b, w, part, st); break;
+    case 1: run_diag<3, 1, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
+    case 2: run_diag<3, 2, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
+    case 3: run_diag<3, 3, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
+    default: run_diag<3, 4, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
   }
 }
 

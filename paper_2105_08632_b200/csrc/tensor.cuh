@@ -81,6 +81,7 @@ bool tensor_supported(int D, int P, int eq);
 // TGV diagnostics partial sums (3 per tile: rho v.v, S^d:S^d, p div v, solution-point
 // weighted); NS only
 void tensor_launch_diag(int D, int P, const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
-                        const TensorBufs& b, const double* w, double* part, cudaStream_t st);
+                        const TensorBufs& b, const double* w, const double* Bq, int nq, double* part,
+                        cudaStream_t st);
 
 }  // namespace sdrt

@@ -71,6 +71,7 @@ lib.sdrt_residual.argtypes = [_vp, _vp, _vp, _vp]
 lib.sdrt_rk_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
 lib.sdrt_rk54_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
 lib.sdrt_diagnostics.argtypes = [_vp, _vp, _vp, _vp]
+lib.sdrt_diagnostics_rule.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_mesh_set_halo.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_mesh_halo_lists.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
 lib.sdrt_mesh_neighbor.argtypes = [_vp, ctypes.c_int64, ctypes.c_int, _vp, _vp]
@@ -288,6 +289,10 @@ RK54_STAGE0 = 10  # staged-API stage code of RK54 stage 0 (include/sdrt.h)
 
 def diagnostics(ctx, U_ptr, out_ptr, stream):
     _check(lib.sdrt_diagnostics(ctx, _vp(U_ptr), _vp(out_ptr), _vp(stream)))
+
+
+def diagnostics_rule(ctx, degree):
+    _check(lib.sdrt_diagnostics_rule(ctx, int(degree)))
 
 
 def stage_grad(ctx, U_ptr, stage, stream):

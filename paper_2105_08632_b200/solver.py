@@ -73,8 +73,12 @@ class Solver:
                        torch.cuda.current_stream(self.device).cuda_stream)
         return U
 
-    def diagnostics(self, U):
-        """TGV ensemble averages (<E*>, eps2, eps3), PAPER.md l.2052-2080 (3-D NS)."""
+    def diagnostics(self, U, degree=10):
+        """TGV ensemble averages (<E*>, eps2, eps3), PAPER.md l.2052-2080 (3-D NS), by the
+        quadrature exact to `degree` (the paper's 10, l.2075; 0 = solution points)."""
+        if degree != getattr(self, "_diag_degree", 10):
+            sdrt.diagnostics_rule(self.ctx, degree)
+        self._diag_degree = degree
         out = torch.empty(3, dtype=torch.float64, device=self.device)
         sdrt.diagnostics(self.ctx, U.data_ptr(), out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
         return out.cpu().numpy()

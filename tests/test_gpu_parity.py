@@ -162,14 +162,16 @@ def test_rk54_parity(name, N, steps):
 
 @pytest.mark.parametrize("name,N", [("c4", 4), ("c5", 3)])
 @pytest.mark.parametrize("state", ["ic", "random"])
-def test_tgv_diagnostics_parity(name, N, state):
-    """sdrt_diagnostics (NEXT row N4) against the oracle's tgv_diagnostics."""
+@pytest.mark.parametrize("degree", [10, 0, 6])
+def test_tgv_diagnostics_parity(name, N, state, degree):
+    """sdrt_diagnostics (NEXT row N4) against the oracle's tgv_diagnostics: the paper's
+    degree-10 quadrature (default), a degree-6 rule and the solution-point sums (0)."""
     from oracle.diagnostics import tgv_diagnostics
     cfg = CONFIGS[name]
     m, R, S = _pair(cfg, N)
     U = initial_state(cfg, m.sol_coords()) if state == "ic" else random_state(cfg, R.ops.nsol, m.K, seed=3, amp=0.2)
-    ref = np.array(tgv_diagnostics(R, U))
-    got = S.diagnostics(S.to_device(U))
+    ref = np.array(tgv_diagnostics(R, U, degree or None))
+    got = S.diagnostics(S.to_device(U), degree)
     scale = np.array([abs(ref[0]), abs(ref[1]), max(abs(ref[1]), abs(ref[2]))])
     assert (np.abs(got - ref) <= 1e-11 * scale).all(), (got, ref)
 
