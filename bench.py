@@ -372,20 +372,23 @@ def main():
 
     # ---------------------------------------------------------------- e2e (host buffers)
     # Every step: host->device copy of the step's input state from pinned memory,
-    # sdrt_rk_step, device->host copy of the new state.  Steps alternate between two
-    # library contexts on two CUDA streams (double buffering), so one step's copies
-    # overlap the other's kernels; the timed region spans all of them on the device.
+    # sdrt_rk_step, device->host copy of the new state.  Steps rotate over three library
+    # contexts on three CUDA streams (triple buffering): a stream's chain H2D -> step ->
+    # D2H then covers three steps, so the copies of neighbouring steps overlap this one's
+    # kernels (with two buffers the chain of 2 copies + 1 step per two steps bounds the
+    # rate once a copy takes more than half a step).  The timed region spans all of them.
+    NBUF = 3 if world == 1 else 1
     pin = torch.empty(S.shape, dtype=torch.float64).pin_memory()
     pin.copy_(U.cpu())
-    outs = [torch.empty_like(pin).pin_memory(), torch.empty_like(pin).pin_memory()]
+    outs = [torch.empty_like(pin).pin_memory() for _ in range(NBUF)]
+    extra = []
     if world > 1:  # ranks exchange halos in step order: one context, one stream
-        S2 = None
-        solvers, bufs = [S, S], [U, U]
+        solvers, bufs = [S], [U]
     else:
-        S2 = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, scheme=args.scheme,
-                    **cfg.physics_kwargs())
-        solvers, bufs = [S, S2], [U, torch.empty_like(U)]
-    side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        extra = [Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, scheme=args.scheme,
+                        **cfg.physics_kwargs()) for _ in range(NBUF - 1)]
+        solvers, bufs = [S] + extra, [U] + [torch.empty_like(U) for _ in range(NBUF - 1)]
+    side = [torch.cuda.Stream(dev) for _ in range(NBUF)]
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -394,7 +397,7 @@ def main():
     for sd in side:
         sd.wait_stream(stream)
     for i in range(args.steps):
-        k = i % 2 if world == 1 else 0
+        k = i % NBUF
         with torch.cuda.stream(side[k]):
             bufs[k].copy_(pin, non_blocking=True)
             step_fn(solvers[k])(bufs[k], cfg.dt, 1)
@@ -407,9 +410,9 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = total_dof_stages / (float(te[0]) * 1e-3) / 1e9
-    e2e_ok = bool(torch.isfinite(torch.from_numpy(outs[(args.steps - 1) % 2].numpy()[:, :, :K])).all())
-    if S2 is not None:
-        S2.close()
+    e2e_ok = bool(torch.isfinite(torch.from_numpy(outs[(args.steps - 1) % NBUF].numpy()[:, :, :K])).all())
+    for s2 in extra:
+        s2.close()
     state_bytes = U.numel() * 8
 
     # ---------------------------------------------------------------- roofline
