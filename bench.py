@@ -480,7 +480,7 @@ def main():
                "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,
                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                        "d2h_bytes_per_step": state_bytes, "result_finite": e2e_ok,
-                       "pipeline": "2 contexts x 2 streams, copies of one step overlap the other's kernels"},
+                       "pipeline": f"{NBUF} contexts x {NBUF} streams, host copies of neighbouring steps overlap each step's kernels"},
                "gpu_launches": launches, "clocks": clk, "kernel_ms": {k: v[0] for k, v in ktimes.items()},
                "ms_per_step_no_events": ms_clean_max / args.steps, "state_finite": finite,
                "finite_trace": dbg}
