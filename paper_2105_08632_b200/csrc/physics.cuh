@@ -113,6 +113,76 @@ struct Phys {
     }
   }
 
+  // Axis-aligned forms for w = wd e_D0 (tensor elements: B7's single normal component,
+  // l.2927-2932): the same fluxes touching only the entries that component needs (for NS
+  // the gradient entries d rho, d(rho v_D0), d(rho v_j) / dx_j of the tangential axes
+  // and all entries along D0), so unused gradient interpolations are dead code.
+  template <int D0>
+  static __device__ __forceinline__ void conv_axis(const PhysDev& ph, const double* u, double wd, double* out) {
+    if constexpr (NV == 1) {
+      out[0] = ph.c[D0] * wd * u[0];
+    } else {
+      const double rho = u[0];
+      const double ir = 1.0 / rho;
+      double vv = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) vv += u[1 + d] * ir * u[1 + d];
+      const double vw = u[1 + D0] * ir * wd;
+      const double p = (ph.gamma - 1.0) * (u[D + 1] - 0.5 * vv);
+      out[0] = rho * vw;
+#pragma unroll
+      for (int i = 0; i < D; ++i) out[1 + i] = i == D0 ? u[1 + i] * vw + p * wd : u[1 + i] * vw;
+      out[D + 1] = (u[D + 1] + p) * vw;
+    }
+  }
+
+  template <int D0>
+  static __device__ __forceinline__ void visc_axis(const PhysDev& ph, const double* u, const double* q, double wd,
+                                                   double* out) {
+    if constexpr (EQ == EQ_LINADVDIFF) {
+      out[0] = -ph.mu * (wd * q[D0]);
+    } else if constexpr (EQ == EQ_NS) {
+      const double g = ph.gamma;
+      const double rho = u[0];
+      const double ir = 1.0 / rho;
+      double v[D], vv = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        v[i] = u[1 + i] * ir;
+        vv += v[i] * v[i];
+      }
+      const double p = (g - 1.0) * (u[D + 1] - 0.5 * rho * vv);
+      // dvn[i] = d v_i / dx_D0, dvt[j] = d v_D0 / dx_j, div from d v_j / dx_j
+      double dvn[D], dvt[D], div = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) dvn[i] = (q[D0 * NV + 1 + i] - v[i] * q[D0 * NV]) * ir;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        dvt[j] = j == D0 ? dvn[D0] : (q[j * NV + 1 + D0] - v[D0] * q[j * NV]) * ir;
+        div += j == D0 ? dvn[D0] : (q[j * NV + 1 + j] - v[j] * q[j * NV]) * ir;
+      }
+      const double kappa = ph.mu * g / ((g - 1.0) * ph.Pr);
+      out[0] = 0.0;
+      double tv = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const double tau = ph.mu * (dvn[i] + dvt[i] - (i == D0 ? (2.0 / 3.0) * div : 0.0));
+        const double s = tau * wd;
+        out[1 + i] = -s;
+        tv += s * v[i];
+      }
+      double vdv = 0.0;
+#pragma unroll
+      for (int i = 0; i < D; ++i) vdv += v[i] * dvn[i];
+      const double dp = (g - 1.0) * (q[D0 * NV + D + 1] - 0.5 * vv * q[D0 * NV] - rho * vdv);
+      const double dT = (dp - p * ir * q[D0 * NV]) * ir;
+      out[D + 1] = -kappa * (dT * wd) - tv;
+    } else {
+#pragma unroll
+      for (int a = 0; a < NV; ++a) out[a] = 0.0;
+    }
+  }
+
   // convective common flux (upwind LF for linear, Rusanov otherwise) along n
   static __device__ __forceinline__ void conv_common(const PhysDev& ph, const double* uL, const double* uR,
                                                      const double* n, double* F) {

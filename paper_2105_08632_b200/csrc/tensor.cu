@@ -311,11 +311,8 @@ __device__ __forceinline__ void publish_g(const TensorGeom& g, const Line1D& L, 
       q[dd * NV + v] = s;
     }
   }
-  double nL[D];
-#pragma unroll
-  for (int k2 = 0; k2 < D; ++k2) nL[k2] = (k2 == d) ? 1.0 : 0.0;  // canonical (left) normal +e_d
   double gv[NV];
-  Ph::visc_dir(ph, u, q, nL, gv);
+  Ph::template visc_axis<d>(ph, u, q, 1.0, gv);  // canonical (left) normal +e_d
 #pragma unroll
   for (int v = 0; v < NV; ++v) Tg[((int64_t)ext * NV + v) * g.Kt + e] = gv[v];
 }
@@ -353,12 +350,10 @@ __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D&
       }
     }
   }
-  double w[D], fc[NV], fv[NV];
+  double fc[NV], fv[NV];
   const double wf = g.detJ * g.jinv[d];
-#pragma unroll
-  for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
-  Ph::conv_dir(ph, ua, w, fc);
-  Ph::visc_dir(ph, ua, qa, w, fv);
+  Ph::template conv_axis<d>(ph, ua, wf, fc);
+  Ph::template visc_axis<d>(ph, ua, qa, wf, fv);
 #pragma unroll
   for (int v = 0; v < NV; ++v) sF[((t * NI + a) * NV + v) * E + el] = fc[v] + fv[v];
 }
@@ -583,10 +578,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
           ua[v] = s;
         }
       }
-      double w[D], f[NV];
-#pragma unroll
-      for (int k = 0; k < D; ++k) w[k] = (k == d) ? wf : 0.0;
-      Ph::conv_dir(ph, ua, w, f);
+      double f[NV];
+      Ph::template conv_axis<d>(ph, ua, wf, f);
 #pragma unroll
       for (int v = 0; v < NV; ++v) sF[((t * NF + a + 1) * NV + v) * E + el] = f[v];
     }
