@@ -88,10 +88,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #define SDRT_SA_MINB 3
 #endif
 #ifndef SDRT_SB_MINB
-#define SDRT_SB_MINB 5
+#define SDRT_SB_MINB 4
 #endif
 #ifndef SDRT_SA_NT
 #define SDRT_SA_NT 256
+#endif
+#ifndef SDRT_SB_PF
+#define SDRT_SB_PF 1
 #endif
 #ifndef SDRT_SB_NT
 #define SDRT_SB_NT 160
@@ -338,6 +341,53 @@ struct NbGather {
         const double own = sUe[(rho * NV + v) * E + el];
         const double uL = left ? own : nb[k][v], uR = left ? nb[k][v] : own;
         sC[(rho * NV + v) * E + el] = wl * uL + wr * uR;
+      }
+    }
+  }
+};
+
+// Kernel B's face gathers issued ahead (register prefetch, SDRT_SB_PF): the
+// neighbour's U trace and the LDG-weighted published viscous traces g of each of the
+// thread's external points, loaded before the tile wait so the latency overlaps it.
+template <int D, int P, int NV, int E, int NT, bool VISC>
+struct FluxGather {
+  using S = SDims<D, P>;
+  static constexpr int ITEMS = S::next * E;
+  static constexpr int CI = (ITEMS + NT - 1) / NT;
+  double un[CI][NV];
+  double gs[VISC ? CI : 1][NV];
+
+  __device__ __forceinline__ void load(const GeomDev& g, const PhysDev& ph, const double* __restrict__ Tu,
+                                       const double* __restrict__ Tg, const int (*sNb)[E], int64_t e0) {
+    const int Kp = (int)g.Kt;
+    const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+#pragma unroll
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * NT;
+      const int el = item % E, rho = item / E;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        un[k][v] = 0.0;
+        if constexpr (VISC) gs[k][v] = 0.0;
+      }
+      if (item >= ITEMS || e0 + el >= g.K) continue;
+      const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
+      const int m = sNb[f][el];
+      const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) un[k][v] = Tu[((int64_t)rho2 * Kp + m) * NV + v];
+      if constexpr (VISC) {
+        const bool left = g.left[s][f];
+        const int64_t e = e0 + el;
+        const int rL = left ? rho : rho2, rR = left ? rho2 : rho;
+        const int64_t eL = left ? e : m, eR = left ? m : e;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double a = 0.0;
+          if (wl != 0.0) a = wl * Tg[((int64_t)rL * Kp + eL) * NV + v];
+          if (wr != 0.0) a = fma(wr, Tg[((int64_t)rR * Kp + eR) * NV + v], a);
+          gs[k][v] = a;
+        }
       }
     }
   }
@@ -679,6 +729,10 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
   SPH(1, 0)
+#if SDRT_SB_PF
+  FluxGather<D, P, NV, E, SDRT_SB_NT, Ph::VISC> fg;
+  fg.load(g, ph, b.Tu, b.Tg, sNb, e0);
+#endif
   mbar_wait(&bar[0], 0);
   // own traces (and, inviscid, U_u)
   const SOpF none{0, 0, 0, 0, nullptr, nullptr};
@@ -689,35 +743,44 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   // common fluxes D~ = +/- s F at external points, in place over the own traces
   const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
   const int Kp = (int)g.Kt;  // trace row stride
-  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
+  auto face_flux = [&](int item, const double* unp, const double* gsp) {
     const int el = item % E, rho = item / E;
     const int64_t e = e0 + el;
     if (e >= g.K) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) sUe[(rho * NV + v) * E + el] = 0.0;
-      continue;
+      return;
     }
     const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
     const int m = sNb[f][el];
-    const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
     const bool left = g.left[s][f];
     double uo[NV], un[NV], gsum[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
-      un[v] = b.Tu[((int64_t)rho2 * Kp + m) * NV + v];
       uo[v] = sUe[(rho * NV + v) * E + el];
       gsum[v] = 0.0;
     }
-    if constexpr (Ph::VISC) {
-      // g_L / g_R published by the left / right element at its own face point
-      const int rL = left ? rho : rho2, rR = left ? rho2 : rho;
-      const int eL = left ? (int)e : m, eR = left ? m : (int)e;
+    if (unp) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        double a = 0.0;
-        if (wl != 0.0) a = wl * b.Tg[((int64_t)rL * Kp + eL) * NV + v];
-        if (wr != 0.0) a = fma(wr, b.Tg[((int64_t)rR * Kp + eR) * NV + v], a);
-        gsum[v] = a;
+        un[v] = unp[v];
+        if constexpr (Ph::VISC) gsum[v] = gsp[v];
+      }
+    } else {
+      const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) un[v] = b.Tu[((int64_t)rho2 * Kp + m) * NV + v];
+      if constexpr (Ph::VISC) {
+        // g_L / g_R published by the left / right element at its own face point
+        const int rL = left ? rho : rho2, rR = left ? rho2 : rho;
+        const int eL = left ? (int)e : m, eR = left ? m : (int)e;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          double a = 0.0;
+          if (wl != 0.0) a = wl * b.Tg[((int64_t)rL * Kp + eL) * NV + v];
+          if (wr != 0.0) a = fma(wr, b.Tg[((int64_t)rR * Kp + eR) * NV + v], a);
+          gsum[v] = a;
+        }
       }
     }
     const ExtMetric mt = b.xm[s * S::next + rho];
@@ -733,7 +796,16 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
       if constexpr (Ph::VISC) Fv += gsum[v] + ph.eta * (uL[v] - uR[v]);
       sUe[(rho * NV + v) * E + el] = sc * Fv;
     }
+  };
+#if SDRT_SB_PF
+#pragma unroll
+  for (int k = 0; k < fg.CI; ++k) {
+    const int item = threadIdx.x + k * SDRT_SB_NT;
+    if (item < S::next * E) face_flux(item, fg.un[k], fg.gs[Ph::VISC ? k : 0]);
   }
+#else
+  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) face_flux(item, nullptr, nullptr);
+#endif
   if constexpr (INT) {
     if (O.fr) {  // FR-SDRT: fluxes at the solution points, F[s][d][v]
       for (int item = threadIdx.x; item < S::nsol * E; item += blockDim.x) {
