@@ -549,9 +549,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
       for (int v = 0; v < NV; ++v) {
         un[k][v] = b.Tu[((side ? xR : xL) * NV + v) * Kt + m];
         if constexpr (Ph::VISC) {
+          // predicated loads into zeroed registers: nothing consumes them here
           const int eL = side ? (int)e : m, eR = side ? m : (int)e;
-          tga[k][v] = wl != 0.0 ? b.Tg[(xL * NV + v) * Kt + eL] : 0.0;
-          tgb[k][v] = wr != 0.0 ? b.Tg[(xR * NV + v) * Kt + eR] : 0.0;
+          tga[k][v] = 0.0;
+          tgb[k][v] = 0.0;
+          if (wl != 0.0) tga[k][v] = b.Tg[(xL * NV + v) * Kt + eL];
+          if (wr != 0.0) tgb[k][v] = b.Tg[(xR * NV + v) * Kt + eR];
         }
       }
     }
