@@ -67,6 +67,8 @@ struct SDims {
 
 template <typename T>
 __host__ __device__ constexpr T cmax(T a, T b) { return a > b ? a : b; }
+template <class T>
+__host__ __device__ constexpr T cmin(T a, T b) { return a < b ? a : b; }
 
 struct STileMaps {
   CUtensorMap uin, un, acc, rint;
@@ -89,6 +91,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #endif
 #ifndef SDRT_SB_MINB
 #define SDRT_SB_MINB 4
+#endif
+#ifndef SDRT_SA_QCH
+#define SDRT_SA_QCH 1024
 #endif
 #ifndef SDRT_SA_NT
 #define SDRT_SA_NT 256
@@ -492,7 +497,10 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
 template <int D, int P, int NV>
 struct SLayoutA {
   using S = SDims<D, P>;
-  static constexpr int X = cmax(cmax(S::nsol * NV, S::next * D * NV), S::nu * D * NV);
+  // Q_ext is formed and published in chunks of QCH external points (whole 8-row
+  // m-tiles of M0), so region X holds one chunk
+  static constexpr int QCH = cmin(SDRT_SA_QCH, (S::next + 7) / 8 * 8);
+  static constexpr int X = cmax(cmax(cmax(S::nsol * NV, S::next * NV), QCH * D * NV), S::nu * D * NV);
   static constexpr int UE = cmax(S::next * NV, S::nu * D * NV);
   static constexpr int UU = S::nu * NV;
   static constexpr int Q = S::nsol * D * NV;
@@ -540,31 +548,42 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   metric_grad<D, P, NV, E>(g, sNb, sQ);
   __syncthreads();
   SPH(0, 4)
-  // gradient at the external points (M0 on each of the D NV gradient rows) into X
-  dmm_blocks<NV, S::kt_sol, E, D>(O.M0, sQ, S::nsol * NV * E, sX);  // Q_ext [next][d][v]
-  __syncthreads();
-  SPH(0, 5)
-  // publish g at the face points of the LDG-weighted side
+  // gradient at the external points (M0 on each of the D NV gradient rows) into X, one
+  // chunk of QCH points at a time, and g published at the chunk's points of the
+  // LDG-weighted side
   const bool pub_left = (0.5 + ph.beta) != 0.0, pub_right = (0.5 - ph.beta) != 0.0;
   const int Kp = (int)g.Kt;  // trace row stride
-  for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) {
-    const int el = item % E, rho = item / E;
-    const int64_t e = e0 + el;
-    if (e >= g.K) continue;
-    const int s = sNb[D + 1][el], f = rho / S::nfp;
-    const bool left = g.left[s][f];
-    if ((left && !pub_left) || (!left && !pub_right)) continue;
-    double u[NV], q[D * NV];
+#pragma unroll 1
+  for (int r0 = 0; r0 < S::next; r0 += Ly::QCH) {
+    const int nr = S::next - r0 < Ly::QCH ? S::next - r0 : Ly::QCH;
+    SOpF Mc = O.M0;
+    Mc.rows = nr;
+    Mc.mt = (nr + 7) / 8;
+    Mc.frag = O.M0.frag + (int64_t)(r0 / 8) * O.M0.kt * 32;
+    if (Mc.kmask) Mc.kmask = O.M0.kmask + r0 / 8;
+    if (r0 > 0) __syncthreads();  // the previous chunk's publish has read X
+    dmm_blocks<NV, S::kt_sol, E, D>(Mc, sQ, S::nsol * NV * E, sX);  // Q_ext [chunk][d][v]
+    __syncthreads();
+  SPH(0, 5)
+    for (int item = threadIdx.x; item < nr * E; item += blockDim.x) {
+      const int el = item % E, rl = item / E, rho = r0 + rl;
+      const int64_t e = e0 + el;
+      if (e >= g.K) continue;
+      const int s = sNb[D + 1][el], f = rho / S::nfp;
+      const bool left = g.left[s][f];
+      if ((left && !pub_left) || (!left && !pub_right)) continue;
+      double u[NV], q[D * NV];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
+      for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
 #pragma unroll
-    for (int k = 0; k < D * NV; ++k) q[k] = sX[(rho * D * NV + k) * E + el];
-    const ExtMetric mt = b.xm[s * S::next + rho];
-    const double nl[3] = {mt.n0, mt.n1, mt.n2};
-    double gv[NV];
-    Ph::visc_dir(ph, u, q, nl, gv);
+      for (int k = 0; k < D * NV; ++k) q[k] = sX[(rl * D * NV + k) * E + el];
+      const ExtMetric mt = b.xm[s * S::next + rho];
+      const double nl[3] = {mt.n0, mt.n1, mt.n2};
+      double gv[NV];
+      Ph::visc_dir(ph, u, q, nl, gv);
 #pragma unroll
-    for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
+      for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
+    }
   }
   __syncthreads();
   SPH(0, 6)
