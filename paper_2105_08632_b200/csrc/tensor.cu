@@ -34,6 +34,12 @@
 #include "tma.cuh"
 #include "diag.cuh"
 
+// kernel A internal fluxes on element pairs (16-byte shared-memory loads): 0 never,
+// 1 always, 2 for scalar equations only (measured: c3 43.7 -> 41.6 us; NS spills)
+#ifndef SDRT_TA_PAIR
+#define SDRT_TA_PAIR 2
+#endif
+
 namespace sdrt {
 
 // Optional per-phase cycle accounting (build with -DSDRT_PHASE_PROF; tools only):
@@ -358,6 +364,61 @@ __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D&
   for (int v = 0; v < NV; ++v) sF[((t * NI + a) * NV + v) * E + el] = fc[v] + fv[v];
 }
 
+// visc_internal for the element pair (el0, el0 + 1): 16-byte shared-memory loads
+// (SDRT_TA_PAIR), the physics evaluated per element
+template <int D, int P, int EQ, int E, int d, int NI>
+__device__ __forceinline__ void visc_internal2(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                                               const double* sU, const double* sQ, double* sF, int t, int a,
+                                               int el0) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NS = T::NS;
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  auto ld2 = [&](const double* base, int idx) { return *reinterpret_cast<const double2*>(base + idx * E + el0); };
+  double2 ua[NV], qa[D * NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    if constexpr (NI == n) {
+      ua[v] = ld2(sU, (lb + a * ls) * NV + v);
+#pragma unroll
+      for (int dd = 0; dd < D; ++dd) qa[dd * NV + v] = ld2(sQ, (dd * NS + (lb + a * ls)) * NV + v);
+    } else {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const double2 x = ld2(sU, (lb + i * ls) * NV + v);
+        s.x = fma(L.Iint[a][i], x.x, s.x);
+        s.y = fma(L.Iint[a][i], x.y, s.y);
+      }
+      ua[v] = s;
+#pragma unroll
+      for (int dd = 0; dd < D; ++dd) {
+        double2 s2 = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const double2 x = ld2(sQ, (dd * NS + (lb + i * ls)) * NV + v);
+          s2.x = fma(L.Iint[a][i], x.x, s2.x);
+          s2.y = fma(L.Iint[a][i], x.y, s2.y);
+        }
+        qa[dd * NV + v] = s2;
+      }
+    }
+  }
+  const double wf = g.detJ * g.jinv[d];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    double u1[NV], q1[D * NV], fc[NV], fv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) u1[v] = h ? ua[v].y : ua[v].x;
+#pragma unroll
+    for (int k = 0; k < D * NV; ++k) q1[k] = h ? qa[k].y : qa[k].x;
+    Ph::template conv_axis<d>(ph, u1, wf, fc);
+    Ph::template visc_axis<d>(ph, u1, q1, wf, fv);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) sF[((t * NI + a) * NV + v) * E + el0 + h] = fc[v] + fv[v];
+  }
+}
+
 // Kernel A (viscous equations) = the element-local "volume" work: gradient, published
 // viscous normal-flux traces, and the internal-flux part of the divergence
 // R_int = M13 M19 P2 F~ (convective + viscous, l.305-311, l.2919-2925) -> b.Rv
@@ -429,7 +490,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
       }
     }
     const int nA = ph_ == 0 ? npub : 0;
-    const int nB = ph_ < D ? NFI : 0;
+    constexpr bool PAIR = SDRT_TA_PAIR == 1 || (SDRT_TA_PAIR == 2 && NV == 1);
+    const int nB = ph_ < D ? (PAIR ? NFI / 2 : NFI) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
     // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
     auto divergence = [&]() {
@@ -465,6 +527,13 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         if (d == 0) publish_g<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
         else if (d == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
         else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+      } else if constexpr (PAIR) {
+        constexpr int E2 = E / 2;
+        const int i2 = item - nA, el = 2 * (i2 % E2), r = i2 / E2, a = r % NI, t = r / NI;
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        if (ph_ == 0) visc_internal2<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if (ph_ == 1) visc_internal2<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+        else if constexpr (D == 3) visc_internal2<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, t, a, el);
       } else {
         const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % NI, t = r / NI;
         double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
