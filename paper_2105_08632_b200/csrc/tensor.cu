@@ -39,6 +39,11 @@
 #ifndef SDRT_TA_PAIR
 #define SDRT_TA_PAIR 2
 #endif
+// kernel A gradient on element pairs (GradNb2), same modes (measured: c3 41.6 -> 40.2 us,
+// c4 253 -> 256 us)
+#ifndef SDRT_TA_GPAIR
+#define SDRT_TA_GPAIR 2
+#endif
 
 namespace sdrt {
 
@@ -242,6 +247,90 @@ struct GradNb {
         q = fma(L.Dfl[i][NI + 1], c1, q);
         sQ[((d * NS + (lb + i * ls)) * NV + v) * E + el] = jd * q;
       }
+    }
+  }
+};
+
+// GradNb on element pairs (el0, el0 + 1): 16-byte shared-memory loads and stores, the
+// same arithmetic per element (SDRT_TA_GPAIR)
+template <int D, int P, int EQ, int E, int THREADS, int NI = P>
+struct GradNb2 {
+  using T = TDims<D, P>;
+  static constexpr int NV = Phys<EQ, D>::NV;
+  static constexpr int E2 = E / 2;
+  static constexpr int ITEMS = D * T::NL * NV * E2;
+  static constexpr int CI = (ITEMS + THREADS - 1) / THREADS;
+  double nb[CI][2][2];  // [item][element of the pair][face side]
+
+  __device__ __forceinline__ void load(const TensorGeom& g, const double* __restrict__ Tu, const int (*sNb)[E],
+                                       int64_t e0) {
+    constexpr int NL = T::NL;
+    const int Kt = (int)g.Kt;
+#pragma unroll
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * THREADS;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) nb[k][h][0] = nb[k][h][1] = 0.0;
+      if (item < ITEMS) {
+        const int el0 = 2 * (item % E2), r = item / E2, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (e0 + el0 + h < g.K) {
+            nb[k][h][0] = Tu[(((2 * d + 1) * NL + t) * NV + v) * Kt + sNb[2 * d][el0 + h]];
+            nb[k][h][1] = Tu[(((2 * d + 0) * NL + t) * NV + v) * Kt + sNb[2 * d + 1][el0 + h]];
+          }
+      }
+    }
+  }
+
+  __device__ __forceinline__ void compute(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                          double* sQ, int64_t e0) const {
+    constexpr int n = T::n, NL = T::NL, NS = T::NS;
+    const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
+#pragma unroll
+    for (int k = 0; k < CI; ++k) {
+      const int item = threadIdx.x + k * THREADS;
+      if (item >= ITEMS) break;
+      const int el0 = 2 * (item % E2), r = item / E2, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
+      const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+      double u[2][n];
+#pragma unroll
+      for (int i = 0; i < n; ++i) {
+        const double2 x = *reinterpret_cast<const double2*>(sU + ((lb + i * ls) * NV + v) * E + el0);
+        u[0][i] = x.x;
+        u[1][i] = x.y;
+      }
+      const double jd = g.jinv[d];
+      double q2[2][n];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double own0 = interp_end<n>(L.Iend[0], u[h]), own1 = interp_end<n>(L.Iend[1], u[h]);
+        const double c0 = wl * nb[k][h][0] + wr * own0;
+        const double c1 = wl * own1 + wr * nb[k][h][1];
+        double ui[NI];
+#pragma unroll
+        for (int a = 0; a < NI; ++a) {
+          if constexpr (NI == n) {
+            ui[a] = u[h][a];
+          } else {
+            double s = 0.0;
+#pragma unroll
+            for (int i = 0; i < n; ++i) s = fma(L.Iint[a][i], u[h][i], s);
+            ui[a] = s;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          double q = L.Dfl[i][0] * c0;
+#pragma unroll
+          for (int a = 0; a < NI; ++a) q = fma(L.Dfl[i][a + 1], ui[a], q);
+          q = fma(L.Dfl[i][NI + 1], c1, q);
+          q2[h][i] = jd * q;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < n; ++i)
+        *reinterpret_cast<double2*>(sQ + ((d * NS + (lb + i * ls)) * NV + v) * E + el0) = make_double2(q2[0][i], q2[1][i]);
     }
   }
 };
@@ -452,7 +541,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   __syncthreads();
   PH(0, 0)
   {
-    GradNb<D, P, EQ, E, NT, NI> gn;
+    constexpr bool GPAIR = SDRT_TA_GPAIR == 1 || (SDRT_TA_GPAIR == 2 && Ph::NV == 1);
+    std::conditional_t<GPAIR, GradNb2<D, P, EQ, E, NT, NI>, GradNb<D, P, EQ, E, NT, NI>> gn;
     gn.load(g, b.Tu, sNb, e0);
     mbar_wait(&bar, 0);
     __syncthreads();
