@@ -39,6 +39,12 @@
 #ifndef SDRT_TA_PAIR
 #define SDRT_TA_PAIR 2
 #endif
+// kernel A internal fluxes and published g by DMMA line interpolation (NS, E = 8);
+// parity-green but measured slower on c4 (253 -> 314 us: only 16 of 32 lanes carry
+// physics after the mma, and the fragments cost registers), so off by default
+#ifndef SDRT_TA_DMMA
+#define SDRT_TA_DMMA 0
+#endif
 // kernel A gradient on element pairs (GradNb2), same modes (measured: c3 41.6 -> 40.2 us,
 // c4 253 -> 256 us)
 #ifndef SDRT_TA_GPAIR
@@ -508,6 +514,87 @@ __device__ __forceinline__ void visc_internal2(const TensorGeom& g, const Line1D
   }
 }
 
+// FP64 tensor-core (DMMA m8n8k4) form of a d-line's interpolations (SDRT_TA_DMMA):
+// one warp per line t, the 8 x 4 operator [Iint (NI rows); Iend (2 rows); 0] applied to
+// every needed component (u_v and the gradient entries, the line's points as k, the 8
+// tile elements as columns).  Lane (r = lane / 4, elements 2 (lane % 4) + {0, 1}) then
+// holds all components at point r of its two elements: r < NI internal flux point ->
+// F~ into sF; r = NI + side (published side) -> g = n_L . f^v into Tg.  The mma is a pure
+// asm statement, so products whose outputs the axis physics never reads are removed.
+__device__ __forceinline__ void dmma_pure(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+template <int D, int P, int EQ, int E, int d, int NI>
+__device__ __forceinline__ void visc_line_dmma(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                                               const double* sU, const double* sQ, double* sF,
+                                               double* __restrict__ Tg, int64_t e0, int t, bool pub0, bool pub1) {
+  static_assert(E == 8, "one 8-column tile per line");
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NS = T::NS, NL = T::NL, KT = (n + 3) / 4;
+  static_assert(NI + 2 <= 8, "operator rows");
+  const int lane = threadIdx.x & 31;
+  const int r = lane >> 2, kc = lane & 3, col = lane >> 2;
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  double a[KT];
+#pragma unroll
+  for (int k = 0; k < KT; ++k) {
+    const int i = 4 * k + kc;
+    double v = 0.0;
+    if (i < n) {
+      if (r < NI) v = (NI == n) ? (r == i ? 1.0 : 0.0) : L.Iint[r][i];
+      else if (r == NI) v = L.Iend[0][i];
+      else if (r == NI + 1) v = L.Iend[1][i];
+    }
+    a[k] = v;
+  }
+  auto line = [&](const double* base) {  // base: the component's point-0 row at element 0
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      const int i = 4 * k + kc;
+      const double b = i < n ? base[(i * ls) * NV * E + col] : 0.0;
+      dmma_pure(c0, c1, a[k], b);
+    }
+    return make_double2(c0, c1);
+  };
+  double2 cu[NV], cq[D * NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) cu[v] = line(sU + (lb * NV + v) * E);
+#pragma unroll
+  for (int dd = 0; dd < D; ++dd)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) cq[dd * NV + v] = line(sQ + ((dd * NS + lb) * NV + v) * E);
+  const bool inner = r < NI;
+  const int side = r - NI;
+  const bool pub = (side == 0 && pub0) || (side == 1 && pub1);
+  if (!inner && !pub) return;
+  const double wf = g.detJ * g.jinv[d];
+  const double wd = inner ? wf : 1.0;  // canonical (left) normal +e_d for the published g
+  const int ext = (2 * d + (side > 0 ? 1 : 0)) * NL + t;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int el = 2 * kc + h;
+    double u[NV], q[D * NV], fc[NV], fv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) u[v] = h ? cu[v].y : cu[v].x;
+#pragma unroll
+    for (int k = 0; k < D * NV; ++k) q[k] = h ? cq[k].y : cq[k].x;
+    Ph::template visc_axis<d>(ph, u, q, wd, fv);
+    if (inner) {
+      Ph::template conv_axis<d>(ph, u, wf, fc);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) sF[((t * NI + r) * NV + v) * E + el] = fc[v] + fv[v];
+    } else if (e0 + el < g.K) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) Tg[((int64_t)ext * NV + v) * g.Kt + e0 + el] = fv[v];
+    }
+  }
+}
+
 // Kernel A (viscous equations) = the element-local "volume" work: gradient, published
 // viscous normal-flux traces, and the internal-flux part of the divergence
 // R_int = M13 M19 P2 F~ (convective + viscous, l.305-311, l.2919-2925) -> b.Rv
@@ -579,9 +666,10 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         }
       }
     }
-    const int nA = ph_ == 0 ? npub : 0;
+    constexpr bool LDMMA = SDRT_TA_DMMA != 0 && E == 8 && Ph::VISC && NV > 1;
+    const int nA = (ph_ == 0 && !LDMMA) ? npub : 0;
     constexpr bool PAIR = SDRT_TA_PAIR == 1 || (SDRT_TA_PAIR == 2 && NV == 1);
-    const int nB = ph_ < D ? (PAIR ? NFI / 2 : NFI) : 0;
+    const int nB = (ph_ < D && !LDMMA) ? (PAIR ? NFI / 2 : NFI) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
     // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
     auto divergence = [&]() {
@@ -608,6 +696,17 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
     if constexpr (!DBUF) {
       if (ph_ >= 1) divergence();
       __syncthreads();
+    }
+    if constexpr (LDMMA) {
+      if (ph_ < D) {
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        const int warp = threadIdx.x >> 5, nw = NT >> 5;
+        for (int t = warp; t < NL; t += nw) {
+          if (ph_ == 0) visc_line_dmma<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, pub0, pub1);
+          else if (ph_ == 1) visc_line_dmma<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, pub0, pub1);
+          else if constexpr (D == 3) visc_line_dmma<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, pub0, pub1);
+        }
+      }
     }
     for (int item = threadIdx.x; item < nA + nB; item += blockDim.x) {
       if (item < nA) {
