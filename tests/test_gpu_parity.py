@@ -97,6 +97,46 @@ def test_full_size_parity(name, steps):
     assert _rel(got, ref) <= TOL, _rel(got, ref)
 
 
+@pytest.mark.parametrize("name,Ns", [("c2", 4), ("c3", 4), ("c5", 4)])
+def test_full_size_tiled_parity(name, Ns):
+    """BASELINE.json full sizes in the bench launch configuration, compared with the oracle
+    at every element: the uniform periodic mesh is translation invariant (PAPER.md
+    l.521-527), so a state with a period of Ns patterns per axis has a residual and an RK4
+    step of the same period.  The oracle runs on one Ns^D period (the same h) on a seeded
+    random state; its results, tiled over the full mesh, must equal the full-size GPU
+    residual and RK4 step (c5: 663 552 tetrahedra)."""
+    from oracle.mesh import build_mesh
+    from oracle.physics import Physics
+    from oracle.residual import Residual, integrate
+    from paper_2105_08632_b200.solver import Solver
+    cfg = CONFIGS[name]
+    D, N = cfg.nd, cfg.N
+    assert N % Ns == 0
+    lo, hi = np.asarray(cfg.lo, dtype=float), np.asarray(cfg.hi, dtype=float)
+    m = build_mesh(cfg.etype, cfg.p, Ns, list(lo), list(lo + (hi - lo) * (Ns / N)))
+    R = Residual(m, Physics(cfg.eq, D, **cfg.physics_kwargs()))
+    Us = random_state(cfg, R.ops.nsol, m.K, seed=7, amp=0.2)
+    nsub = m.K // Ns ** D
+
+    def tile(A):  # element order: pattern (x fastest) major, subcell innermost
+        a = A.reshape(A.shape[:2] + (Ns,) * D + (nsub,))
+        a = np.tile(a, (1, 1) + (N // Ns,) * D + (1,))
+        return a.reshape(A.shape[:2] + (N ** D * nsub,))
+
+    S = Solver(cfg.etype, cfg.p, N, cfg.lo, cfg.hi, cfg.eq, device="cuda", **cfg.physics_kwargs())
+    K = S.K
+    Uf = tile(Us)
+    assert Uf.shape[2] == K
+    got = S.to_host(S.residual(S.to_device(Uf)))[:, :, :K]
+    assert _rel(got, tile(R(Us))) <= TOL, _rel(got, tile(R(Us)))
+    Ud = S.to_device(Uf)
+    S.rk_step(Ud, cfg.dt, 1)
+    ref = tile(integrate(R, Us, cfg.dt, 1))
+    got = S.to_host(Ud)[:, :, :K]
+    assert _rel(got, ref) <= TOL, _rel(got, ref)
+    S.close()
+
+
 def test_divergence_is_reported():
     from paper_2105_08632_b200 import sdrt
     cfg = CONFIGS["c2"]
