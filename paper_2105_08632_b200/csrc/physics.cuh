@@ -214,6 +214,34 @@ struct Phys {
     }
   }
 
+  // conv_common along the axis normal +e_D0 (tensor faces): the same Rusanov flux without
+  // the structural zeros of the normal
+  template <int D0>
+  static __device__ __forceinline__ void conv_common_axis(const PhysDev& ph, const double* uL, const double* uR,
+                                                          double* F) {
+    if constexpr (NV == 1) {
+      const double cn = ph.c[D0];
+      F[0] = 0.5 * cn * (uL[0] + uR[0]) + 0.5 * fabs(cn) * (uL[0] - uR[0]);
+    } else {
+      double fL[NV], fR[NV];
+      conv_axis<D0>(ph, uL, 1.0, fL);
+      conv_axis<D0>(ph, uR, 1.0, fR);
+      const double irL = 1.0 / uL[0], irR = 1.0 / uR[0];
+      double vvL = 0.0, vvR = 0.0;
+#pragma unroll
+      for (int d = 0; d < D; ++d) {
+        vvL += uL[1 + d] * uL[1 + d];
+        vvR += uR[1 + d] * uR[1 + d];
+      }
+      const double vnL = uL[1 + D0] * irL, vnR = uR[1 + D0] * irR;
+      const double pL = (ph.gamma - 1.0) * (uL[D + 1] - 0.5 * vvL * irL);
+      const double pR = (ph.gamma - 1.0) * (uR[D + 1] - 0.5 * vvR * irR);
+      const double phi = fmax(fabs(vnL) + sqrt(ph.gamma * pL * irL), fabs(vnR) + sqrt(ph.gamma * pR * irR));
+#pragma unroll
+      for (int a = 0; a < NV; ++a) F[a] = 0.5 * (fL[a] + fR[a]) + 0.5 * phi * (uL[a] - uR[a]);
+    }
+  }
+
   // common normal flux along nL (left element's unit normal)
   static __device__ __forceinline__ void common_flux(const PhysDev& ph, const double* uL, const double* uR,
                                                      const double* qL, const double* qR, const double* n,

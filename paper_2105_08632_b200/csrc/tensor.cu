@@ -821,9 +821,6 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
     constexpr int d = decltype(dc)::value;
     const double wf = g.detJ * g.jinv[d];  // transformed-flux weight detJ (J^-1)_dd
     const double sface = g.sface[d];
-    double nL[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) nL[k] = (k == d) ? 1.0 : 0.0;
     for (int item = threadIdx.x; item < (INT ? NL * NI * E : 0); item += blockDim.x) {
       const int el = item % E, r = item / E, a = r % NI, t = r / NI;
       const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
@@ -861,7 +858,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
       const double* uL = side ? uo : un[k];
       const double* uR = side ? un[k] : uo;
       double F[NV];
-      Ph::conv_common(ph, uL, uR, nL, F);
+      Ph::template conv_common_axis<d>(ph, uL, uR, F);
       if constexpr (Ph::VISC) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
