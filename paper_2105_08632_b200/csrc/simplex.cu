@@ -386,12 +386,18 @@ struct FluxGather {
         const int64_t e = e0 + el;
         const int rL = left ? rho : rho2, rR = left ? rho2 : rho;
         const int64_t eL = left ? e : m, eR = left ? m : e;
+        // one published side (beta = +-1/2): its raw g by a predicated load nothing
+        // consumes here (weighted at use); two sides: combined now
+        const bool one = (wl == 0.0) != (wr == 0.0);
+        const int64_t gi = one ? (wl != 0.0 ? (int64_t)rL * Kp + eL : (int64_t)rR * Kp + eR) : 0;
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          double a = 0.0;
-          if (wl != 0.0) a = wl * Tg[((int64_t)rL * Kp + eL) * NV + v];
-          if (wr != 0.0) a = fma(wr, Tg[((int64_t)rR * Kp + eR) * NV + v], a);
-          gs[k][v] = a;
+          if (one) {
+            gs[k][v] = Tg[gi * NV + v];
+          } else {
+            double a = wl * Tg[((int64_t)rL * Kp + eL) * NV + v];
+            gs[k][v] = fma(wr, Tg[((int64_t)rR * Kp + eR) * NV + v], a);
+          }
         }
       }
     }
@@ -820,7 +826,14 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
 #pragma unroll
   for (int k = 0; k < fg.CI; ++k) {
     const int item = threadIdx.x + k * SDRT_SB_NT;
-    if (item < S::next * E) face_flux(item, fg.un[k], fg.gs[Ph::VISC ? k : 0]);
+    double gk[NV];
+    {
+      const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
+      const double w1 = (wl == 0.0) != (wr == 0.0) ? (wl != 0.0 ? wl : wr) : 1.0;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) gk[v] = Ph::VISC ? w1 * fg.gs[Ph::VISC ? k : 0][v] : 0.0;
+    }
+    if (item < S::next * E) face_flux(item, fg.un[k], gk);
   }
 #else
   for (int item = threadIdx.x; item < S::next * E; item += blockDim.x) face_flux(item, nullptr, nullptr);
