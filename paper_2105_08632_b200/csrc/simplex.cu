@@ -259,30 +259,27 @@ __device__ __forceinline__ double sop_at(const SOpF& M, int r, int c) {
 
 // ---------------------------------------------------------------- tile helpers
 // neighbour of element e across local face f (pattern arithmetic, periodic)
+template <int D>
 __device__ __forceinline__ int snbr(const GeomDev& g, int e, int s, int f) {
-  int pat = e / g.nsub;
-  int c[3] = {0, 0, 0};
+  // pattern coordinates in registers (no dynamically indexed local array)
+  const int pat = e / g.nsub;
+  const int c0 = pat % g.Nloc[0];
+  const int r = pat / g.Nloc[0];
+  const int c1 = D == 2 ? r : r % g.Nloc[1];
+  const int c2 = D == 2 ? 0 : r / g.Nloc[1];
+  int cc[3] = {c0 + g.off[s][f][0], c1 + g.off[s][f][1], D == 3 ? c2 + g.off[s][f][2] : 0};
+  const int cs[3] = {c0, c1, c2};
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
-    if (d < g.nd) {
-      c[d] = pat % g.Nloc[d];
-      pat /= g.Nloc[d];
+  for (int d = 0; d < D; ++d)
+    if ((cc[d] < 0 || cc[d] >= g.Nloc[d]) && g.halo[d]) {
+      // ghost column: slab (d, side), tangential pattern index, neighbour sub-cell
+      const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
+      const int tang = D == 2 ? cs[a] : cs[a] + g.Nloc[a] * cs[bb];
+      return (int)g.gbase[d][cc[d] < 0 ? 0 : 1] + tang * g.nsub + g.nshape[s][f];
     }
-  int id = 0, mul = 1;
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
-    if (d < g.nd) {
-      int cc = c[d] + g.off[s][f][d];
-      if ((cc < 0 || cc >= g.Nloc[d]) && g.halo[d]) {
-        // ghost column: slab (d, side), tangential pattern index, neighbour sub-cell
-        const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
-        const int tang = g.nd == 2 ? c[a] : c[a] + g.Nloc[a] * c[bb];
-        return (int)g.gbase[d][cc < 0 ? 0 : 1] + tang * g.nsub + g.nshape[s][f];
-      }
-      cc = cc < 0 ? cc + g.Nloc[d] : (cc >= g.Nloc[d] ? cc - g.Nloc[d] : cc);
-      id += mul * cc;
-      mul *= g.Nloc[d];
-    }
+  for (int d = 0; d < D; ++d) cc[d] = cc[d] < 0 ? cc[d] + g.Nloc[d] : (cc[d] >= g.Nloc[d] ? cc[d] - g.Nloc[d] : cc[d]);
+  const int id = D == 2 ? cc[0] + g.Nloc[0] * cc[1] : cc[0] + g.Nloc[0] * (cc[1] + g.Nloc[1] * cc[2]);
   return id * g.nsub + g.nshape[s][f];
 }
 
@@ -293,7 +290,7 @@ __device__ __forceinline__ void fill_neighbours(const GeomDev& g, int (*sNb)[E],
     const int el = idx % E, f = idx / E;
     const int e = (int)e0 + el;
     const int s = e % g.nsub;
-    sNb[f][el] = f == D + 1 ? s : (e < g.K ? snbr(g, e, s, f) : 0);
+    sNb[f][el] = f == D + 1 ? s : (e < g.K ? snbr<D>(g, e, s, f) : 0);
   }
 }
 
@@ -810,8 +807,12 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
     }
     const ExtMetric mt = b.xm[s * S::next + rho];
     const double nl[3] = {mt.n0, mt.n1, mt.n2};
-    const double* uL = left ? uo : un;
-    const double* uR = left ? un : uo;
+    double uL[NV], uR[NV];  // by value: a runtime pointer select would put uo/un in local memory
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      uL[v] = left ? uo[v] : un[v];
+      uR[v] = left ? un[v] : uo[v];
+    }
     double F[NV];
     Ph::conv_common(ph, uL, uR, nl, F);
     const double sc = left ? mt.s : -mt.s;

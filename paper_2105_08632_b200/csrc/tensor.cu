@@ -94,21 +94,25 @@ __device__ __forceinline__ int lstr(int d) {
 // 32-bit arithmetic (K < 2^31); evaluated once per tile element (fill_nbrs).
 template <int D>
 __device__ __forceinline__ int tnbr(const TensorGeom& g, int e, int d, int delta) {
-  int c[3];
-  c[0] = e % g.N[0];
+  // pattern coordinates in registers (no dynamically indexed local array)
+  const int c0 = e % g.N[0];
   const int r = e / g.N[0];
-  c[1] = D == 2 ? r : r % g.N[1];
-  c[2] = D == 2 ? 0 : r / g.N[1];
-  int v = c[d] + delta;
-  if ((v < 0 || v >= g.N[d]) && g.halo[d]) {
+  const int c1 = D == 2 ? r : r % g.N[1];
+  const int c2 = D == 2 ? 0 : r / g.N[1];
+  const int Nd = d == 0 ? g.N[0] : (d == 1 ? g.N[1] : g.N[2]);
+  int v = (d == 0 ? c0 : (d == 1 ? c1 : c2)) + delta;
+  const bool hal = d == 0 ? g.halo[0] != 0 : (d == 1 ? g.halo[1] != 0 : g.halo[2] != 0);
+  if ((v < 0 || v >= Nd) && hal) {
     // ghost column of the neighbouring rank's element: slab (d, side), tangential index
-    const int a = d == 0 ? 1 : 0, bb = d == 2 ? 1 : 2;
-    const int tang = D == 2 ? c[a] : c[a] + g.N[a] * c[bb];
+    const int ca = d == 0 ? c1 : c0, cb = d == 2 ? c1 : c2;
+    const int na = d == 0 ? g.N[1] : g.N[0];
+    const int tang = D == 2 ? ca : ca + na * cb;
     return (int)g.gbase[d][v < 0 ? 0 : 1] + tang;
   }
-  v = v < 0 ? v + g.N[d] : (v >= g.N[d] ? v - g.N[d] : v);
-  c[d] = v;
-  return c[0] + g.N[0] * (c[1] + g.N[1] * c[2]);
+  v = v < 0 ? v + Nd : (v >= Nd ? v - Nd : v);
+  if (d == 0) return v + g.N[0] * (c1 + g.N[1] * c2);
+  if (d == 1) return c0 + g.N[0] * (v + g.N[1] * c2);
+  return c0 + g.N[0] * (c1 + g.N[1] * v);
 }
 
 // neighbour ids of a tile's elements: sNb[2d + side][el] (side 0: x_d - 1, 1: x_d + 1)
@@ -855,8 +859,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
         for (int i = 0; i < n; ++i) ul[i] = sU[((lb + i * ls) * NV + v) * E + el];
         uo[v] = interp_end<n>(L.Iend[side], ul);
       }
-      const double* uL = side ? uo : un[k];
-      const double* uR = side ? un[k] : uo;
+      double uL[NV], uR[NV];  // by value (no runtime pointer select into register arrays)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        uL[v] = side ? uo[v] : un[k][v];
+        uR[v] = side ? un[k][v] : uo[v];
+      }
       double F[NV];
       Ph::template conv_common_axis<d>(ph, uL, uR, F);
       if constexpr (Ph::VISC) {
