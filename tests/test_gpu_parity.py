@@ -216,6 +216,26 @@ def test_tgv_diagnostics_parity(name, N, state, degree):
     assert (np.abs(got - ref) <= 1e-11 * scale).all(), (got, ref)
 
 
+def test_diagnostics_rule_errors():
+    """sdrt_diagnostics_rule accepts 0 (solution points) and 1..10 only; the diagnostics
+    are refused on a non-NS context."""
+    from paper_2105_08632_b200 import sdrt
+    cfg = CONFIGS["c4"]
+    m, R, S = _pair(cfg, 3)
+    for bad in (-1, 11):
+        with pytest.raises(sdrt.SdrtError) as e:
+            sdrt.diagnostics_rule(S.ctx, bad)
+        assert e.value.code == -1
+    for ok in (0, 1, 10):
+        sdrt.diagnostics_rule(S.ctx, ok)
+    cfg2 = CONFIGS["c3"]
+    _, _, S2 = _pair(cfg2, 3)
+    U = S2.to_device(initial_state(cfg2, S2.sol_coords()))
+    with pytest.raises(sdrt.SdrtError) as e:
+        S2.diagnostics(U)
+    assert e.value.code == -2
+
+
 FR_CASES = [(sch, n, N, st) for sch in ("frsdrt", "frdg")
             for (n, N, st) in [("c1", 5, 20), ("c3", 3, 3), ("c4", (3, 4, 3), 3), ("c4", 4, 2)]] + \
            [(sch, n, N, st) for sch in ("frsdrt", "frdg")
