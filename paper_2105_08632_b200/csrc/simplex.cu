@@ -474,6 +474,7 @@ __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev&
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const __grid_constant__ STileMaps tm,
                                                  double* __restrict__ T) {
+  pdl_wait();
   using S = SDims<D, P>;
   constexpr int NV = Phys<EQ, D>::NV;
   extern __shared__ __align__(128) double smem[];
@@ -513,6 +514,7 @@ struct SLayoutA {
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
                                                const __grid_constant__ STileMaps tm) {
+  pdl_wait();
   SPH_INIT
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
@@ -611,6 +613,7 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad_fr(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
                                                                const __grid_constant__ STileMaps tm) {
+  pdl_wait();
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
   constexpr int NV = Ph::NV;
@@ -718,6 +721,7 @@ struct SLayoutB {
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
                                                 double dt, const __grid_constant__ STileMaps tm) {
+  pdl_wait();
   SPH_INIT
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
@@ -1027,21 +1031,21 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
         auto k = ks_grad_fr<D, P, EQ, C::E>;
         const size_t sm = (size_t)(SDims<D, P>::nsol * (1 + D) + SDims<D, P>::next * D) * C::NV * C::E * sizeof(double);
         sset_smem((const void*)k, sm);
-        k<<<grid, 256, sm, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
+        CUDA_LAUNCH_OK(launch_pdl(k, grid, 256, sm, st, g, O, ph, b, smaps(tma, b, b.Uin, false)));
       } else {
         auto k = ks_grad<D, P, EQ, C::E>;
         sset_smem((const void*)k, C::SMEM_A);
-        k<<<grid, SDRT_SA_NT, C::SMEM_A, st>>>(g, O, ph, b, smaps(tma, b, b.Uin, false));
+        CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SA_NT, C::SMEM_A, st, g, O, ph, b, smaps(tma, b, b.Uin, false)));
       }
     }
   } else if (which == 1) {
     auto k = ks_stage<D, P, EQ, C::E>;
     sset_smem((const void*)k, C::SMEM_B);
-    k<<<grid, SDRT_SB_NT, C::SMEM_B, st>>>(g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true));
+    CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SB_NT, C::SMEM_B, st, g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true)));
   } else {
     auto k = ks_traces<D, P, EQ, C::E>;
     sset_smem((const void*)k, C::SMEM_T);
-    k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, O, smaps(tma, b, U, false), T);
+    CUDA_LAUNCH_OK(launch_pdl(k, grid, C::THREADS, C::SMEM_T, st, g, O, smaps(tma, b, U, false), T));
   }
 }
 

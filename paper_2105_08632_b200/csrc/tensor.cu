@@ -367,6 +367,7 @@ __device__ __forceinline__ void write_traces(const TensorGeom& g, const Line1D& 
 template <int D, int P, int EQ, int E>
 __global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const __grid_constant__ TileMaps tm,
                                                  double* __restrict__ T) {
+  pdl_wait();
   constexpr int NV = Phys<EQ, D>::NV;
   constexpr int ROWS = TDims<D, P>::NS * NV;
   extern __shared__ __align__(128) double smem[];
@@ -609,6 +610,7 @@ __device__ __forceinline__ void visc_line_dmma(const TensorGeom& g, const Line1D
 template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
 __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
                                                     const __grid_constant__ TileMaps tm) {
+  pdl_wait();
   PH_INIT
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
@@ -750,6 +752,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
 template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
 __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
                                                    double dt, const __grid_constant__ TileMaps tm) {
+  pdl_wait();
   PH_INIT
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
@@ -1123,14 +1126,14 @@ static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph
       if (grid == 0) return;
       auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A, NI>;
       set_smem<D, P, EQ>((const void*)ka, C::smem_a(NI));
-      ka<<<grid, C::NTA, C::smem_a(NI), st>>>(g, L, ph, b, maps_for(tma, b, false));
+      CUDA_LAUNCH_OK(launch_pdl(ka, grid, C::NTA, C::smem_a(NI), st, g, L, ph, b, maps_for(tma, b, false)));
     }
   } else {
     const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::E - 1) / C::E);
     if (grid == 0) return;
     auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI>;
     set_smem<D, P, EQ>((const void*)kb, C::smem_b(2, NI));
-    kb<<<grid, C::NTB, C::smem_b(stage, NI), st>>>(g, L, ph, b, stage, dt, maps_for(tma, b, true));
+    CUDA_LAUNCH_OK(launch_pdl(kb, grid, C::NTB, C::smem_b(stage, NI), st, g, L, ph, b, stage, dt, maps_for(tma, b, true)));
   }
 }
 
@@ -1151,7 +1154,7 @@ static void run_traces(const TensorGeom& g, const Line1D& L, TensorTma* tma, con
   set_smem<D, P, EQ>((const void*)k, C::SMEM_T);
   TensorBufs b{};
   b.Uin = U;
-  k<<<grid, C::THREADS, C::SMEM_T, st>>>(g, L, maps_for(tma, b, false), Tu);
+  CUDA_LAUNCH_OK(launch_pdl(k, grid, C::THREADS, C::SMEM_T, st, g, L, maps_for(tma, b, false), Tu));
 }
 
 template <int D, int P, int EQ>

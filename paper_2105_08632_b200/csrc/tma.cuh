@@ -1,6 +1,7 @@
 // TMA (cp.async.bulk.tensor) + mbarrier helpers shared by the fused kernels, and the
 // host-side encoder of 2-D tile descriptors over element-major [rows][Kp] fp64 arrays.
 #pragma once
+#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -87,6 +88,47 @@ inline const CUtensorMap& cached_tile_map(Cache* t, const void* ptr) {
   encode_tile_map(&t->map[i], ptr, t->rows, t->E, t->Kp);
   t->ptr[i] = ptr;
   return t->map[i];
+}
+
+
+// ---- programmatic dependent launch (SDRT_PDL): a stage kernel is launched with
+// programmatic stream serialization, so its CTAs are scheduled while the previous
+// kernel drains; pdl_wait() (first statement of the kernel) blocks until that kernel has
+// completed and its writes are visible.  Kernels without pdl_wait are launched normally.
+#ifndef SDRT_PDL
+#define SDRT_PDL 1
+#endif
+__device__ __forceinline__ void pdl_wait() {
+#if SDRT_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+#define CUDA_LAUNCH_OK(x)                                                                     \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) throw std::runtime_error(std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                     Args&&... args) {
+#if SDRT_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+#else
+  k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+  return cudaGetLastError();
+#endif
 }
 
 }  // namespace sdrt
