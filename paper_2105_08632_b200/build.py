@@ -1,9 +1,11 @@
 """Build libsdrt.so in-tree with nvcc for sm_100a (no torch extension machinery)."""
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -18,6 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-v"] + (["-DSDRT_PHASE_PROF"] if PROF else []) + EXTRA_DEFS
 CXX_FLAGS = ["-O2", "-std=gnu++17", "-fPIC", "-Wall"]
+INCLUDES = []
+LINK_LIBS = ["-lquadmath", "-lcudart"]
 
 
 def sources():
@@ -29,35 +33,51 @@ def _nvcc():
     return cand if os.path.exists(cand) else "nvcc"
 
 
+def _stamp():
+    """Flags + defines the library is built with; a change forces a rebuild."""
+    return hashlib.sha1(" ".join(ARCH + NVCC_FLAGS + CXX_FLAGS + LINK_LIBS).encode()).hexdigest()
+
+
+def _compile(s):
+    o = os.path.join(BUILD, os.path.basename(s) + ".o")
+    if s.endswith(".cu"):
+        cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, *INCLUDES, "-c", s, "-o", o]
+    else:
+        cmd = ["g++", *CXX_FLAGS, *INCLUDES, "-c", s, "-o", o]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return o, r.returncode, " ".join(cmd) + "\n" + r.stdout + r.stderr
+
+
 def build(verbose=False, force=False):
     srcs = sources()
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     hdrs.append(os.path.join(HERE, "..", "include", "sdrt.h"))
-    if not force and os.path.exists(OUT):
+    stamp_file = OUT + ".stamp"
+    if not force and os.path.exists(OUT) and os.path.exists(stamp_file):
         t = os.path.getmtime(OUT)
-        if all(os.path.getmtime(f) < t for f in srcs + hdrs):
+        if open(stamp_file).read() == _stamp() and all(os.path.getmtime(f) < t for f in srcs + hdrs):
             return OUT
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
-    logs = []
+    # largest translation units first so the pool stays busy
+    order = sorted(srcs, key=lambda f: -os.path.getsize(f))
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = dict(zip(order, ex.map(_compile, order)))
+    objs, logs = [], []
     for s in srcs:
-        o = os.path.join(BUILD, os.path.basename(s) + ".o")
-        if s.endswith(".cu"):
-            cmd = [_nvcc(), *ARCH, *NVCC_FLAGS, "-c", s, "-o", o]
-        else:
-            cmd = ["g++", *CXX_FLAGS, "-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(logs[-1])
+        o, rc, log = results[s]
+        logs.append(log)
+        if rc != 0:
+            sys.stderr.write(log)
             raise RuntimeError(f"compile failed: {s}")
         objs.append(o)
-    cmd = [_nvcc(), *ARCH, "-shared", "-o", OUT, *objs, "-lquadmath", "-lcudart"]
+    cmd = [_nvcc(), *ARCH, "-shared", "-o", OUT, *objs, *LINK_LIBS]
     r = subprocess.run(cmd, capture_output=True, text=True)
     logs.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
     if r.returncode != 0:
         sys.stderr.write(logs[-1])
         raise RuntimeError("link failed")
+    with open(stamp_file, "w") as f:
+        f.write(_stamp())
     with open(os.path.join(BUILD, "build.log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:

@@ -138,6 +138,7 @@ struct RuleSpec {
   int degree;
   std::vector<double> start;  // starting orbit parameters (select the root)
   bool minimise;              // one free parameter fixed by min next-degree defect
+  double fixed_num = 0, fixed_den = 0;  // or: first orbit parameter held at num/den
 };
 
 static RuleSpec rule_spec(int D, int n) {
@@ -147,7 +148,10 @@ static RuleSpec rule_spec(int D, int n) {
   if (D == 2 && n == 10) return {{S3, S21, S111}, 5, {0.055, 0.07, 0.29}, true};
   if (D == 3 && n == 1) return {{S4}, 1, {}, false};
   if (D == 3 && n == 4) return {{S31}, 2, {0.14}, false};
-  if (D == 3 && n == 10) return {{S31, S22}, 3, {0.07, 0.09}, true};
+  // tet p=3 interior: the S31 parameter is fixed at 17/250 (reading O1, round 2: the
+  // degree-3 family is spatially unstable for a >= 0.069; a = 0.068 reproduces the
+  // paper's tet SDRT3 RK4 tau_MAX, under the SDRT2 calibration)
+  if (D == 3 && n == 10) return {{S31, S22}, 3, {0.07, 0.09}, false, 17, 250};
   throw std::runtime_error("no simplex rule of this size (supported: tri p<=4, tet p<=3)");
 }
 
@@ -277,6 +281,9 @@ static std::vector<std::vector<qd>> simplex_rule(int D, int n) {
   }
   if (S.nunk == 1) {  // centroid
     x[0] = 1;
+  } else if (S.spec.fixed_den > 0) {
+    x[first_par] = (qd)S.spec.fixed_num / (qd)S.spec.fixed_den;
+    S.solve(x, first_par);
   } else if (!S.spec.minimise) {
     S.solve(x, -1);
   } else {

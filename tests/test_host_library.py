@@ -39,7 +39,7 @@ def test_library_exports_every_header_symbol(sdrt):
 
 
 CASES = [("quad", 1), ("quad", 2), ("quad", 3), ("quad", 4), ("tri", 1), ("tri", 2), ("tri", 3),
-         ("tri", 4), ("hex", 1), ("hex", 2), ("hex", 3), ("tet", 1), ("tet", 2), ("tet", 3)]
+         ("tri", 4), ("hex", 1), ("hex", 2), ("hex", 3), ("hex", 4), ("tet", 1), ("tet", 2), ("tet", 3)]
 
 
 @pytest.mark.parametrize("etype,p", CASES)
