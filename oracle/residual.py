@@ -70,7 +70,9 @@ class Residual:
         Qt = Qt.reshape(D, nsol, NV, K)
         return np.einsum("kji,jsak->isak", m.Jinv, Qt)            # q_i = sum_j Jinv[j,i] q~_j
 
-    def __call__(self, U):
+    def _fluxes(self, U):
+        """Steps 1-4: internal transformed fluxes F~_int (N_int, NV.K) and the common
+        flux F (NV, F.nfp) at every face point, computed once per face point."""
         o, m, ph = self.ops, self.mesh, self.ph
         nsol, NV, K = U.shape
         D = o.nd
@@ -97,6 +99,13 @@ class Residual:
             qL = np.stack([Qext[d][self.pL, :, self.fL].T for d in range(D)])
             qR = np.stack([Qext[d][self.pR, :, self.fR].T for d in range(D)])
         Fc = phys.common_flux(ph, uL, uR, qL, qR, self.nL)         # (NV, F.nfp)
+        return Fint, Fc
+
+    def __call__(self, U):
+        o, m = self.ops, self.mesh
+        nsol, NV, K = U.shape
+        Fint, Fc = self._fluxes(U)
+        # D~_L = +s_L F, D~_R = -s_R F (O28: the same F on both sides)
         Dt = self._face_scatter((self.s[self.pL, self.fL] * Fc).T,
                                 (-self.s[self.pR, self.fR] * Fc).T, (o.next, NV, K))
         # step 5-6
@@ -104,8 +113,10 @@ class Residual:
         return (-R.reshape(nsol, NV, K)) / m.detJ[None, None, :]
 
     def face_common_flux(self, U):
-        """Per-face-point common flux F (NV, F.nfp) for the antisymmetry check (O28)."""
-        raise NotImplementedError
+        """Per-face-point common flux F (NV, F.nfp), faces in mesh order (left element,
+        left local face), points in the left element's local order (O28): the left side
+        receives D~ = +s_L F and the right side D~ = -s_R F of this one value."""
+        return self._fluxes(U)[1]
 
 
 def rk4_step(L, u, dt):
