@@ -147,6 +147,14 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* m, const sdrt_operators* o, const s
                             void* d_ws, size_t ws_bytes, void* stream, sdrt_ctx** out);
 /* dU/dt = -J^-1 R~ for the device state d_U -> d_dUdt (both [N_sol][N_V][K_pad]). */
 sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* stream);
+/* Conservation check (reading O28): the residual of d_U as sdrt_residual, and in d_F
+ * ([N_ext][N_V][K_pad], device, caller-owned) the common normal flux F (Rusanov /
+ * upwind + LDG, along the LEFT element's unit normal, before the
+ * metric scale s) that each element applied at each of its external points: the left
+ * side applies D~ = +s F, the right side D~ = -s F of the same value, so for every
+ * face point F(left, q) == F(right, perm[q]) bit for bit.  Single-rank contexts (as
+ * sdrt_residual).  Errors: SDRT_E_INVALID_ARG for null pointers. */
+sdrt_status sdrt_face_flux(sdrt_ctx* c, const double* d_U, double* d_dUdt, double* d_F, void* stream);
 /* nsteps classical RK4 steps of size dt, in place on d_U. check_every > 0 syncs the
  * stream every check_every steps and returns SDRT_E_DIVERGED (message names the
  * first non-finite / non-physical element and step) if the state went bad. */

@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(256) k_int_flux(GeomDev g, PhysDev ph, const d
 template <int EQ, int D>
 __global__ void __launch_bounds__(256) k_face_flux(GeomDev g, PhysDev ph, const ExtMetric* __restrict__ xm,
                                                    const double* __restrict__ Uext,
-                                                   const double* __restrict__ Qext, double* __restrict__ Xd) {
+                                                   const double* __restrict__ Qext, double* __restrict__ Xd,
+                                                   double* __restrict__ Fexp) {
   using P = Phys<EQ, D>;
   constexpr int NV = P::NV;
   const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -206,6 +207,9 @@ __global__ void __launch_bounds__(256) k_face_flux(GeomDev g, PhysDev ph, const 
   const double sc = left ? mt.s : -mt.s;
 #pragma unroll
   for (int a = 0; a < NV; ++a) Xd[((int64_t)e * NV + a) * g.Kp + n] = sc * F[a];
+  if (Fexp)  // O28 export: the common flux this element applies at its ext point e
+#pragma unroll
+    for (int a = 0; a < NV; ++a) Fexp[((int64_t)e * NV + a) * g.Kp + n] = F[a];
 }
 
 // k = -R~/detJ ; mode 0: out = k ; RK4 stage update otherwise (3-register form):
@@ -432,6 +436,7 @@ struct sdrt_ctx {
   int32_t *h_srow = nullptr, *h_scol = nullptr, *h_rrow = nullptr, *h_rcol = nullptr;
   double* h_stage = nullptr;  // loopback staging buffer
   bool auto_halo = false;     // library performs the (loopback) exchange itself
+  double* Fexp = nullptr;     // sdrt_face_flux: per-ext-point common flux export (residual only)
 };
 
 // Dense operator in DMMA fragment order (simplex.cuh SOpF): rows padded to 8, columns
@@ -519,19 +524,34 @@ static int cub_points(int etype, int D, int degree) {
   return D == 2 ? n * n : n * n * n;
 }
 
+// Which path a context runs: the fused tensor / simplex element kernels, or the generic
+// operator path (unsupported element-degree-equation combinations, or the
+// SDRT_FORCE_GENERIC=1 cross-check hook).  Decided before the workspace is planned so
+// each path reserves only its own buffers.
+enum PathKind { PATH_GENERIC = 0, PATH_TENSOR = 1, PATH_SIMPLEX = 2 };
+static PathKind choose_path(const Mesh& m, const sdrt_physics* ph) {
+  const char* fg = getenv("SDRT_FORCE_GENERIC");
+  if (fg && fg[0] == '1') return PATH_GENERIC;
+  if (etype_tensor(m.etype)) return tensor_supported(m.nd, m.p, ph->eq) ? PATH_TENSOR : PATH_GENERIC;
+  return simplex_supported(m.nd, m.p, ph->eq) ? PATH_SIMPLEX : PATH_GENERIC;
+}
+
 static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph, std::vector<OpHost>* packed) {
   const RefElement& r = O.ref;
   int D = m.nd, NV = nvars(ph->eq, D);
   bool visc = ph->eq == SDRT_EQ_LINADVDIFF || ph->eq == SDRT_EQ_NS;
+  const bool gen = choose_path(m, ph) == PATH_GENERIC;
   size_t col = (size_t)NV * m.K_pad * sizeof(double);
   Plan p;
   size_t o = 0;
-  p.off_uext = o; o += align256(r.next * col);
-  p.off_xg = o; o += align256((r.next + r.nu) * col);
-  p.off_q = o; o += visc ? align256((size_t)r.nsol * D * col) : 0;
-  p.off_qext = o; o += visc ? align256((size_t)r.next * D * col) : 0;
-  p.off_qu = o; o += visc ? align256((size_t)r.nu * D * col) : 0;
-  p.off_xd = o; o += align256((r.next + (size_t)D * r.nu) * col);
+  // generic-path intermediates (Appendix-B products in HBM); none on the fused paths
+  p.off_uext = o; o += gen ? align256(r.next * col) : 0;
+  p.off_xg = o; o += gen ? align256((r.next + r.nu) * col) : 0;
+  p.off_q = o; o += gen && visc ? align256((size_t)r.nsol * D * col) : 0;
+  p.off_qext = o; o += gen && visc ? align256((size_t)r.next * D * col) : 0;
+  p.off_qu = o; o += gen && visc ? align256((size_t)r.nu * D * col) : 0;
+  p.off_xd = o; o += gen ? align256((r.next + (size_t)D * r.nu) * col) : 0;
+  // R~ (generic) / R_int (fused, viscous), the RK stage register and accumulator
   p.off_r = o; o += align256((size_t)r.nsol * col);
   p.off_us = o; o += align256((size_t)r.nsol * col);
   p.off_acc = o; o += align256((size_t)r.nsol * col);
@@ -539,7 +559,7 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   build_ops(O, D, ops);
   size_t ob = 0;
   std::vector<OpHost> pk;
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < (gen ? 4 : 0); ++i) {
     pk.push_back(pack(ops[i]));
     ob += align256(pk.back().ptr.size() * sizeof(int)) + align256(pk.back().col.size() * sizeof(int) + 4) +
           align256(pk.back().val.size() * sizeof(double) + 8);
@@ -548,7 +568,7 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.ops_bytes = ob;
   p.off_xm = o; o += align256((size_t)m.nsub * r.next * sizeof(ExtMetric));
   p.off_bad = o; o += 256;
-  size_t tb = align256((size_t)r.next * NV * m.Kt * sizeof(double));
+  size_t tb = gen ? 0 : align256((size_t)r.next * NV * m.Kt * sizeof(double));  // fused: trace arrays
   p.off_tu0 = o; o += tb;
   p.off_tu1 = o; o += tb;
   p.off_tg = o; o += tb;
@@ -656,9 +676,9 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     c->ACC = (double*)(base + p.off_acc);
     c->xm = (ExtMetric*)(base + p.off_xm);
     c->bad = (unsigned long long*)(base + p.off_bad);
-    // operators
+    // operators (generic path)
     size_t o = p.off_ops;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < (int)pk.size(); ++i) {
       OpHost& h = pk[i];
       int* dptr = (int*)(base + o);
       CUDA_OK(cudaMemcpyAsync(dptr, h.ptr.data(), h.ptr.size() * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -756,8 +776,15 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     // generic operator path, a test hook for cross-checking the two)
     c->etype = m.etype;
     c->p = m.p;
-    const char* fg = getenv("SDRT_FORCE_GENERIC");
-    c->fused = etype_tensor(m.etype) && !(fg && fg[0] == '1') && tensor_supported(m.nd, m.p, ph->eq);
+    const PathKind path = choose_path(m, ph);
+    c->fused = path == PATH_TENSOR;
+    if (c->fused && (int64_t)r.next * c->nv * m.Kt >= (int64_t(1) << 31)) {
+      // the tensor kernels index trace arrays [N_ext][N_V][K_t] in 32-bit arithmetic
+      delete c;
+      set_error("unsupported: mesh too large for the fused tensor kernels (N_ext N_V K_trace >= 2^31; "
+                "hex p=3 Navier-Stokes: K < 4.4e6 elements per rank)");
+      return SDRT_E_UNSUPPORTED;
+    }
     if (c->fused) {
       TensorGeom& t = c->tg;
       std::memset(&t, 0, sizeof(t));
@@ -812,7 +839,7 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       c->Tu[1] = (double*)(base + p.off_tu1);
       c->Tg = (double*)(base + p.off_tg);
     }
-    c->sfused = !etype_tensor(m.etype) && !(fg && fg[0] == '1') && simplex_supported(m.nd, m.p, ph->eq);
+    c->sfused = path == PATH_SIMPLEX;
     if (O.scheme != 0 && !c->fused && !c->sfused) {
       delete c;
       set_error("unsupported: FR schemes run on the fused element kernels");
@@ -1017,7 +1044,8 @@ static void residual_impl(sdrt_ctx* c, const double* U, int stage, double dt, do
   }
   {
     Mark mk(c, st, T_FFLUX);
-    k_face_flux<EQ, D><<<dim3(gx, c->next), 256, 0, st>>>(g, c->ph, c->xm, c->Uext, c->Qext, c->Xd);
+    k_face_flux<EQ, D><<<dim3(gx, c->next), 256, 0, st>>>(g, c->ph, c->xm, c->Uext, c->Qext, c->Xd,
+                                                                             c->Fexp);
   }
   apply(c, T_DIV, c->op[3], c->Xd, c->R, W, st);                                 // R~ = Dv [D~; F~_u]
   {
@@ -1095,6 +1123,7 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
   b.Tu_next = c->Tu[c->cur ^ 1];
   b.Tg = c->Tg;
   b.Rv = c->R;
+  b.Fexp = stage < 0 ? c->Fexp : nullptr;
   if (c->visc) {
     {
       Mark mk(c, st, T_FA);
@@ -1133,6 +1162,7 @@ static void sfused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, d
   b.Tg = c->Tg;
   b.Rint = c->R;
   b.xm = c->xm;
+  b.Fexp = stage < 0 ? c->Fexp : nullptr;
   if (c->visc) {
     {
       Mark mk(c, st, T_SA);
@@ -1196,6 +1226,17 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
     CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })
+}
+
+sdrt_status sdrt_face_flux(sdrt_ctx* c, const double* d_U, double* d_dUdt, double* d_F, void* stream) {
+  if (!c || !d_F) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  c->Fexp = d_F;
+  const sdrt_status st = sdrt_residual(c, d_U, d_dUdt, stream);
+  c->Fexp = nullptr;
+  return st;
 }
 
 sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int check_every, void* stream) {

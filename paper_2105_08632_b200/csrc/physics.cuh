@@ -183,63 +183,66 @@ struct Phys {
     }
   }
 
+  // ---- common fluxes with explicitly rounded arithmetic (reading O28) ----------------
+  // The fused kernels evaluate a face point's common flux on BOTH sides of the face,
+  // from bit-identical inputs, in whichever inlined copy of the face code owns each
+  // side's item.  With free FMA contraction the compiler may fuse different products
+  // in different copies (measured: 1-ulp differences on tets with eta != 0), so every
+  // operation of the common flux is an explicit IEEE op (__dmul_rn / __dadd_rn /
+  // __fma_rn, IEEE division and sqrt): the same inputs give the same bits everywhere.
+  static __device__ __forceinline__ double dot_rn(const double* a, const double* b) {
+    double s = __dmul_rn(a[0], b[0]);
+#pragma unroll
+    for (int d = 1; d < D; ++d) s = __fma_rn(a[d], b[d], s);
+    return s;
+  }
+  // Euler flux along n plus the Rusanov wave speed |v.n| + a of one state
+  static __device__ __forceinline__ double euler_dir_rn(const PhysDev& ph, const double* u, const double* n,
+                                                        double* f) {
+    const double ir = 1.0 / u[0];
+    const double vn = __dmul_rn(dot_rn(u + 1, n), ir);
+    const double vv = __dmul_rn(dot_rn(u + 1, u + 1), ir);                          // rho |v|^2
+    const double p = __dmul_rn(ph.gamma - 1.0, __fma_rn(-0.5, vv, u[D + 1]));
+    f[0] = __dmul_rn(u[0], vn);
+#pragma unroll
+    for (int i = 0; i < D; ++i) f[1 + i] = __fma_rn(p, n[i], __dmul_rn(u[1 + i], vn));
+    f[D + 1] = __dmul_rn(__dadd_rn(u[D + 1], p), vn);
+    return __dadd_rn(fabs(vn), sqrt(__dmul_rn(__dmul_rn(ph.gamma, p), ir)));
+  }
+
   // convective common flux (upwind LF for linear, Rusanov otherwise) along n
   static __device__ __forceinline__ void conv_common(const PhysDev& ph, const double* uL, const double* uR,
                                                      const double* n, double* F) {
     if constexpr (NV == 1) {
-      double cn = 0.0;
-#pragma unroll
-      for (int d = 0; d < D; ++d) cn += ph.c[d] * n[d];
-      F[0] = 0.5 * cn * (uL[0] + uR[0]) + 0.5 * fabs(cn) * (uL[0] - uR[0]);
+      const double cn = dot_rn(ph.c, n);
+      F[0] = __fma_rn(__dmul_rn(0.5, fabs(cn)), __dsub_rn(uL[0], uR[0]),
+                      __dmul_rn(__dmul_rn(0.5, cn), __dadd_rn(uL[0], uR[0])));
     } else {
       double fL[NV], fR[NV];
-      conv_dir(ph, uL, n, fL);
-      conv_dir(ph, uR, n, fR);
-      const double irL = 1.0 / uL[0], irR = 1.0 / uR[0];
-      double vnL = 0.0, vnR = 0.0, vvL = 0.0, vvR = 0.0;
+      const double sL = euler_dir_rn(ph, uL, n, fL), sR = euler_dir_rn(ph, uR, n, fR);
+      const double hphi = __dmul_rn(0.5, fmax(sL, sR));
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        vnL += uL[1 + d] * n[d];
-        vnR += uR[1 + d] * n[d];
-        vvL += uL[1 + d] * uL[1 + d];
-        vvR += uR[1 + d] * uR[1 + d];
-      }
-      vnL *= irL;
-      vnR *= irR;
-      const double pL = (ph.gamma - 1.0) * (uL[D + 1] - 0.5 * vvL * irL);
-      const double pR = (ph.gamma - 1.0) * (uR[D + 1] - 0.5 * vvR * irR);
-      const double phi = fmax(fabs(vnL) + sqrt(ph.gamma * pL * irL), fabs(vnR) + sqrt(ph.gamma * pR * irR));
-#pragma unroll
-      for (int a = 0; a < NV; ++a) F[a] = 0.5 * (fL[a] + fR[a]) + 0.5 * phi * (uL[a] - uR[a]);
+      for (int a = 0; a < NV; ++a)
+        F[a] = __fma_rn(hphi, __dsub_rn(uL[a], uR[a]), __dmul_rn(0.5, __dadd_rn(fL[a], fR[a])));
     }
   }
 
-  // conv_common along the axis normal +e_D0 (tensor faces): the same Rusanov flux without
-  // the structural zeros of the normal
+  // conv_common along the axis normal +e_D0 (tensor faces): the same Rusanov flux
   template <int D0>
   static __device__ __forceinline__ void conv_common_axis(const PhysDev& ph, const double* uL, const double* uR,
                                                           double* F) {
-    if constexpr (NV == 1) {
-      const double cn = ph.c[D0];
-      F[0] = 0.5 * cn * (uL[0] + uR[0]) + 0.5 * fabs(cn) * (uL[0] - uR[0]);
-    } else {
-      double fL[NV], fR[NV];
-      conv_axis<D0>(ph, uL, 1.0, fL);
-      conv_axis<D0>(ph, uR, 1.0, fR);
-      const double irL = 1.0 / uL[0], irR = 1.0 / uR[0];
-      double vvL = 0.0, vvR = 0.0;
-#pragma unroll
-      for (int d = 0; d < D; ++d) {
-        vvL += uL[1 + d] * uL[1 + d];
-        vvR += uR[1 + d] * uR[1 + d];
-      }
-      const double vnL = uL[1 + D0] * irL, vnR = uR[1 + D0] * irR;
-      const double pL = (ph.gamma - 1.0) * (uL[D + 1] - 0.5 * vvL * irL);
-      const double pR = (ph.gamma - 1.0) * (uR[D + 1] - 0.5 * vvR * irR);
-      const double phi = fmax(fabs(vnL) + sqrt(ph.gamma * pL * irL), fabs(vnR) + sqrt(ph.gamma * pR * irR));
-#pragma unroll
-      for (int a = 0; a < NV; ++a) F[a] = 0.5 * (fL[a] + fR[a]) + 0.5 * phi * (uL[a] - uR[a]);
-    }
+    double n[3] = {0.0, 0.0, 0.0};
+    n[D0] = 1.0;
+    conv_common(ph, uL, uR, n, F);
+  }
+
+  // LDG part of the common flux (l.330-335, O10) from the LDG-weighted published
+  // viscous normal flux gsum = (1/2+b) g_L + (1/2-b) g_R: F + gsum + eta (u_L - u_R)
+  static __device__ __forceinline__ double ldg_rn(double F, double gsum, double eta, double uL, double uR) {
+    return __dadd_rn(F, __fma_rn(eta, __dsub_rn(uL, uR), gsum));
+  }
+  static __device__ __forceinline__ double gsum_rn(double wl, double gL, double wr, double gR) {
+    return __fma_rn(wr, gR, __dmul_rn(wl, gL));
   }
 
   // common normal flux along nL (left element's unit normal)

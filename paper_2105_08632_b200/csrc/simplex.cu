@@ -342,7 +342,7 @@ struct NbGather {
       for (int v = 0; v < NV; ++v) {
         const double own = sUe[(rho * NV + v) * E + el];
         const double uL = left ? own : nb[k][v], uR = left ? nb[k][v] : own;
-        sC[(rho * NV + v) * E + el] = wl * uL + wr * uR;
+        sC[(rho * NV + v) * E + el] = __fma_rn(wr, uR, __dmul_rn(wl, uL));  // explicit: same bits both sides
       }
     }
   }
@@ -392,8 +392,8 @@ struct FluxGather {
           if (one) {
             gs[k][v] = Tg[gi * NV + v];
           } else {
-            double a = wl * Tg[((int64_t)rL * Kp + eL) * NV + v];
-            gs[k][v] = fma(wr, Tg[((int64_t)rR * Kp + eR) * NV + v], a);
+            gs[k][v] = Phys<EQ_NS, D>::gsum_rn(wl, Tg[((int64_t)rL * Kp + eL) * NV + v], wr,
+                                               Tg[((int64_t)rR * Kp + eR) * NV + v]);
           }
         }
       }
@@ -803,8 +803,8 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           double a = 0.0;
-          if (wl != 0.0) a = wl * b.Tg[((int64_t)rL * Kp + eL) * NV + v];
-          if (wr != 0.0) a = fma(wr, b.Tg[((int64_t)rR * Kp + eR) * NV + v], a);
+          if (wl != 0.0) a = __dmul_rn(wl, b.Tg[((int64_t)rL * Kp + eL) * NV + v]);
+          if (wr != 0.0) a = __fma_rn(wr, b.Tg[((int64_t)rR * Kp + eR) * NV + v], a);
           gsum[v] = a;
         }
       }
@@ -823,8 +823,9 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       double Fv = F[v];
-      if constexpr (Ph::VISC) Fv += gsum[v] + ph.eta * (uL[v] - uR[v]);
+      if constexpr (Ph::VISC) Fv = Ph::ldg_rn(Fv, gsum[v], ph.eta, uL[v], uR[v]);
       sUe[(rho * NV + v) * E + el] = sc * Fv;
+      if (b.Fexp) b.Fexp[((int64_t)rho * NV + v) * g.Kp + e] = Fv;  // O28 export
     }
   };
 #if SDRT_SB_PF
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
       const double wl = 0.5 + ph.beta, wr = 0.5 - ph.beta;
       const double w1 = (wl == 0.0) != (wr == 0.0) ? (wl != 0.0 ? wl : wr) : 1.0;
 #pragma unroll
-      for (int v = 0; v < NV; ++v) gk[v] = Ph::VISC ? w1 * fg.gs[Ph::VISC ? k : 0][v] : 0.0;
+      for (int v = 0; v < NV; ++v) gk[v] = Ph::VISC ? __dmul_rn(w1, fg.gs[Ph::VISC ? k : 0][v]) : 0.0;
     }
     if (item < S::next * E) face_flux(item, fg.un[k], gk);
   }

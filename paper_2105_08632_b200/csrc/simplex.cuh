@@ -43,6 +43,7 @@ struct SimplexBufs {
   double* Tg;
   double* Rint;          // internal-flux divergence M13 M19 P2 F~ [N_sol][N_V][Kp] (kernel A -> B)
   const ExtMetric* xm;   // [nsub][N_ext]
+  double* Fexp = nullptr;  // optional (residual only): common flux F per own ext point [N_ext][N_V][Kp]
 };
 
 // TMA descriptors of [N_sol N_V rows][Kp] arrays (cached per pointer), tiles of E elements

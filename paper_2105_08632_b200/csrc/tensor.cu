@@ -874,14 +874,18 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
           double gsum = 0.0;
-          if (wl != 0.0) gsum = wl * tga[k][v];
-          if (wr != 0.0) gsum = fma(wr, tgb[k][v], gsum);
-          F[v] += gsum + ph.eta * (uL[v] - uR[v]);
+          if (wl != 0.0) gsum = __dmul_rn(wl, tga[k][v]);
+          if (wr != 0.0) gsum = __fma_rn(wr, tgb[k][v], gsum);
+          F[v] = Ph::ldg_rn(F[v], gsum, ph.eta, uL[v], uR[v]);
         }
       }
       const int kf = side ? NF - 1 : 0;
 #pragma unroll
       for (int v = 0; v < NV; ++v) sF[((t * NF + kf) * NV + v) * E + el] = sface * F[v];
+      if (b.Fexp && e0 + el < g.K) {  // O28 export: F at the own ext point (2d + side, t)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) b.Fexp[((int64_t)((2 * d + side) * NL + t) * NV + v) * g.Kp + e0 + el] = F[v];
+      }
     }
     if constexpr (d + 1 < D) load_dir(std::integral_constant<int, d + 1>{});
     if (d == 0) mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed

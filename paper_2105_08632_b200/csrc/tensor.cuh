@@ -54,6 +54,7 @@ struct TensorBufs {
   double* Tu_next;    // traces of the stage output
   double* Tg;         // published viscous normal-flux traces [N_ext][N_V][Kp]
   double* Rv;         // viscous internal-flux divergence M13 F~_v [N_sol][N_V][Kp] (kernel A -> B)
+  double* Fexp = nullptr;  // optional (residual only): common flux F per own ext point [N_ext][N_V][Kp]
 };
 
 // TMA descriptors of the element-major state-like arrays [N_sol N_V rows][Kp] seen by

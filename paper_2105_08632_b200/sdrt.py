@@ -68,6 +68,7 @@ lib.sdrt_ctx_workspace_bytes.argtypes = [_vp, _vp, ctypes.POINTER(PhysicsT)]
 lib.sdrt_ctx_workspace_bytes.restype = ctypes.c_size_t
 lib.sdrt_ctx_create.argtypes = [_vp, _vp, ctypes.POINTER(PhysicsT), _vp, ctypes.c_size_t, _vp, ctypes.POINTER(_vp)]
 lib.sdrt_residual.argtypes = [_vp, _vp, _vp, _vp]
+lib.sdrt_face_flux.argtypes = [_vp, _vp, _vp, _vp, _vp]
 lib.sdrt_rk_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
 lib.sdrt_rk54_step.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int, _vp]
 lib.sdrt_diagnostics.argtypes = [_vp, _vp, _vp, _vp]
@@ -93,7 +94,7 @@ lib.sdrt_ctx_destroy.restype = None
 EXPORTED = ["sdrt_abi_version", "sdrt_last_error", "sdrt_mesh_create", "sdrt_mesh_info",
             "sdrt_mesh_export_maps", "sdrt_mesh_sol_coords", "sdrt_mesh_detj", "sdrt_mesh_destroy",
             "sdrt_operators_build", "sdrt_operators_get", "sdrt_operators_destroy",
-            "sdrt_ctx_workspace_bytes", "sdrt_ctx_create", "sdrt_residual", "sdrt_rk_step",
+            "sdrt_ctx_workspace_bytes", "sdrt_ctx_create", "sdrt_residual", "sdrt_face_flux", "sdrt_rk_step",
             "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_kernel_times",
             "sdrt_mesh_set_halo", "sdrt_mesh_halo_lists", "sdrt_mesh_neighbor", "sdrt_halo_info",
             "sdrt_halo_pack", "sdrt_halo_unpack", "sdrt_stage_traces", "sdrt_stage_grad", "sdrt_stage_flux"]
@@ -233,6 +234,10 @@ def ctx_create(m, o, ph, ws_ptr, ws_bytes, stream):
 
 def residual(ctx, U_ptr, dUdt_ptr, stream):
     _check(lib.sdrt_residual(ctx, _vp(U_ptr), _vp(dUdt_ptr), _vp(stream)))
+
+
+def face_flux(ctx, U_ptr, dUdt_ptr, F_ptr, stream):
+    _check(lib.sdrt_face_flux(ctx, _vp(U_ptr), _vp(dUdt_ptr), _vp(F_ptr), _vp(stream)))
 
 
 def rk_step(ctx, U_ptr, dt, nsteps, check_every=0, stream=0):

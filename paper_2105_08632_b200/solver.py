@@ -62,6 +62,15 @@ class Solver:
         sdrt.residual(self.ctx, U.data_ptr(), out.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream)
         return out
 
+    def face_flux(self, U):
+        """(dU/dt, F): the residual and the common flux F each element applied at each of
+        its external points, [N_ext][N_V][K_pad] (reading O28; sdrt_face_flux)."""
+        out = torch.empty_like(U)
+        F = torch.zeros((self.info["next"], self.nv, self.info["K_pad"]), dtype=torch.float64, device=self.device)
+        sdrt.face_flux(self.ctx, U.data_ptr(), out.data_ptr(), F.data_ptr(),
+                       torch.cuda.current_stream(self.device).cuda_stream)
+        return out, F
+
     def rk_step(self, U, dt, nsteps=1, check_every=0):
         sdrt.rk_step(self.ctx, U.data_ptr(), dt, nsteps, check_every,
                      torch.cuda.current_stream(self.device).cuda_stream)
