@@ -227,13 +227,37 @@ struct Phys {
     }
   }
 
+  // Euler flux along +e_D0 and the Rusanov wave speed (explicitly rounded, no
+  // structural zeros of the normal)
+  template <int D0>
+  static __device__ __forceinline__ double euler_axis_rn(const PhysDev& ph, const double* u, double* f) {
+    const double ir = 1.0 / u[0];
+    const double vn = __dmul_rn(u[1 + D0], ir);
+    const double vv = __dmul_rn(dot_rn(u + 1, u + 1), ir);
+    const double p = __dmul_rn(ph.gamma - 1.0, __fma_rn(-0.5, vv, u[D + 1]));
+    f[0] = u[1 + D0];
+#pragma unroll
+    for (int i = 0; i < D; ++i) f[1 + i] = i == D0 ? __fma_rn(u[1 + i], vn, p) : __dmul_rn(u[1 + i], vn);
+    f[D + 1] = __dmul_rn(__dadd_rn(u[D + 1], p), vn);
+    return __dadd_rn(fabs(vn), sqrt(__dmul_rn(__dmul_rn(ph.gamma, p), ir)));
+  }
+
   // conv_common along the axis normal +e_D0 (tensor faces): the same Rusanov flux
   template <int D0>
   static __device__ __forceinline__ void conv_common_axis(const PhysDev& ph, const double* uL, const double* uR,
                                                           double* F) {
-    double n[3] = {0.0, 0.0, 0.0};
-    n[D0] = 1.0;
-    conv_common(ph, uL, uR, n, F);
+    if constexpr (NV == 1) {
+      const double cn = ph.c[D0];
+      F[0] = __fma_rn(__dmul_rn(0.5, fabs(cn)), __dsub_rn(uL[0], uR[0]),
+                      __dmul_rn(__dmul_rn(0.5, cn), __dadd_rn(uL[0], uR[0])));
+    } else {
+      double fL[NV], fR[NV];
+      const double sL = euler_axis_rn<D0>(ph, uL, fL), sR = euler_axis_rn<D0>(ph, uR, fR);
+      const double hphi = __dmul_rn(0.5, fmax(sL, sR));
+#pragma unroll
+      for (int a = 0; a < NV; ++a)
+        F[a] = __fma_rn(hphi, __dsub_rn(uL[a], uR[a]), __dmul_rn(0.5, __dadd_rn(fL[a], fR[a])));
+    }
   }
 
   // LDG part of the common flux (l.330-335, O10) from the LDG-weighted published

@@ -718,7 +718,7 @@ struct SLayoutB {
   static constexpr int TOTAL = 4 * U + UE + UU + F;
 };
 
-template <int D, int P, int EQ, int E>
+template <int D, int P, int EQ, int E, bool FEXP = false>
 __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b, int stage,
                                                 double dt, const __grid_constant__ STileMaps tm) {
   pdl_wait();
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
       double Fv = F[v];
       if constexpr (Ph::VISC) Fv = Ph::ldg_rn(Fv, gsum[v], ph.eta, uL[v], uR[v]);
       sUe[(rho * NV + v) * E + el] = sc * Fv;
-      if (b.Fexp) b.Fexp[((int64_t)rho * NV + v) * g.Kp + e] = Fv;  // O28 export
+      if (FEXP) b.Fexp[((int64_t)rho * NV + v) * g.Kp + e] = Fv;  // O28 export (residual only)
     }
   };
 #if SDRT_SB_PF
@@ -1040,7 +1040,7 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
       }
     }
   } else if (which == 1) {
-    auto k = ks_stage<D, P, EQ, C::E>;
+    auto k = b.Fexp ? ks_stage<D, P, EQ, C::E, true> : ks_stage<D, P, EQ, C::E>;
     sset_smem((const void*)k, C::SMEM_B);
     CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SB_NT, C::SMEM_B, st, g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true)));
   } else {

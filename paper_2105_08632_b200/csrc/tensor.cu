@@ -50,6 +50,11 @@
 #ifndef SDRT_TA_GPAIR
 #define SDRT_TA_GPAIR 2
 #endif
+// kernel A internal fluxes and published g by register-blocked line items (visc_line):
+// 0 off (per-point items), 1 on
+#ifndef SDRT_TA_LINE
+#define SDRT_TA_LINE 1
+#endif
 
 namespace sdrt {
 
@@ -519,6 +524,100 @@ __device__ __forceinline__ void visc_internal2(const TensorGeom& g, const Line1D
   }
 }
 
+// Register-blocked line item (SDRT_TA_LINE): one item = one d-line t of one element.
+// The outputs of the line -- its NI internal flux points and the published end(s) --
+// are produced in passes of LGRP outputs: per pass, every component the axis physics
+// reads (u and the gradient entries; the others are dead code) is loaded from shared
+// memory once and interpolated to the pass's outputs from registers (the line
+// operators are kernel parameters: constant-bank DFMA operands), so one shared-memory
+// load feeds LGRP DFMAs instead of one, with LGRP x (N_V + D N_V) accumulators live.
+// Outputs: internal transformed fluxes F~ = detJ J^-1 (f^c - f^v) -> sF[t][a][v][el],
+// published viscous normal flux g = n_L . f^v at the end(s) -> Tg (PAPER.md l.305-311,
+// l.330-335; B7 l.2927-2932).
+// scalar equations (N_V = 1): all outputs of a line in one pass
+#ifndef SDRT_TA_LGRP
+#define SDRT_TA_LGRP 4
+#endif
+// systems (N_V > 1, the NS registers): line items on/off, outputs per pass, and whether
+// each pass is its own item (SDRT_TA_LSPLIT_SYS = 1).  Measured on c4 (hex p=3 NS, kernel
+// A per launch): per-point items 251 us; line items with 128-thread CTAs (254 registers,
+// 8 warps / SM) 253 us; one item per 2-output pass at 256 threads (spills) 291 us;
+// per-output passes 337 us.  The NS line items need ~2x the registers, which halves the
+// resident warps and cancels the 40 % cut in shared-memory wavefronts; off for systems.
+#ifndef SDRT_TA_LINE_SYS
+#define SDRT_TA_LINE_SYS 0
+#endif
+#ifndef SDRT_TA_LGRP_SYS
+#define SDRT_TA_LGRP_SYS 2
+#endif
+#ifndef SDRT_TA_LSPLIT_SYS
+#define SDRT_TA_LSPLIT_SYS 1
+#endif
+// PUB: published ends, bit 0 = the x_d = -1 end (side 0), bit 1 = the x_d = +1 end
+// G: outputs per pass; SPLIT: the line's passes are separate items (gsel = this item's)
+template <int D, int P, int EQ, int E, int d, int NI, int PUB, int G, bool SPLIT>
+__device__ __forceinline__ void visc_line(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                          const double* sQ, double* sF, double* __restrict__ Tg, int64_t e0, int t,
+                                          int el, int gsel) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NS = T::NS, NL = T::NL;
+  constexpr int NC = NV + D * NV;  // components: u_v, then q[dd][v]
+  constexpr int NO = NI + (PUB & 1) + (PUB >> 1 & 1);
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  const double wf = g.detJ * g.jinv[d];
+  const int64_t e = e0 + el;
+#pragma unroll
+  for (int g0 = 0; g0 < NO; g0 += G) {
+    if (SPLIT && g0 != gsel * G) continue;
+    double o[G][NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double* base = c < NV ? sU + (lb * NV + c) * E + el : sQ + (((c / NV - 1) * NS + lb) * NV + c % NV) * E + el;
+      double x[n];
+#pragma unroll
+      for (int i = 0; i < n; ++i) x[i] = base[i * ls * NV * E];
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int k = g0 + j;
+        if (k >= NO) break;
+        if (k < NI) {
+          if constexpr (NI == n) {  // FR: the flux points are the solution points (Iint = I)
+            o[j][c] = x[k];
+          } else {
+            double s = L.Iint[k][0] * x[0];
+#pragma unroll
+            for (int i = 1; i < n; ++i) s = fma(L.Iint[k][i], x[i], s);
+            o[j][c] = s;
+          }
+        } else {
+          const int side = PUB == 3 ? k - NI : (PUB == 2 ? 1 : 0);
+          o[j][c] = interp_end<n>(L.Iend[side], x);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int k = g0 + j;
+      if (k >= NO) break;
+      if (k < NI) {
+        double fc[NV], fv[NV];
+        Ph::template conv_axis<d>(ph, o[j], wf, fc);
+        Ph::template visc_axis<d>(ph, o[j], o[j] + NV, wf, fv);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) sF[((t * NI + k) * NV + v) * E + el] = fc[v] + fv[v];
+      } else if (e < g.K) {
+        const int side = PUB == 3 ? k - NI : (PUB == 2 ? 1 : 0);
+        double gv[NV];
+        Ph::template visc_axis<d>(ph, o[j], o[j] + NV, 1.0, gv);  // canonical (left) normal +e_d
+        const int ext = (2 * d + side) * NL + t;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) Tg[((int64_t)ext * NV + v) * g.Kt + e] = gv[v];
+      }
+    }
+  }
+}
+
 // FP64 tensor-core (DMMA m8n8k4) form of a d-line's interpolations (SDRT_TA_DMMA):
 // one warp per line t, the 8 x 4 operator [Iint (NI rows); Iend (2 rows); 0] applied to
 // every needed component (u_v and the gradient entries, the line's points as k, the 8
@@ -656,13 +755,28 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
     // phase ph_: fluxes of direction ph_ (buffer ph_&1) [+ publish g in phase 0], then
     // the divergence of direction ph_-1 (buffer (ph_-1)&1) whose partial sums were
     // requested from L2 before the flux work
-    constexpr int CD = (NDI + NT - 1) / NT;
     const int dd = ph_ - 1;
-    double prev[CD][P + 1];
-    if (ph_ >= 2) {
+    // LINE mode with fewer line items than threads (NL E < NT): threads 0 .. NL E - 1
+    // run one line item each, the others all divergence items (so the heavy line work
+    // never holds the divergence prefetch registers)
+    constexpr bool LINE = (NV > 1 ? SDRT_TA_LINE_SYS : SDRT_TA_LINE) != 0 && SDRT_TA_DMMA == 0;
+    constexpr int LG = NV > 1 ? SDRT_TA_LGRP_SYS : SDRT_TA_LGRP;   // outputs per pass
+    constexpr bool LSP = NV > 1 && SDRT_TA_LSPLIT_SYS != 0;          // one item per pass
+    constexpr int NGRP = LSP ? (NI + 2 + LG - 1) / LG : 1;
+    constexpr int NLI = NL * E * NGRP;  // line items per direction
+    constexpr bool LSPLIT = LINE && NLI < NT;
+    constexpr int NDT = LSPLIT ? NT - NLI : NT;  // threads running divergence items
+    constexpr int CD = (NDI + NDT - 1) / NDT;
+    const bool divthr = !LSPLIT || (int)threadIdx.x >= NLI;
+    const int dtid = LSPLIT ? (int)threadIdx.x - NLI : (int)threadIdx.x;
+    // partial sums of R_int requested before the flux work (not in LSPLIT mode: there
+    // the divergence threads do no flux work, and the prefetch registers would be live
+    // across the line items in the register allocation)
+    double prev[LSPLIT ? 1 : CD][P + 1];
+    if (!LSPLIT && ph_ >= 2 && divthr) {
 #pragma unroll
       for (int k = 0; k < CD; ++k) {
-        const int item = threadIdx.x + k * NT;
+        const int item = dtid + k * NDT;
         const int el = item % E, r = item / E, v = r % NV, t = r / NV;
         if (item < NDI && e0 + el < g.K) {
           const int lb = lbase<D, P>(dd, t), ls = lstr<D, P>(dd);
@@ -673,16 +787,17 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
       }
     }
     constexpr bool LDMMA = SDRT_TA_DMMA != 0 && E == 8 && Ph::VISC && NV > 1;
-    const int nA = (ph_ == 0 && !LDMMA) ? npub : 0;
+    const int nA = (ph_ == 0 && !LDMMA && !LINE) ? npub : 0;
     constexpr bool PAIR = SDRT_TA_PAIR == 1 || (SDRT_TA_PAIR == 2 && NV == 1);
-    const int nB = (ph_ < D && !LDMMA) ? (PAIR ? NFI / 2 : NFI) : 0;
+    const int nB = (ph_ < D && !LDMMA && !LINE) ? (PAIR ? NFI / 2 : NFI) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
     // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
     auto divergence = [&]() {
       const double* f0 = sF + (DBUF ? (dd & 1) * NFB : 0);
+      if (!divthr) return;
 #pragma unroll
       for (int k = 0; k < CD; ++k) {
-        const int item = threadIdx.x + k * NT;
+        const int item = dtid + k * NDT;
         const int el = item % E, r = item / E, v = r % NV, t = r / NV;
         if (item >= NDI || e0 + el >= g.K) continue;
         const int lb = lbase<D, P>(dd, t), ls = lstr<D, P>(dd);
@@ -692,7 +807,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         double* dst = b.Rv + (int64_t)(lb * NV + v) * g.Kp + e0 + el;
 #pragma unroll
         for (int i = 0; i <= P; ++i) {
-          double acc = ph_ >= 2 ? prev[k][i] : 0.0;
+          double acc = 0.0;
+          if constexpr (LSPLIT) {
+            if (ph_ >= 2) acc = dst[(int64_t)i * ls * NV * g.Kp];
+          } else if (ph_ >= 2) {
+            acc = prev[k][i];
+          }
 #pragma unroll
           for (int a = 0; a < NI; ++a) acc = fma(L.Dfl[i][a + 1], f[a], acc);
           dst[(int64_t)i * ls * NV * g.Kp] = acc;
@@ -712,6 +832,26 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
           else if (ph_ == 1) visc_line_dmma<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, pub0, pub1);
           else if constexpr (D == 3) visc_line_dmma<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, pub0, pub1);
         }
+      }
+    }
+    if constexpr (LINE) {
+      const int pubm = (pub0 ? 1 : 0) | (pub1 ? 2 : 0);
+      // items: (line, element[, pass]); LSP: one item per pass of LG outputs (more
+      // items, each loading the line once) instead of one per line
+      auto line_d = [&](auto dc, int t, int el, double* f1, int gs) {
+        constexpr int d = decltype(dc)::value;
+        switch (pubm) {  // block-uniform: one instantiation per published-side set
+          case 2: visc_line<D, P, EQ, E, d, NI, 2, LG, LSP>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, el, gs); break;
+          case 1: visc_line<D, P, EQ, E, d, NI, 1, LG, LSP>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, el, gs); break;
+          default: visc_line<D, P, EQ, E, d, NI, 3, LG, LSP>(g, L, ph, sU, sQ, f1, b.Tg, e0, t, el, gs); break;
+        }
+      };
+      for (int it = threadIdx.x; it < (ph_ < D ? NLI : 0); it += LSPLIT ? NLI : NT) {
+        const int el = it % E, t = (it / E) % NL, gs = it / (E * NL);
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        if (ph_ == 0) line_d(std::integral_constant<int, 0>{}, t, el, f1, gs);
+        else if (ph_ == 1) line_d(std::integral_constant<int, 1>{}, t, el, f1, gs);
+        else if constexpr (D == 3) line_d(std::integral_constant<int, 2>{}, t, el, f1, gs);
       }
     }
     for (int item = threadIdx.x; item < nA + nB; item += blockDim.x) {
@@ -749,7 +889,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
 // traces + LDG jump, l.312-340), the face part of the divergence M14 D~ (l.2919-2925),
 // [inviscid equations: also the internal fluxes and M13 F~, which kernel A does
 // otherwise], R~ = sum + R_int, -R~/detJ, RK4 update, new traces.
-template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI, bool FEXP = false>
 __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
                                                    double dt, const __grid_constant__ TileMaps tm) {
   pdl_wait();
@@ -882,7 +1022,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
       const int kf = side ? NF - 1 : 0;
 #pragma unroll
       for (int v = 0; v < NV; ++v) sF[((t * NF + kf) * NV + v) * E + el] = sface * F[v];
-      if (b.Fexp && e0 + el < g.K) {  // O28 export: F at the own ext point (2d + side, t)
+      if (FEXP && e0 + el < g.K) {  // O28 export (residual only): F at the own ext point (2d + side, t)
 #pragma unroll
         for (int v = 0; v < NV; ++v) b.Fexp[((int64_t)((2 * d + side) * NL + t) * NV + v) * g.Kp + e0 + el] = F[v];
       }
@@ -1073,7 +1213,12 @@ struct TCfg {
 #ifndef SDRT_TA_NT
 #define SDRT_TA_NT 256
 #endif
-  static constexpr int NTA = SDRT_TA_NT;
+// systems (N_V > 1): 128-thread CTAs so the register-blocked line items (SDRT_TA_LINE,
+// LGRP outputs per pass) get up to 255 registers at two CTAs per SM
+#ifndef SDRT_TA_NT_SYS
+#define SDRT_TA_NT_SYS 256
+#endif
+  static constexpr int NTA = NV > 1 ? SDRT_TA_NT_SYS : SDRT_TA_NT;
 #ifndef SDRT_TB_MINB
 #define SDRT_TB_MINB 2
 #endif
@@ -1135,7 +1280,7 @@ static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph
   } else {
     const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::E - 1) / C::E);
     if (grid == 0) return;
-    auto kb = kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI>;
+    auto kb = b.Fexp ? kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI, true> : kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI>;
     set_smem<D, P, EQ>((const void*)kb, C::smem_b(2, NI));
     CUDA_LAUNCH_OK(launch_pdl(kb, grid, C::NTB, C::smem_b(stage, NI), st, g, L, ph, b, stage, dt, maps_for(tma, b, true)));
   }

@@ -7,7 +7,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SDRT_LIB"] = os.path.join(ROOT, "paper_2105_08632_b200", "libsdrt_prof.so")
+os.environ.setdefault("SDRT_LIB", os.path.join(ROOT, "paper_2105_08632_b200", "libsdrt_prof.so"))
 import torch  # noqa: E402
 from paper_2105_08632_b200 import sdrt  # noqa: E402
 from paper_2105_08632_b200.solver import Solver  # noqa: E402
