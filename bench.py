@@ -8,12 +8,13 @@ configuration's full mesh.  value = N_sol * N_V * K_elems * 4 * steps (summed ov
 ranks) / max-over-ranks device time / 1e9  [GDOF-stage/s]  (1/PM of PAPER.md
 Eq. performance_per_iter_measure l.2942-2951 with N_RK = 4).
 
-N > 1 (torchrun, one rank per GPU): weak scaling with the element-partitioned path
+N > 1 (one rank per GPU; `--gpus N` without torchrun re-launches itself under
+torch.distributed.run): weak scaling with the element-partitioned path
 (paper_2105_08632_b200.dist): the global periodic mesh is the configuration's mesh
-repeated pgrid times (1: 1x1x1, 2: 2x1x1, 4: 2x2x1, 8: 2x2x2; same h, so each rank owns
-exactly the configuration's block) and face traces cross rank boundaries through NCCL
-point-to-point halo exchanges every stage.  --impl reference times the CPU oracle
-(rank 0 only).
+repeated pgrid times along the slow axes (3-D 2: 1x1x2, 4: 1x2x2, 8: 1x2x4; same h, so
+each rank owns exactly the configuration's block) and face traces cross rank boundaries
+through the library's own NCCL halo exchange (sdrt_ctx_attach_comm) every stage,
+overlapped with the interior tiles.  --impl reference times the CPU oracle (rank 0 only).
 """
 from __future__ import annotations
 
@@ -35,7 +36,7 @@ import numpy as np  # noqa: E402
 
 from sdrt_inputs import CONFIGS, initial_state  # noqa: E402
 
-METRIC = "SDRT residual GDOF-stage/s (fp64)"
+METRIC = "SDRT residual GDOF-stage/s (fp64) and % of HBM roofline at 1/2/4/8 B200"  # BASELINE.json
 # reference-arm sample size (patterns per axis) so K steps of the oracle take ~1 s each
 REF_SUBBOX = {"c1": 8, "c2": 40, "c3": 6, "c4": 8, "c5": 4}
 UNIT = "GDOF-stage/s"
@@ -264,6 +265,19 @@ def run_reference(args, cfg):
     return 0
 
 
+def relaunch(n):
+    """`python bench.py --gpus N` outside torchrun: run the same command as N ranks of one
+    node (torch.distributed.run, rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -279,6 +293,8 @@ def main():
                     help="rk4: classical (BASELINE.json configs); rk54: the paper's PM protocol (N_RK = 5)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -305,7 +321,8 @@ def main():
         hi = [l + (h - l) * g for l, h, g in zip(cfg.lo, cfg.hi, pgrid)]
         S = DistSolver(cfg.etype, cfg.p, Ng, cfg.lo, hi, cfg.eq, device=dev, pgrid=pgrid, scheme=args.scheme,
                        **cfg.physics_kwargs())
-        parallelism = f"element partition {'x'.join(map(str, pgrid))}, NCCL halo"
+        parallelism = (f"element partition {'x'.join(map(str, pgrid))} over {world} GPUs, halo exchange "
+                       f"inside libsdrt over NCCL ({S.transport}), overlapped with interior tiles")
     else:
         S = Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, scheme=args.scheme,
                    **cfg.physics_kwargs())
@@ -377,48 +394,28 @@ def main():
     value = total_dof_stages / (ms_max * 1e-3) / 1e9
 
     # ---------------------------------------------------------------- e2e (host buffers)
-    # Every step: host->device copy of the step's input state from pinned memory,
-    # sdrt_rk_step, device->host copy of the new state.  Steps rotate over three library
-    # contexts on three CUDA streams (triple buffering): a stream's chain H2D -> step ->
-    # D2H then covers three steps, so the copies of neighbouring steps overlap this one's
-    # kernels (with two buffers the chain of 2 copies + 1 step per two steps bounds the
-    # rate once a copy takes more than half a step).  The timed region spans all of them.
-    NBUF = 3 if world == 1 else 1
+    # A dependent trajectory through the public API with the state in host memory: every
+    # step copies the state host->device from pinned memory, runs sdrt_rk_step (one RK4
+    # step) and copies the new state device->host into the same pinned buffer, which is
+    # the next step's input.  Step i+1 consumes step i's output, so nothing overlaps.
     pin = torch.empty(S.shape, dtype=torch.float64).pin_memory()
     pin.copy_(U.cpu())
-    outs = [torch.empty_like(pin).pin_memory() for _ in range(NBUF)]
-    extra = []
-    if world > 1:  # ranks exchange halos in step order: one context, one stream
-        solvers, bufs = [S], [U]
-    else:
-        extra = [Solver(cfg.etype, cfg.p, cfg.N, cfg.lo, cfg.hi, cfg.eq, device=dev, scheme=args.scheme,
-                        **cfg.physics_kwargs()) for _ in range(NBUF - 1)]
-        solvers, bufs = [S] + extra, [U] + [torch.empty_like(U) for _ in range(NBUF - 1)]
-    side = [torch.cuda.Stream(dev) for _ in range(NBUF)]
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a0.record(stream)
-    for sd in side:
-        sd.wait_stream(stream)
     for i in range(args.steps):
-        k = i % NBUF
-        with torch.cuda.stream(side[k]):
-            bufs[k].copy_(pin, non_blocking=True)
-            step_fn(solvers[k])(bufs[k], cfg.dt, 1)
-            outs[k].copy_(bufs[k], non_blocking=True)
-    for sd in side:
-        stream.wait_stream(sd)
+        U.copy_(pin, non_blocking=True)
+        step_fn(S)(U, cfg.dt, 1)
+        pin.copy_(U, non_blocking=True)
     a1.record(stream)
     torch.cuda.synchronize(dev)
     te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_val = total_dof_stages / (float(te[0]) * 1e-3) / 1e9
-    e2e_ok = bool(torch.isfinite(torch.from_numpy(outs[(args.steps - 1) % NBUF].numpy()[:, :, :K])).all())
-    for s2 in extra:
-        s2.close()
+    e2e_ok = bool(torch.isfinite(pin[:, :, :K]).all())
     state_bytes = U.numel() * 8
 
     # ---------------------------------------------------------------- roofline
@@ -486,7 +483,8 @@ def main():
                "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,
                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                        "d2h_bytes_per_step": state_bytes, "result_finite": e2e_ok,
-                       "pipeline": f"{NBUF} contexts x {NBUF} streams, host copies of neighbouring steps overlap each step's kernels"},
+                       "pipeline": "dependent trajectory: per step H2D state (pinned) -> sdrt_rk_step -> D2H "
+                                   "state, the next step reads the host copy; serialized on one stream"},
                "gpu_launches": launches, "clocks": clk, "kernel_ms": {k: v[0] for k, v in ktimes.items()},
                "ms_per_step_instrumented": ms_inst_max / args.steps, "state_finite": finite,
                "finite_trace": dbg}

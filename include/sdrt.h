@@ -216,6 +216,24 @@ sdrt_status sdrt_stage_flux_part(sdrt_ctx* c, double* d_U, int stage, double dt,
 sdrt_status sdrt_halo_info(const sdrt_ctx* c, int* nslab, int* peer, int* d, int* side, int64_t* offset);
 sdrt_status sdrt_halo_pack(sdrt_ctx* c, int which, double* d_send, void* stream);
 sdrt_status sdrt_halo_unpack(sdrt_ctx* c, int which, const double* d_recv, void* stream);
+/* NCCL inside the library.  Rank 0 calls sdrt_comm_unique_id and
+ * broadcasts the 128 bytes to the other ranks (e.g. with torch.distributed); every rank
+ * then calls sdrt_ctx_attach_comm on its context (collective: all ranks of the
+ * partition, one GPU each, current device selected).  From then on sdrt_residual,
+ * sdrt_rk_step and sdrt_rk54_step run the whole multi-rank stage inside the library:
+ * the face traces of each partition face are packed, exchanged by grouped
+ * ncclSend/ncclRecv on the library's comm stream (ordered against the caller's stream
+ * by events) and unpacked into ghost columns, overlapped with the interior tiles; a
+ * check_every > 0 divergence check is all-reduced so every rank returns
+ * SDRT_E_DIVERGED together.  The partitioned result equals the single-rank one element
+ * by element.  rank / nranks must be those the mesh was created with.  A single-rank
+ * mesh with sdrt_mesh_set_halo(m, 1) exchanges its periodic faces through NCCL with
+ * itself (nranks = 1).  NCCL is loaded at run time (libnccl.so.2; the process's copy
+ * if one is loaded).  Errors: SDRT_E_NCCL (NCCL missing or failing), SDRT_E_INVALID_ARG,
+ * SDRT_E_UNSUPPORTED (no halo slabs / no fused path).  The communicator is destroyed
+ * with the context. */
+sdrt_status sdrt_comm_unique_id(uint8_t id[128]);
+sdrt_status sdrt_ctx_attach_comm(sdrt_ctx* c, const uint8_t id[128], int rank, int nranks);
 /* Number of kernel launches enqueued by the last sdrt_residual / sdrt_rk_step call. */
 int64_t sdrt_ctx_last_launches(const sdrt_ctx* c);
 void sdrt_ctx_destroy(sdrt_ctx* c);

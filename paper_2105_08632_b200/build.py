@@ -20,8 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-v"] + (["-DSDRT_PHASE_PROF"] if PROF else []) + EXTRA_DEFS
 CXX_FLAGS = ["-O2", "-std=gnu++17", "-fPIC", "-Wall"]
-INCLUDES = []
-LINK_LIBS = ["-lquadmath", "-lcudart"]
+INCLUDES = ["-I" + os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "include")]
+LINK_LIBS = ["-lquadmath", "-lcudart", "-ldl"]
 
 
 def sources():

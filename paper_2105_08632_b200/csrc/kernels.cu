@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "capi_internal.h"
+#include "comm.h"
 #include "ctx.h"
 #include "tensor.cuh"
 #include "simplex.cuh"
@@ -435,6 +436,10 @@ struct sdrt_ctx {
   int64_t slab_off[7];        // entry offsets of each slab in the send/recv lists
   int32_t *h_srow = nullptr, *h_scol = nullptr, *h_rrow = nullptr, *h_rcol = nullptr;
   double* h_stage = nullptr;  // loopback staging buffer
+  double* h_send = nullptr;   // NCCL exchange buffers (workspace)
+  double* h_recv = nullptr;
+  NcclComm* comm = nullptr;   // sdrt_ctx_attach_comm: the library exchanges through NCCL
+  int rank = 0, nranks = 1;
   bool auto_halo = false;     // library performs the (loopback) exchange itself
   double* Fexp = nullptr;     // sdrt_face_flux: per-ext-point common flux export (residual only)
 };
@@ -579,12 +584,13 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
     for (auto& h : s4) o += align256(h.frag.size() * sizeof(double)) + align256(h.kmask.size() * sizeof(unsigned) + 4);
   }
   // halo lists: send (row, col) and recv (row, col) int32 for all slabs, + a loopback
-  // staging buffer of the same number of values
+  // staging buffer of the same number of values, + the send / recv buffers of the
+  // library's own NCCL exchange (sdrt_ctx_attach_comm)
   size_t ent = 0;
   for (const HaloSlab& S : m.slabs) ent += S.send_row.size();
   p.halo_entries = ent;
   p.off_halo = o;
-  o += align256(ent * 4 * sizeof(int32_t)) + align256(ent * NV * sizeof(double));
+  o += align256(ent * 4 * sizeof(int32_t)) + 3 * align256(ent * NV * sizeof(double));
   // interior / boundary tile lists of the fused paths (tiles of >= 8 elements)
   p.off_tiles = o;
   o += align256(((size_t)m.K / 8 + 2) * sizeof(int32_t));
@@ -731,6 +737,8 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     c->needs_halo = c->nslab > 0;
     c->loopback = c->needs_halo;
     c->auto_halo = false;
+    c->rank = m.rank;
+    c->nranks = m.nranks;
     {
       int64_t ofs = 0;
       std::vector<int32_t> lists;
@@ -762,6 +770,8 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         CUDA_OK(cudaMemcpyAsync(c->h_rrow, rr.data(), ofs * 4, cudaMemcpyHostToDevice, st));
         CUDA_OK(cudaMemcpyAsync(c->h_rcol, rcol.data(), ofs * 4, cudaMemcpyHostToDevice, st));
         c->h_stage = (double*)(base + p.off_halo + align256(ofs * 4 * sizeof(int32_t)));
+        c->h_send = (double*)((char*)c->h_stage + align256(ofs * c->nv * sizeof(double)));
+        c->h_recv = (double*)((char*)c->h_send + align256(ofs * c->nv * sizeof(double)));
         CUDA_OK(cudaStreamSynchronize(st));
       }
     }
@@ -927,6 +937,7 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
 void sdrt_ctx_destroy(sdrt_ctx* c) {
   if (!c) return;
   for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->comm) nccl_comm_destroy(c->comm);
   delete c;
 }
 
@@ -1180,6 +1191,11 @@ static void sfused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, d
   }
 }
 
+// library-internal multi-rank stepping over NCCL (defined at the end of this file)
+static void comm_steps(sdrt_ctx* c, double* U, double dt, int nsteps, const int* stages, int nstages, cudaStream_t st);
+static void comm_residual(sdrt_ctx* c, const double* U, double* out, cudaStream_t st);
+static bool comm_check(sdrt_ctx* c, const double* U, cudaStream_t st, int64_t* bad_elem);
+
 typedef void (*ResFn)(sdrt_ctx*, const double*, int, double, double*, double*, cudaStream_t);
 typedef bool (*ChkFn)(sdrt_ctx*, const double*, cudaStream_t, int64_t*);
 
@@ -1210,8 +1226,14 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->comm) {
+      comm_residual(c, d_U, d_dUdt, st);
+      CUDA_OK(cudaGetLastError());
+      return SDRT_OK;
+    }
     if (c->needs_halo && !c->auto_halo) {
-      set_error("unsupported: multi-rank context; use the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
+      set_error("unsupported: multi-rank context without a communicator; call sdrt_ctx_attach_comm, or use "
+                "the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
       return SDRT_E_UNSUPPORTED;
     }
     if (c->fused) {
@@ -1247,8 +1269,28 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->comm) {
+      static const int rk4[4] = {0, 1, 2, 3};
+      for (int done = 0; done < nsteps;) {
+        const int n = check_every > 0 ? std::min(check_every, nsteps - done) : nsteps - done;
+        comm_steps(c, d_U, dt, n, rk4, 4, st);
+        done += n;
+        int64_t bad;
+        if (check_every > 0 && !comm_check(c, d_U, st, &bad)) {
+          char buf[200];
+          snprintf(buf, sizeof buf, "diverged after step %d: %s", done,
+                   bad >= 0 ? ("element " + std::to_string(bad) + " of this rank non-finite or non-physical").c_str()
+                            : "non-finite or non-physical state on another rank");
+          set_error(buf);
+          return SDRT_E_DIVERGED;
+        }
+      }
+      CUDA_OK(cudaGetLastError());
+      return SDRT_OK;
+    }
     if (c->needs_halo && !c->auto_halo) {
-      set_error("unsupported: multi-rank context; use the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
+      set_error("unsupported: multi-rank context without a communicator; call sdrt_ctx_attach_comm, or use "
+                "the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
       return SDRT_E_UNSUPPORTED;
     }
     ResFn res = pick_res(c->eq, c->nd);
@@ -1288,8 +1330,24 @@ sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int 
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->comm) {
+      static const int rk54[5] = {RK54_STAGE0, RK54_STAGE0 + 1, RK54_STAGE0 + 2, RK54_STAGE0 + 3, RK54_STAGE0 + 4};
+      for (int done = 0; done < nsteps;) {
+        const int n = check_every > 0 ? std::min(check_every, nsteps - done) : nsteps - done;
+        comm_steps(c, d_U, dt, n, rk54, 5, st);
+        done += n;
+        int64_t bad;
+        if (check_every > 0 && !comm_check(c, d_U, st, &bad)) {
+          set_error("diverged after step " + std::to_string(done) + " (RK54, multi-rank)");
+          return SDRT_E_DIVERGED;
+        }
+      }
+      CUDA_OK(cudaGetLastError());
+      return SDRT_OK;
+    }
     if (c->needs_halo && !c->auto_halo) {
-      set_error("unsupported: multi-rank context; use the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
+      set_error("unsupported: multi-rank context without a communicator; call sdrt_ctx_attach_comm, or use "
+                "the staged API (sdrt_stage_*) with sdrt_halo_pack/unpack");
       return SDRT_E_UNSUPPORTED;
     }
     if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
@@ -1541,6 +1599,163 @@ sdrt_status sdrt_stage_flux_part(sdrt_ctx* c, double* d_U, int stage, double dt,
     CUDA_OK(cudaGetLastError());
     return SDRT_OK;
   })
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------
+// Multi-rank stepping inside the library: the U traces after the
+// trace-producing kernel and, for viscous equations, the published viscous traces after
+// kernel A are packed on the compute stream, exchanged by grouped ncclSend / ncclRecv
+// on the library's comm stream (ordered by events), and unpacked into the ghost trace
+// columns.  While an exchange is in flight the interior tiles (no ghost reads) run;
+// the boundary tiles run after the unpack.  Per-element arithmetic is that of the
+// single-rank kernels, so the partitioned result equals the single-rank one.
+namespace sdrt {
+
+static void check_status(sdrt_status s) {
+  if (s != SDRT_OK) throw std::runtime_error(sdrt_last_error());
+}
+
+// pack `which` (0: U traces, 1: viscous traces) and post the exchange on the comm stream
+static void comm_start(sdrt_ctx* c, int which, cudaStream_t st) {
+  if (c->nslab == 0) return;
+  halo_pack(c, which, c->h_send, st);
+  NcclComm* cm = c->comm;
+  CUDA_OK(cudaEventRecord(nccl_comm_event(cm, 0), st));
+  CUDA_OK(cudaStreamWaitEvent(nccl_comm_stream(cm), nccl_comm_event(cm, 0), 0));
+  const double* sb[6];
+  double* rb[6];
+  int64_t ns[6], nr[6];
+  int ps[6], pr[6];
+  for (int i = 0; i < c->nslab; ++i) {
+    int j = -1;  // the slab that receives what the peer of slab i's opposite side sends
+    for (int k = 0; k < c->nslab; ++k)
+      if (c->slab_d[k] == c->slab_d[i] && c->slab_side[k] == 1 - c->slab_side[i]) j = k;
+    if (j < 0) throw std::runtime_error("internal: halo slab without its opposite");
+    // what I send from slab (d, side) lands in the peer's slab (d, 1-side); what I
+    // receive in slab (d, 1-side) the peer there sent from its slab (d, side).  Every
+    // rank posts in slab order, so NCCL's in-order matching per peer pair pairs them.
+    sb[i] = c->h_send + c->slab_off[i] * c->nv;
+    ns[i] = (c->slab_off[i + 1] - c->slab_off[i]) * c->nv;
+    ps[i] = c->slab_peer[i];
+    rb[i] = c->h_recv + c->slab_off[j] * c->nv;
+    nr[i] = (c->slab_off[j + 1] - c->slab_off[j]) * c->nv;
+    pr[i] = c->slab_peer[j];
+  }
+  nccl_exchange(cm, c->nslab, sb, ns, ps, rb, nr, pr);
+  CUDA_OK(cudaEventRecord(nccl_comm_event(cm, 1), nccl_comm_stream(cm)));
+}
+
+// make the compute stream wait for the exchange and unpack into the ghost columns
+static void comm_finish(sdrt_ctx* c, int which, cudaStream_t st) {
+  if (c->nslab == 0) return;
+  CUDA_OK(cudaStreamWaitEvent(st, nccl_comm_event(c->comm, 1), 0));
+  halo_unpack(c, which, c->h_recv, st);
+}
+
+static void comm_steps(sdrt_ctx* c, double* U, double dt, int nsteps, const int* stages, int nstages,
+                       cudaStream_t st) {
+  if (nsteps <= 0) return;
+  const bool ah = c->auto_halo;
+  c->auto_halo = false;  // the staged calls must not run the loopback kernels
+  const int64_t l0 = c->launches;
+  check_status(sdrt_stage_traces(c, U, st));
+  c->launches += l0;
+  comm_start(c, 0, st);
+  for (int step = 0; step < nsteps; ++step)
+    for (int k = 0; k < nstages; ++k) {
+      const int s = stages[k];
+      if (c->visc) {
+        check_status(sdrt_stage_grad_part(c, U, s, 1, st));  // interior || U-trace exchange
+        comm_finish(c, 0, st);
+        check_status(sdrt_stage_grad_part(c, U, s, 2, st));
+        comm_start(c, 1, st);
+        check_status(sdrt_stage_flux_part(c, U, s, dt, nullptr, 1, st));  // interior || g exchange
+        comm_finish(c, 1, st);
+      } else {
+        check_status(sdrt_stage_flux_part(c, U, s, dt, nullptr, 1, st));
+        comm_finish(c, 0, st);
+      }
+      check_status(sdrt_stage_flux_part(c, U, s, dt, nullptr, 2, st));
+      comm_start(c, 0, st);  // traces of the new stage input
+    }
+  comm_finish(c, 0, st);
+  c->auto_halo = ah;
+}
+
+static void comm_residual(sdrt_ctx* c, const double* U, double* out, cudaStream_t st) {
+  const bool ah = c->auto_halo;
+  c->auto_halo = false;
+  double* Um = const_cast<double*>(U);  // stage -1 reads U only
+  check_status(sdrt_stage_traces(c, U, st));
+  comm_start(c, 0, st);
+  comm_finish(c, 0, st);
+  if (c->visc) {
+    check_status(sdrt_stage_grad(c, Um, -1, st));
+    comm_start(c, 1, st);
+    comm_finish(c, 1, st);
+  }
+  check_status(sdrt_stage_flux(c, Um, -1, 0.0, out, st));
+  c->auto_halo = ah;
+}
+
+// divergence check over all ranks: every rank learns whether any rank went bad
+static bool comm_check(sdrt_ctx* c, const double* U, cudaStream_t st, int64_t* bad_elem) {
+  int64_t local = -1;
+  const bool ok = pick_chk(c->eq, c->nd)(c, U, st, &local);
+  unsigned long long flag = ok ? ~0ull : 0ull, host = 0;
+  CUDA_OK(cudaMemcpyAsync(c->bad + 1, &flag, sizeof(flag), cudaMemcpyHostToDevice, st));
+  nccl_allreduce_min_u64(c->comm, c->bad + 1, st);
+  CUDA_OK(cudaMemcpyAsync(&host, c->bad + 1, sizeof(host), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cudaStreamSynchronize(st));
+  *bad_elem = ok ? -1 : local;
+  return host == ~0ull;
+}
+
+}  // namespace sdrt
+
+extern "C" {
+
+sdrt_status sdrt_comm_unique_id(uint8_t id[128]) {
+  if (!id) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  try {
+    nccl_unique_id(id);
+    return SDRT_OK;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return SDRT_E_NCCL;
+  }
+}
+
+sdrt_status sdrt_ctx_attach_comm(sdrt_ctx* c, const uint8_t id[128], int rank, int nranks) {
+  if (!c || !id || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_error("invalid argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (rank != c->rank || nranks != c->nranks) {
+    set_error("communicator rank / size differ from the mesh partition's (sdrt_mesh_create rank, nranks)");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (!c->needs_halo || (!c->fused && !c->sfused)) {
+    set_error("unsupported: the context has no halo slabs (single-rank mesh without sdrt_mesh_set_halo) or "
+              "no fused path");
+    return SDRT_E_UNSUPPORTED;
+  }
+  if (c->comm) {
+    nccl_comm_destroy(c->comm);
+    c->comm = nullptr;
+  }
+  try {
+    c->comm = nccl_comm_create(id, rank, nranks);
+    return SDRT_OK;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return SDRT_E_NCCL;
+  }
 }
 
 }  // extern "C"

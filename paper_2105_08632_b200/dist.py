@@ -18,24 +18,37 @@ from .solver import Solver
 
 
 def default_pgrid(nranks, nd):
-    """1 -> 1x1x1, 2 -> 2x1x1, 4 -> 2x2x1, 8 -> 2x2x2 (x first)."""
+    """Pattern-block partition over the SLOW axes (3-D: z, y, z, ...; 2-D: y):
+    3-D 1 -> 1x1x1, 2 -> 1x1x2, 4 -> 1x2x2, 8 -> 1x2x4.  The fused kernels' tiles are runs
+    of consecutive elements along x, so a partition face normal to x would make the first
+    and last tile of every x-row a boundary tile (SURVEY §8(e)'s 2x2x2 leaves 44 % of the
+    c4 tiles interior); with x never cut, a tile is boundary only in the y/z pattern layers
+    next to a partition face: 88 % of c4's tiles run while the halo exchange is in flight
+    (the interior-first effect of §8(e) without reordering the ABI element order)."""
     g = [1, 1, 1]
-    k, d = nranks, 0
+    axes = [2, 1] if nd == 3 else [1]
+    k, i = nranks, 0
     while k > 1:
         if k % 2:
             raise ValueError("nranks must be a power of two")
-        g[d % nd] *= 2
+        g[axes[i % len(axes)]] *= 2
         k //= 2
-        d += 1
+        i += 1
     return g[:nd]
 
 
 class DistSolver(Solver):
-    """Solver over this rank's block; rk_step / residual run the staged API with a halo
-    exchange after every trace-producing kernel."""
+    """Solver over this rank's block.
+
+    transport = "library" (default for CUDA devices without host staging): the halo
+    exchange runs inside libsdrt over NCCL (sdrt_comm_unique_id on rank 0, broadcast with
+    torch.distributed, sdrt_ctx_attach_comm on every rank); rk_step / residual are then the
+    plain library calls.  transport = "torch": the staged API with the exchange through
+    torch.distributed point-to-point (gloo with host staging: CPU-side and single-device
+    multi-process tests)."""
 
     def __init__(self, etype, p, N, lo, hi, eq, device="cuda", group=None, pgrid=None, staging=False,
-                 force_self_halo=False, **phys):
+                 force_self_halo=False, transport=None, **phys):
         self.group = group
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         nranks = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -45,12 +58,21 @@ class DistSolver(Solver):
         super().__init__(etype, p, N, lo, hi, eq, device=device, rank=rank, nranks=nranks, pgrid=pgrid,
                          _pre_ctx=self._set_halo, **phys)
         self.rank = rank
+        self.nranks = nranks
         self.staging = staging
         self.peers, self.sd, self.sside, self.off = sdrt.halo_info(self.ctx)
         n = self.off[-1] if self.off else 0
         self.send = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
         self.recv = torch.zeros(max(n, 1), dtype=torch.float64, device=self.device)
         self.exchanges = 0
+        if transport is None:
+            transport = "library" if (self.device.type == "cuda" and not staging and len(self.peers) > 0) else "torch"
+        self.transport = transport
+        if transport == "library":
+            uid = [sdrt.comm_unique_id() if rank == 0 else None]
+            if nranks > 1:
+                dist.broadcast_object_list(uid, src=0, group=group)
+            sdrt.ctx_attach_comm(self.ctx, uid[0], rank, nranks)
 
     def _set_halo(self, mesh):
         sdrt.mesh_set_halo(mesh, self._force)
@@ -102,6 +124,8 @@ class DistSolver(Solver):
         self.exchanges += 1
 
     def residual(self, U, out=None):
+        if self.transport == "library":
+            return Solver.residual(self, U, out)
         out = torch.empty_like(U) if out is None else out
         st = self._stream()
         sdrt.stage_traces(self.ctx, U.data_ptr(), st)
@@ -114,10 +138,38 @@ class DistSolver(Solver):
 
     def rk54_step(self, U, dt, nsteps=1, check_every=0):
         """RK54 over the same overlapped staged sequence (stage codes 10..14)."""
-        return self._steps(U, dt, nsteps, [sdrt.RK54_STAGE0 + s for s in range(5)])
+        if self.transport == "library":
+            return Solver.rk54_step(self, U, dt, nsteps, check_every)
+        return self._checked(U, dt, nsteps, check_every, [sdrt.RK54_STAGE0 + s for s in range(5)])
 
     def rk_step(self, U, dt, nsteps=1, check_every=0):
-        return self._steps(U, dt, nsteps, [0, 1, 2, 3])
+        if self.transport == "library":
+            return Solver.rk_step(self, U, dt, nsteps, check_every)
+        return self._checked(U, dt, nsteps, check_every, [0, 1, 2, 3])
+
+    def _checked(self, U, dt, nsteps, check_every, stages):
+        """torch transport: the steps in chunks of check_every with an all-reduced
+        finite / positive-density / positive-energy check after each (the library does
+        the same on its own transport, SDRT_E_DIVERGED on every rank together)."""
+        done = 0
+        while done < nsteps:
+            n = min(check_every, nsteps - done) if check_every > 0 else nsteps - done
+            self._steps(U, dt, n, stages)
+            done += n
+            if check_every > 0:
+                u = U[:, :, :self.K]
+                ok = bool(torch.isfinite(u).all())
+                if ok and self.nv > 1:
+                    ok = bool((u[:, 0] > 0).all()) and bool((u[:, -1] > 0).all())
+                flag = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64,
+                                    device=self.device if dist.is_initialized() and
+                                    dist.get_backend(self.group) == "nccl" else "cpu")
+                if dist.is_initialized():
+                    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+                if flag.item() < 1.0:
+                    raise sdrt.SdrtError(-7, f"diverged after step {done} (rank {self.rank}: "
+                                             f"{'bad' if not ok else 'ok'} locally)")
+        return U
 
     def _steps(self, U, dt, nsteps, stages):
         """Time steps with the halo exchange overlapped with interior work: each

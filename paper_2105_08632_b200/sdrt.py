@@ -88,6 +88,8 @@ lib.sdrt_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_ctx_kernel_times.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_int)]
 lib.sdrt_ctx_last_launches.argtypes = [_vp]
 lib.sdrt_ctx_last_launches.restype = ctypes.c_int64
+lib.sdrt_comm_unique_id.argtypes = [_vp]
+lib.sdrt_ctx_attach_comm.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int]
 lib.sdrt_ctx_destroy.argtypes = [_vp]
 lib.sdrt_ctx_destroy.restype = None
 
@@ -97,7 +99,8 @@ EXPORTED = ["sdrt_abi_version", "sdrt_last_error", "sdrt_mesh_create", "sdrt_mes
             "sdrt_ctx_workspace_bytes", "sdrt_ctx_create", "sdrt_residual", "sdrt_face_flux", "sdrt_rk_step",
             "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_kernel_times",
             "sdrt_mesh_set_halo", "sdrt_mesh_halo_lists", "sdrt_mesh_neighbor", "sdrt_halo_info",
-            "sdrt_halo_pack", "sdrt_halo_unpack", "sdrt_stage_traces", "sdrt_stage_grad", "sdrt_stage_flux"]
+            "sdrt_halo_pack", "sdrt_halo_unpack", "sdrt_stage_traces", "sdrt_stage_grad", "sdrt_stage_flux",
+            "sdrt_comm_unique_id", "sdrt_ctx_attach_comm"]
 
 
 def _check(code):
@@ -234,6 +237,18 @@ def ctx_create(m, o, ph, ws_ptr, ws_bytes, stream):
 
 def residual(ctx, U_ptr, dUdt_ptr, stream):
     _check(lib.sdrt_residual(ctx, _vp(U_ptr), _vp(dUdt_ptr), _vp(stream)))
+
+
+def comm_unique_id():
+    """128-byte NCCL unique id (rank 0; broadcast it to the other ranks)."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib.sdrt_comm_unique_id(buf))
+    return bytes(buf)
+
+
+def ctx_attach_comm(ctx, uid, rank, nranks):
+    buf = (ctypes.c_uint8 * 128)(*uid)
+    _check(lib.sdrt_ctx_attach_comm(ctx, buf, int(rank), int(nranks)))
 
 
 def face_flux(ctx, U_ptr, dUdt_ptr, F_ptr, stream):
