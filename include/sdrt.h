@@ -87,8 +87,12 @@ int sdrt_abi_version(void);
 const char* sdrt_last_error(void);
 
 /* Uniform mesh of N[0] x N[1] (x N[2]) patterns on the box [lo, hi], each pattern
- * split into N_p sub-cells. periodic[d] must be 1 (only
- * periodic meshes are supported by this hot path). N[d] >= 3.
+ * split into N_p sub-cells. periodic[d] = 1: periodic axis;
+ * 0: far-field boundaries at x_d = lo[d] and hi[d] (the paper's vortex, PAPER.md l.1952:
+ * "the limiting values of the initial conditions ... at boundaries with constant x"):
+ * the boundary faces' exterior state is a constant far-field state set with
+ * sdrt_ctx_set_farfield (fused element paths only).  periodic = NULL: all periodic.
+ * N[d] >= 3.
  * Multi-rank: the pattern grid is block-partitioned by pgrid (pgrid[d] divides
  * N[d]); rank r owns block (r % pg0, (r / pg0) % pg1, r / (pg0 pg1)).
  * Single rank: rank = 0, nranks = 1, pgrid = NULL.
@@ -216,6 +220,14 @@ sdrt_status sdrt_stage_flux_part(sdrt_ctx* c, double* d_U, int stage, double dt,
 sdrt_status sdrt_halo_info(const sdrt_ctx* c, int* nslab, int* peer, int* d, int* side, int64_t* offset);
 sdrt_status sdrt_halo_pack(sdrt_ctx* c, int which, double* d_send, void* stream);
 sdrt_status sdrt_halo_unpack(sdrt_ctx* c, int which, const double* d_recv, void* stream);
+/* Far-field boundaries (NEXT row N4): state[N_V] (host, conserved
+ * variables) is the exterior state of every far-field boundary face.  The common
+ * flux there is the interior one of l.312-340 with u_ext = state and, for viscous
+ * equations, a zero exterior gradient (the viscous flux of a constant state), the
+ * left/right roles by reading O14.  Must be called once before sdrt_residual /
+ * sdrt_rk_step on a context whose mesh has a non-periodic axis (SDRT_E_INVALID_ARG
+ * from those otherwise); synchronous.  SDRT_E_INVALID_ARG if the mesh is periodic. */
+sdrt_status sdrt_ctx_set_farfield(sdrt_ctx* c, const double* state, void* stream);
 /* NCCL inside the library.  Rank 0 calls sdrt_comm_unique_id and
  * broadcasts the 128 bytes to the other ranks (e.g. with torch.distributed); every rank
  * then calls sdrt_ctx_attach_comm on its context (collective: all ranks of the

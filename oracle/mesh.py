@@ -72,6 +72,7 @@ class Mesh:
     is_left: np.ndarray     # K x nfaces bool
     nbr_elem: np.ndarray    # N_ext x K  neighbour element of each external point
     nbr_pt: np.ndarray      # N_ext x K  matching external point index in the neighbour
+    periodic: tuple = ()    # per axis; False: far-field boundaries (faces with a -1 side)
 
     def sol_coords(self):
         """Physical coordinates of solution points, shape (N_sol, D, K) (reading O21)."""
@@ -85,7 +86,9 @@ class Mesh:
         return np.einsum("kij,sj->sik", self.J, xr) + self.x0.T[None, :, :]
 
 
-def build_mesh(etype, p, N, lo, hi):
+def build_mesh(etype, p, N, lo, hi, periodic=None):
+    """periodic[d] = 0: far-field boundaries at x_d = lo, hi: faces there
+    have no partner; they are listed with -1 for the missing (exterior) side."""
     ops = build_operators(etype, p)
     D = ops.nd
     N = tuple(int(n) for n in (N if np.ndim(N) else [N] * D))
@@ -120,26 +123,39 @@ def build_mesh(etype, p, N, lo, hi):
         raise ValueError("non-positive det J")
     Jinv = np.linalg.inv(J)
     # ---------------------------------------------------------------- face pairing
+    per = np.ones(D, dtype=bool) if periodic is None else np.asarray(periodic[:D], dtype=bool)
     L = hi - lo
     xr = ops.xext + 1.0
     xe = np.einsum("kij,sj->ksi", J, xr) + x0[:, None, :]     # K x N_ext x D
     nf, nfp = ops.nfaces, ops.nfp
     xe = xe.reshape(K, nf, nfp, D)
     tol = 1e-9 * float(np.min(h))
-    # face key: centroid wrapped into the periodic box, rounded
+    # face key: centroid wrapped into the periodic box (periodic axes only), rounded
     cen = xe.mean(axis=2)
-    cen = np.mod(cen - lo + 0.5 * tol, L) - 0.5 * tol
+    cen = np.where(per, np.mod(cen - lo + 0.5 * tol, L) - 0.5 * tol, cen - lo)
     key = np.round(cen / (1e-6 * float(np.min(h)))).astype(np.int64).reshape(K * nf, D)
     order = np.lexsort(key.T[::-1])
     ks = key[order]
-    same_next = np.all(ks[1:] == ks[:-1], axis=1)
-    # every key must occur exactly twice: pairs are (order[2i], order[2i+1])
-    if len(order) % 2 or not np.all(same_next[0::2]) or np.any(same_next[1::2]):
-        raise ValueError("face pairing failed: a face centroid is not shared by exactly 2 faces")
-    A, B = order[0::2], order[1::2]
-    partner = np.empty(K * nf, dtype=np.int64)
-    partner[A] = B
-    partner[B] = A
+    # group equal keys: interior faces come in pairs, far-field boundary faces alone
+    partner = np.full(K * nf, -1, dtype=np.int64)
+    i = 0
+    while i < len(order):
+        j = i + 1
+        while j < len(order) and np.all(ks[j] == ks[i]):
+            j += 1
+        if j - i == 2:
+            partner[order[i]], partner[order[i + 1]] = order[i + 1], order[i]
+        elif j - i != 1:
+            raise ValueError("face pairing failed: a face centroid is shared by more than 2 faces")
+        i = j
+    cflat = cen.reshape(K * nf, D)
+    lone = np.nonzero(partner < 0)[0]
+    on_ff = np.zeros(len(lone), dtype=bool)
+    for d in range(D):
+        if not per[d]:
+            on_ff |= (np.abs(cflat[lone, d]) < tol) | (np.abs(cflat[lone, d] - L[d]) < tol)
+    if not np.all(on_ff):
+        raise ValueError("face pairing failed: an unpaired face is not on a far-field boundary")
     # outward physical unit normals: n = J^-T n~ / |J^-T n~|
     fn = ops.face_normals
     nphys = np.einsum("kji,fj->kfi", Jinv, fn)
@@ -149,23 +165,31 @@ def build_mesh(etype, p, N, lo, hi):
     first = np.argmax(nz, axis=2)
     is_left = np.take_along_axis(nphys, first[..., None], axis=2)[..., 0] > 0
     flat_left = is_left.reshape(K * nf)
-    if np.any(flat_left == flat_left[partner]):
+    paired = partner >= 0
+    if np.any(flat_left[paired] == flat_left[partner[paired]]):
         raise ValueError("left/right rule is not antisymmetric")
     # face point permutation by coordinate matching (mod periodic box)
     xf = xe.reshape(K * nf, nfp, D)
-    d = xf[partner][:, None, :, :] - xf[:, :, None, :]        # [face, q, q', D]
-    d = d - L * np.round(d / L)
+    pt = np.where(paired, partner, np.arange(K * nf))
+    d = xf[pt][:, None, :, :] - xf[:, :, None, :]              # [face, q, q', D]
+    d = d - np.where(per, L * np.round(d / L), 0.0)
     dist = np.max(np.abs(d), axis=3)
     perm_all = np.argmin(dist, axis=2)                         # [face, q] -> q'
-    if np.any(np.take_along_axis(dist, perm_all[..., None], axis=2) > tol):
+    if np.any(np.take_along_axis(dist, perm_all[..., None], axis=2)[paired] > tol):
         raise ValueError("face point matching failed")
-    pe, pf = partner // nf, partner % nf
-    nbr_elem = np.repeat(pe.reshape(K, nf), nfp, axis=1).T.copy()          # N_ext x K
-    nbr_pt = (pf.reshape(K, nf, 1) * nfp + perm_all.reshape(K, nf, nfp)).reshape(K, nf * nfp).T.copy()
-    lidx = np.nonzero(flat_left)[0]                                        # sorted (e, f)
+    perm_all[~paired] = -1
+    pe = np.where(paired, partner // nf, -1)
+    pf = np.where(paired, partner % nf, -1)
+    nbr_elem = np.repeat(pe.reshape(K, nf), nfp, axis=1).T.copy()          # N_ext x K (-1: far field)
+    nbr_pt = np.where(perm_all < 0, -1, pf[:, None] * nfp + perm_all).reshape(K, nf * nfp).T.copy()
+    # faces in (element, local face) scan order: those whose left element this is, and
+    # far-field faces (exterior side -1, listed from the interior element)
+    lidx = np.nonzero(flat_left | ~paired)[0]
     F = len(lidx)
-    face_elem = np.stack([lidx // nf, pe[lidx]], axis=1).astype(np.int32)
-    face_lface = np.stack([lidx % nf, pf[lidx]], axis=1).astype(np.int8)
+    me, mf = lidx // nf, lidx % nf
+    lft = flat_left[lidx]
+    face_elem = np.stack([np.where(lft, me, -1), np.where(lft, pe[lidx], me)], axis=1).astype(np.int32)
+    face_lface = np.stack([np.where(lft, mf, -1), np.where(lft, pf[lidx], mf)], axis=1).astype(np.int8)
     face_perm = perm_all[lidx].astype(np.int16).reshape(F, nfp)
     return Mesh(etype, p, D, N, lo, hi, h, K, nsub, J, detJ, Jinv, x0,
-                face_elem, face_lface, face_perm, is_left, nbr_elem, nbr_pt)
+                face_elem, face_lface, face_perm, is_left, nbr_elem, nbr_pt, tuple(bool(x) for x in per))

@@ -24,34 +24,62 @@ from .operators import build_operators
 
 
 class Residual:
-    def __init__(self, mesh, ph):
+    """farfield: exterior state (N_V,) of the far-field boundary faces of a mesh with a
+    non-periodic axis (boundaries take the limiting values of the
+    initial field).  Such a face is evaluated like any other with the exterior side a
+    GHOST element (column K of the trace arrays) whose traces are the far-field state
+    and whose gradient is zero (the viscous flux of a constant state); left/right by the
+    same rule O14."""
+
+    def __init__(self, mesh, ph, farfield=None):
         self.mesh = mesh
         self.ph = ph
         self.ops = build_operators(mesh.etype, mesh.p)
         o, m = self.ops, mesh
         D = o.nd
-        # per external point reference normal and metric scale
+        K = m.K
+        # per external point reference normal and metric scale (+ a ghost column K)
         fn = o.ext_normal                                         # N_ext x D
         jn = np.einsum("kji,sj->ski", m.Jinv, fn)                 # J^-T n~  [s, k, i]
         nrm = np.linalg.norm(jn, axis=2)                          # N_ext x K
-        self.s = m.detJ[None, :] * nrm                            # N_ext x K
+        self.s = np.concatenate([m.detJ[None, :] * nrm, np.zeros((o.next, 1))], axis=1)
         self.nphys = jn / nrm[..., None]                          # N_ext x K x D
-        # face-point lists (flattened over faces x face points)
+        # face-point lists (flattened over faces x face points); -1 (far field) -> ghost K
         nfp = o.nfp
         F = m.face_elem.shape[0]
-        self.fL = np.repeat(m.face_elem[:, 0].astype(np.int64), nfp)
-        self.fR = np.repeat(m.face_elem[:, 1].astype(np.int64), nfp)
+        fe = m.face_elem.astype(np.int64)
+        fl = m.face_lface.astype(np.int64)
+        gL, gR = fe[:, 0] < 0, fe[:, 1] < 0
+        self.ghost_faces = int(gL.sum() + gR.sum())
+        if self.ghost_faces and farfield is None:
+            raise ValueError("the mesh has far-field faces: pass the far-field state")
+        self.farfield = None if farfield is None else np.asarray(farfield, dtype=np.float64)
         q = np.tile(np.arange(nfp), F)
-        self.pL = m.face_lface[:, 0].astype(np.int64).repeat(nfp) * nfp + q
-        self.pR = m.face_lface[:, 1].astype(np.int64).repeat(nfp) * nfp + m.face_perm.astype(np.int64).reshape(-1)
-        self.nL = self.nphys[self.pL, self.fL].T                  # D x (F.nfp)
+        perm = m.face_perm.astype(np.int64).reshape(-1)
+        self.fL = np.repeat(np.where(gL, K, fe[:, 0]), nfp)
+        self.fR = np.repeat(np.where(gR, K, fe[:, 1]), nfp)
+        # a ghost side takes the interior side's point index (ghost traces are constant)
+        self.pL = np.where(np.repeat(gL, nfp), fl[:, 1].repeat(nfp) * nfp + q, fl[:, 0].repeat(nfp) * nfp + q)
+        self.pR = np.where(np.repeat(gL, nfp), self.pL,
+                           np.where(np.repeat(gR, nfp), self.pL, fl[:, 1].repeat(nfp) * nfp + perm))
+        # the left element's outward unit normal (ghost left: minus the interior's)
+        gl = np.repeat(gL, nfp)
+        nin = self.nphys[np.where(gl, self.pR, self.pL), np.where(gl, self.fR, self.fL)]
+        self.nL = np.where(gl[:, None], -nin, nin).T              # D x (F.nfp)
 
     # ---------------------------------------------------------------- helpers
+    def _ghost(self, A, zero=False):
+        """Append the ghost column: far-field traces (or zero gradients)."""
+        g = np.zeros(A.shape[:-1] + (1,))
+        if not zero and self.farfield is not None:
+            g[..., :, 0] = self.farfield[None, :] if A.ndim == 3 else self.farfield[None, None, :]
+        return np.concatenate([A, g], axis=-1)
+
     def _face_scatter(self, valL, valR, shape):
-        out = np.zeros(shape)
+        out = np.zeros(shape[:-1] + (shape[-1] + 1,))
         out[self.pL, :, self.fL] = valL
         out[self.pR, :, self.fR] = valR
-        return out
+        return out[..., :-1]
 
     def gradient(self, U):
         """Physical gradient Q (D, N_sol, N_V, K) of the conserved variables (step 2)."""
@@ -59,7 +87,7 @@ class Residual:
         nsol, NV, K = U.shape
         D = o.nd
         Uf = U.reshape(nsol, NV * K)
-        Uext = (o.M0 @ Uf).reshape(o.next, NV, K)
+        Uext = self._ghost((o.M0 @ Uf).reshape(o.next, NV, K))
         Uu = (o.M12 @ Uf).reshape(o.nu, NV, K)
         uL = Uext[self.pL, :, self.fL]                            # (F.nfp, NV)
         uR = Uext[self.pR, :, self.fR]
@@ -77,12 +105,12 @@ class Residual:
         nsol, NV, K = U.shape
         D = o.nd
         Uf = U.reshape(nsol, NV * K)
-        Uext = (o.M0 @ Uf).reshape(o.next, NV, K)
+        Uext = self._ghost((o.M0 @ Uf).reshape(o.next, NV, K))
         Uu = (o.M12 @ Uf).reshape(o.nu, NV, K)
         Qext = Qu = None
         if ph.viscous:
             Q = self.gradient(U)
-            Qext = np.stack([(o.M0 @ Q[d].reshape(nsol, NV * K)).reshape(o.next, NV, K)
+            Qext = np.stack([self._ghost((o.M0 @ Q[d].reshape(nsol, NV * K)).reshape(o.next, NV, K), zero=True)
                              for d in range(D)])
             Qu = np.stack([(o.M12 @ Q[d].reshape(nsol, NV * K)).reshape(o.nu, NV, K)
                            for d in range(D)])

@@ -25,17 +25,10 @@ sdrt_status sdrt_mesh_create(int etype, int p, const int N[3], const double lo[3
     sdrt::set_error("unsupported element type");
     return SDRT_E_UNSUPPORTED;
   }
-  int D = sdrt::etype_dim(etype);
-  if (periodic)
-    for (int d = 0; d < D; ++d)
-      if (!periodic[d]) {
-        sdrt::set_error("unsupported: only periodic meshes are implemented");
-        return SDRT_E_UNSUPPORTED;
-      }
   SDRT_TRY({
     auto* m = new sdrt_mesh;
     try {
-      m->m = sdrt::build_mesh(etype, p, N, lo, hi, rank, nranks, pgrid);
+      m->m = sdrt::build_mesh(etype, p, N, lo, hi, rank, nranks, pgrid, periodic);
     } catch (...) {
       delete m;
       throw;
@@ -69,10 +62,22 @@ sdrt_status sdrt_mesh_info(const sdrt_mesh* mm, sdrt_mesh_info_t* out) {
   }
   out->K = m.K;
   out->K_pad = m.K_pad;
-  int64_t nl = 0;
-  for (int s = 0; s < m.nsub; ++s)
-    for (int f = 0; f < r.nfaces; ++f) nl += m.link[s * r.nfaces + f].left;
-  out->n_faces = nl * (m.K / m.nsub);
+  // faces whose left element is local, plus far-field boundary faces of local elements
+  int64_t nf = 0;
+  for (int64_t e = 0; e < m.K; ++e) {
+    int c[3];
+    m.gcoords(e, c);
+    for (int f = 0; f < r.nfaces; ++f) {
+      const sdrt::FaceLink& L = m.link[(e % m.nsub) * r.nfaces + f];
+      bool ff = false;
+      for (int d = 0; d < m.nd; ++d) {
+        const int cc = c[d] + L.off[d];
+        if (!m.periodic[d] && (cc < 0 || cc >= m.Nglob[d])) ff = true;
+      }
+      nf += (L.left || ff) ? 1 : 0;
+    }
+  }
+  out->n_faces = nf;
   out->K_trace = m.Kt;
   return SDRT_OK;
 }
@@ -93,24 +98,30 @@ sdrt_status sdrt_mesh_export_maps(const sdrt_mesh* mm, int32_t* face_elem, int8_
     for (int f = 0; f < r.nfaces; ++f) {
       const sdrt::FaceLink& L = m.link[s * r.nfaces + f];
       if (is_left) is_left[e * r.nfaces + f] = (uint8_t)L.left;
-      if (!L.left) continue;
+      bool ff = false;  // far-field boundary face: the neighbour is outside the domain
+      for (int d = 0; d < m.nd; ++d) {
+        const int cc = c[d] + L.off[d];
+        if (!m.periodic[d] && (cc < 0 || cc >= m.Nglob[d])) ff = true;
+      }
+      if (!L.left && !ff) continue;
       int64_t g = 0, mul = 1;
       for (int d = 0; d < m.nd; ++d) {
         int cc = ((c[d] + L.off[d]) % m.Nglob[d] + m.Nglob[d]) % m.Nglob[d];
         g += mul * cc;
         mul *= m.Nglob[d];
       }
-      int64_t nb = g * m.nsub + L.nshape;
+      const int64_t nb = ff ? -1 : g * m.nsub + L.nshape;
+      const int64_t me = m.global_id(e);
       if (face_elem) {
-        face_elem[2 * F] = (int32_t)m.global_id(e);
-        face_elem[2 * F + 1] = (int32_t)nb;
+        face_elem[2 * F] = (int32_t)(L.left ? me : -1);
+        face_elem[2 * F + 1] = (int32_t)(L.left ? nb : me);
       }
       if (face_lface) {
-        face_lface[2 * F] = (int8_t)f;
-        face_lface[2 * F + 1] = (int8_t)L.nface;
+        face_lface[2 * F] = (int8_t)(L.left ? f : -1);
+        face_lface[2 * F + 1] = (int8_t)(L.left ? (ff ? -1 : L.nface) : f);
       }
       if (face_perm)
-        for (int q = 0; q < r.nfp; ++q) face_perm[F * r.nfp + q] = (int16_t)L.perm[q];
+        for (int q = 0; q < r.nfp; ++q) face_perm[F * r.nfp + q] = (int16_t)(ff ? -1 : L.perm[q]);
       ++F;
     }
   }

@@ -297,6 +297,22 @@ __global__ void k_halo_unpack(double* __restrict__ T, int64_t Kt, int NV, const 
   T[trace_at(row[k], v, col[k], Kt, NV, pm)] = buf[idx];
 }
 
+// far-field ghost entries (boundaries with the limiting values of the
+// initial field): the U traces of the ghost element = the far-field state, its published
+// viscous normal flux = 0 (f^v of a constant state)
+__global__ void k_ff_fill(double* __restrict__ Tu0, double* __restrict__ Tu1, double* __restrict__ Tg, int64_t Kt,
+                          int NV, const int32_t* __restrict__ row, const int32_t* __restrict__ col, int64_t n,
+                          const double* __restrict__ state, bool pm) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * NV) return;
+  const int64_t k = idx / NV;
+  const int v = (int)(idx % NV);
+  const int64_t at = trace_at(row[k], v, col[k], Kt, NV, pm);
+  Tu0[at] = state[v];
+  Tu1[at] = state[v];
+  if (Tg) Tg[at] = 0.0;
+}
+
 // sum of the per-tile diagnostics partials in a fixed order (one block), scaled:
 // out = { <rho v.v>, 2 mu <S:S>, -<p div v> }
 __global__ void k_diag_final(const double* __restrict__ part, int64_t ntile, double inv_vol, double mu,
@@ -349,7 +365,8 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
-      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_tiles, off_diag, off_cub, total;
+      off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_ff, off_tiles, off_diag, off_cub,
+      total;
   size_t ops_bytes;
 };
 
@@ -439,6 +456,10 @@ struct sdrt_ctx {
   double* h_send = nullptr;   // NCCL exchange buffers (workspace)
   double* h_recv = nullptr;
   NcclComm* comm = nullptr;   // sdrt_ctx_attach_comm: the library exchanges through NCCL
+  int64_t ff_n = 0;           // far-field ghost entries
+  int32_t *ff_row = nullptr, *ff_col = nullptr;
+  double* ff_state = nullptr;
+  bool ff_pending = false;    // far-field entries not yet filled (sdrt_ctx_set_farfield)
   int rank = 0, nranks = 1;
   bool auto_halo = false;     // library performs the (loopback) exchange itself
   double* Fexp = nullptr;     // sdrt_face_flux: per-ext-point common flux export (residual only)
@@ -591,6 +612,9 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.halo_entries = ent;
   p.off_halo = o;
   o += align256(ent * 4 * sizeof(int32_t)) + 3 * align256(ent * NV * sizeof(double));
+  // far-field ghost entries (row, col) int32 + the far-field state
+  p.off_ff = o;
+  o += align256(m.ff_row.size() * 2 * sizeof(int32_t)) + 256;
   // interior / boundary tile lists of the fused paths (tiles of >= 8 elements)
   p.off_tiles = o;
   o += align256(((size_t)m.K / 8 + 2) * sizeof(int32_t));
@@ -775,6 +799,15 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         CUDA_OK(cudaStreamSynchronize(st));
       }
     }
+    c->ff_n = (int64_t)m.ff_row.size();
+    if (c->ff_n > 0) {
+      c->ff_row = (int32_t*)(base + p.off_ff);
+      c->ff_col = c->ff_row + c->ff_n;
+      c->ff_state = (double*)(base + p.off_ff + align256(c->ff_n * 2 * sizeof(int32_t)));
+      CUDA_OK(cudaMemcpyAsync(c->ff_row, m.ff_row.data(), c->ff_n * 4, cudaMemcpyHostToDevice, st));
+      CUDA_OK(cudaMemcpyAsync(c->ff_col, m.ff_col.data(), c->ff_n * 4, cudaMemcpyHostToDevice, st));
+      c->ff_pending = true;
+    }
     std::vector<ExtMetric> xm(m.nsub * r.next);
     for (int i = 0; i < m.nsub * r.next; ++i)
       xm[i] = ExtMetric{m.sscale[i], m.nleft[i][0], m.nleft[i][1], m.nleft[i][2]};
@@ -856,9 +889,9 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       return SDRT_E_UNSUPPORTED;
     }
     c->sops.fr = O.scheme != 0;
-    if (m.slabs.size() > 0 && !c->fused && !c->sfused) {
+    if ((m.slabs.size() > 0 || !m.ff_row.empty()) && !c->fused && !c->sfused) {
       delete c;
-      set_error("unsupported: halo exchange is implemented for the fused paths only");
+      set_error("unsupported: halo exchange and far-field boundaries are implemented for the fused paths only");
       return SDRT_E_UNSUPPORTED;
     }
     if (c->sfused) {
@@ -1226,6 +1259,10 @@ sdrt_status sdrt_residual(sdrt_ctx* c, const double* d_U, double* d_dUdt, void* 
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->ff_pending) {
+      set_error("far-field boundaries not set: call sdrt_ctx_set_farfield first");
+      return SDRT_E_INVALID_ARG;
+    }
     if (c->comm) {
       comm_residual(c, d_U, d_dUdt, st);
       CUDA_OK(cudaGetLastError());
@@ -1269,6 +1306,10 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->ff_pending) {
+      set_error("far-field boundaries not set: call sdrt_ctx_set_farfield first");
+      return SDRT_E_INVALID_ARG;
+    }
     if (c->comm) {
       static const int rk4[4] = {0, 1, 2, 3};
       for (int done = 0; done < nsteps;) {
@@ -1330,6 +1371,10 @@ sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int 
   SDRT_TRY({
     c->launches = 0;
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->ff_pending) {
+      set_error("far-field boundaries not set: call sdrt_ctx_set_farfield first");
+      return SDRT_E_INVALID_ARG;
+    }
     if (c->comm) {
       static const int rk54[5] = {RK54_STAGE0, RK54_STAGE0 + 1, RK54_STAGE0 + 2, RK54_STAGE0 + 3, RK54_STAGE0 + 4};
       for (int done = 0; done < nsteps;) {
@@ -1759,3 +1804,26 @@ sdrt_status sdrt_ctx_attach_comm(sdrt_ctx* c, const uint8_t id[128], int rank, i
 }
 
 }  // extern "C"
+
+extern "C" sdrt_status sdrt_ctx_set_farfield(sdrt_ctx* c, const double* state, void* stream) {
+  if (!c || !state) {
+    set_error("null argument");
+    return SDRT_E_INVALID_ARG;
+  }
+  if (c->ff_n == 0) {
+    set_error("the mesh has no far-field boundaries (all axes periodic)");
+    return SDRT_E_INVALID_ARG;
+  }
+  SDRT_TRY({
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_OK(cudaMemcpyAsync(c->ff_state, state, c->nv * sizeof(double), cudaMemcpyHostToDevice, st));
+    const int64_t tot = c->ff_n * c->nv;
+    k_ff_fill<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(c->Tu[0], c->Tu[1], c->visc ? c->Tg : nullptr, c->g.Kt,
+                                                             c->nv, c->ff_row, c->ff_col, c->ff_n, c->ff_state,
+                                                             c->sfused);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(st));  // the host state buffer may go away
+    c->ff_pending = false;
+    return SDRT_OK;
+  })
+}

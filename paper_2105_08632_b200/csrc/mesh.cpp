@@ -84,8 +84,9 @@ int64_t Mesh::global_id(int64_t e) const {
 }
 
 Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const double hi[3], int rank,
-                int nranks, const int pgrid[3]) {
+                int nranks, const int pgrid[3], const int periodic[3]) {
   Mesh m;
+  for (int d = 0; d < 3; ++d) m.periodic[d] = (periodic && d < etype_dim(etype)) ? (periodic[d] != 0) : 1;
   m.etype = etype;
   m.p = p;
   m.nd = etype_dim(etype);
@@ -296,8 +297,11 @@ void build_halo(Mesh& m, bool force_self_halo) {
   const int D = m.nd;
   m.slabs.clear();
   int64_t cur = m.K_pad;
+  m.ff_row.clear();
+  m.ff_col.clear();
   for (int d = 0; d < 3; ++d) {
-    m.halo[d] = d < D && (m.pgrid[d] > 1 || force_self_halo);
+    // ghost columns on partition axes, loopback axes and far-field (non-periodic) axes
+    m.halo[d] = d < D && (m.pgrid[d] > 1 || force_self_halo || !m.periodic[d]);
     for (int side = 0; side < 2; ++side) m.gbase[d][side] = 0;
   }
   for (int d = 0; d < D; ++d) {
@@ -324,7 +328,10 @@ void build_halo(Mesh& m, bool force_self_halo) {
       S.d = d;
       S.side = side;
       int pc[3] = {rc[0], rc[1], rc[2]};
-      pc[d] = (pc[d] + (side ? 1 : -1) + m.pgrid[d]) % m.pgrid[d];
+      pc[d] += side ? 1 : -1;
+      // a far-field side: the block's face lies on a non-periodic domain boundary
+      const bool farfield = !m.periodic[d] && (pc[d] < 0 || pc[d] >= m.pgrid[d]);
+      pc[d] = (pc[d] + m.pgrid[d]) % m.pgrid[d];
       S.peer = rank_of(pc);
       const int dir = side ? 1 : -1;
       // my boundary layer facing `side`, and my ghost slab on `side` (the peer's layer)
@@ -361,6 +368,11 @@ void build_halo(Mesh& m, bool force_self_halo) {
                 }
             }
         }
+      if (farfield) {  // nothing to exchange: the ghost entries are filled with the far field
+        m.ff_row.insert(m.ff_row.end(), S.recv_row.begin(), S.recv_row.end());
+        m.ff_col.insert(m.ff_col.end(), S.recv_col.begin(), S.recv_col.end());
+        continue;
+      }
       m.slabs.push_back(S);
     }
   }

@@ -29,6 +29,11 @@ struct HaloSlab {
 };
 
 struct Mesh {
+  int periodic[3] = {1, 1, 1};  // 0: far-field boundaries on this axis
+  // far-field ghost trace entries (trace row, ghost column): the rows of the ghost element
+  // across a far-field boundary face that the boundary element reads; filled once with
+  // the far-field state (sdrt_ctx_set_farfield), never exchanged
+  std::vector<int32_t> ff_row, ff_col;
   int etype, p, nd, nsub;
   int Nloc[3], Nglob[3], offset[3];
   int rank, nranks, pgrid[3];
@@ -57,7 +62,7 @@ struct Mesh {
 };
 
 Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const double hi[3], int rank,
-                int nranks, const int pgrid[3]);
+                int nranks, const int pgrid[3], const int periodic[3] = nullptr);
 // (Re)build the ghost layout and halo lists; force_self_halo routes periodic wraps of
 // single-rank axes through the halo path as well (loopback testing on one device).
 void build_halo(Mesh& m, bool force_self_halo);

@@ -89,6 +89,7 @@ lib.sdrt_ctx_kernel_times.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.P
 lib.sdrt_ctx_last_launches.argtypes = [_vp]
 lib.sdrt_ctx_last_launches.restype = ctypes.c_int64
 lib.sdrt_comm_unique_id.argtypes = [_vp]
+lib.sdrt_ctx_set_farfield.argtypes = [_vp, _vp, _vp]
 lib.sdrt_ctx_attach_comm.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int]
 lib.sdrt_ctx_destroy.argtypes = [_vp]
 lib.sdrt_ctx_destroy.restype = None
@@ -100,7 +101,7 @@ EXPORTED = ["sdrt_abi_version", "sdrt_last_error", "sdrt_mesh_create", "sdrt_mes
             "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_kernel_times",
             "sdrt_mesh_set_halo", "sdrt_mesh_halo_lists", "sdrt_mesh_neighbor", "sdrt_halo_info",
             "sdrt_halo_pack", "sdrt_halo_unpack", "sdrt_stage_traces", "sdrt_stage_grad", "sdrt_stage_flux",
-            "sdrt_comm_unique_id", "sdrt_ctx_attach_comm"]
+            "sdrt_comm_unique_id", "sdrt_ctx_attach_comm", "sdrt_ctx_set_farfield"]
 
 
 def _check(code):
@@ -117,16 +118,17 @@ def last_error():
 
 
 # ------------------------------------------------------------------ meshes
-def mesh_create(etype, p, N, lo, hi, rank=0, nranks=1, pgrid=None):
+def mesh_create(etype, p, N, lo, hi, rank=0, nranks=1, pgrid=None, periodic=None):
     et = ETYPES[etype] if isinstance(etype, str) else int(etype)
     N3 = list(N) + [1] * (3 - len(N))
     lo3 = list(lo) + [0.0] * (3 - len(lo))
     hi3 = list(hi) + [1.0] * (3 - len(hi))
+    per = [1, 1, 1] if periodic is None else [int(bool(x)) for x in periodic] + [1] * (3 - len(periodic))
     pg = None
     if pgrid is not None:
         pg = (ctypes.c_int * 3)(*(list(pgrid) + [1] * (3 - len(pgrid))))
     out = _vp()
-    _check(lib.sdrt_mesh_create(et, p, _i3(*N3), _d3(*lo3), _d3(*hi3), _i3(1, 1, 1), rank, nranks, pg,
+    _check(lib.sdrt_mesh_create(et, p, _i3(*N3), _d3(*lo3), _d3(*hi3), _i3(*per), rank, nranks, pg,
                                 ctypes.byref(out)))
     return out
 
@@ -237,6 +239,12 @@ def ctx_create(m, o, ph, ws_ptr, ws_bytes, stream):
 
 def residual(ctx, U_ptr, dUdt_ptr, stream):
     _check(lib.sdrt_residual(ctx, _vp(U_ptr), _vp(dUdt_ptr), _vp(stream)))
+
+
+def ctx_set_farfield(ctx, state, stream):
+    """Far-field exterior state (N_V conserved values, host) of the non-periodic axes."""
+    st = np.ascontiguousarray(np.asarray(state, dtype=np.float64))
+    _check(lib.sdrt_ctx_set_farfield(ctx, st.ctypes.data, _vp(stream)))
 
 
 def comm_unique_id():

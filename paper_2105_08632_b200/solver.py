@@ -13,10 +13,11 @@ from . import sdrt
 
 class Solver:
     def __init__(self, etype, p, N, lo, hi, eq, device="cuda", rank=0, nranks=1, pgrid=None, _pre_ctx=None,
-                 force_self_halo=False, scheme="sdrt", **phys):
+                 force_self_halo=False, scheme="sdrt", periodic=None, farfield=None, **phys):
         D = 2 if etype in ("quad", "tri") else 3
         Nl = list(N) if np.ndim(N) else [int(N)] * D
-        self.mesh = sdrt.mesh_create(etype, p, Nl, lo, hi, rank=rank, nranks=nranks, pgrid=pgrid)
+        self.mesh = sdrt.mesh_create(etype, p, Nl, lo, hi, rank=rank, nranks=nranks, pgrid=pgrid,
+                                     periodic=periodic)
         if _pre_ctx is not None:
             _pre_ctx(self.mesh)
         elif force_self_halo:
@@ -36,6 +37,8 @@ class Solver:
         self._ws_bytes = nbytes
         stream = torch.cuda.current_stream(self.device).cuda_stream
         self.ctx = sdrt.ctx_create(self.mesh, self.ops, self.phys, self._ws_ptr, nbytes, stream)
+        if farfield is not None:  # exterior state of the non-periodic axes
+            sdrt.ctx_set_farfield(self.ctx, farfield, stream)
 
     @property
     def shape(self):

@@ -80,6 +80,26 @@ def test_mesh_maps_bit_exact(sdrt, etype, p, N):
         sdrt.mesh_destroy(m)
 
 
+@pytest.mark.parametrize("etype,p,N,per", [("quad", 2, (4, 3), (0, 1)), ("tri", 3, (4, 3), (0, 1)),
+                                           ("hex", 2, (3, 4, 3), (0, 1, 1)), ("tet", 2, (3, 3, 4), (1, 0, 1))])
+def test_farfield_mesh_maps_bit_exact(sdrt, etype, p, N, per):
+    """Far-field meshes (non-periodic axis): the face list (boundary
+    faces with -1 for the exterior side) and the left flags equal the oracle's."""
+    D = len(N)
+    lo, hi = [0.0] * D, [1.0 + 0.5 * d for d in range(D)]
+    m = sdrt.mesh_create(etype, p, list(N), lo, hi, periodic=per)
+    try:
+        fe, fl, fp, il = sdrt.mesh_export_maps(m)
+        M = build_mesh(etype, p, tuple(N), lo, hi, periodic=per)
+        assert (fe < 0).any()
+        assert np.array_equal(fe, M.face_elem)
+        assert np.array_equal(fl, M.face_lface)
+        assert np.array_equal(fp, M.face_perm)
+        assert np.array_equal(il.astype(bool), M.is_left)
+    finally:
+        sdrt.mesh_destroy(m)
+
+
 def test_errors_are_reported(sdrt):
     with pytest.raises(sdrt.SdrtError) as e:
         sdrt.operators_build("tet", 4)

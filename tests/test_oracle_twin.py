@@ -58,8 +58,9 @@ def _dmono(e, x, c):
 
 
 class Twin:
-    def __init__(self, etype, p, mesh, ph):
+    def __init__(self, etype, p, mesh, ph, farfield=None):
         self.ph, self.m = ph, mesh
+        self.farfield = farfield
         ref = reference_element(etype, p)
         D = self.D = ref.nd
         f = lambda pts: np.array([[float(c) for c in x] for x in pts])
@@ -87,16 +88,22 @@ class Twin:
         self.nphys = jn / np.linalg.norm(jn, axis=2)[..., None]
         # neighbours by coordinate matching modulo the periodic box
         L = mesh.hi - mesh.lo
+        per = np.array(mesh.periodic if getattr(mesh, "periodic", ()) else [True] * D)
         tol = 1e-9 * float(np.min(mesh.h))
         P = self.xphys_ext.reshape(K * self.next, D)
         self.nbr = np.empty((K, self.next, 2), dtype=np.int64)
         for e in range(K):
             for s in range(self.next):
                 d = P - self.xphys_ext[e, s]
-                d -= L * np.round(d / L)
+                d -= np.where(per, L * np.round(d / L), 0.0)
                 dist = np.abs(d).max(axis=1)
                 nn = self.nphys.reshape(K * self.next, D)
                 cand = np.nonzero((dist < tol) & (np.abs(nn + self.nphys[e, s]).max(axis=1) < 1e-12))[0]
+                if len(cand) == 0:  # far-field boundary point: the exterior is the far field
+                    x = self.xphys_ext[e, s] - mesh.lo
+                    assert any(not per[c] and (abs(x[c]) < tol or abs(x[c] - L[c]) < tol) for c in range(D))
+                    self.nbr[e, s] = (-1, -1)
+                    continue
                 assert len(cand) == 1, (e, s, cand)
                 self.nbr[e, s] = divmod(int(cand[0]), self.next)
         # left rule O14 re-derived: first non-zero component of the physical normal > 0
@@ -117,14 +124,15 @@ class Twin:
         nsol, NV, K = U.shape
         ext = lambda e: [self.interp(U[:, :, e], self.xf[s]) for s in range(self.next)]
         uext = np.array([ext(e) for e in range(K)])                      # K x N_ext x NV
+        ff = self.farfield
+        uout = lambda e, s: ff if self.nbr[e, s, 0] < 0 else uext[self.nbr[e, s, 0], self.nbr[e, s, 1]]
         q_sol = None
         if ph.viscous:
             q_sol = np.zeros((K, nsol, D, NV))
             for e in range(K):
                 w = np.zeros((len(self.xf), NV))
                 for s in range(self.next):
-                    f2, s2 = self.nbr[e, s]
-                    uo = uext[f2, s2]
+                    uo = uout(e, s)
                     w[s] = phys.common_value(ph, uext[e, s], uo) if self.left[e, s] else \
                         phys.common_value(ph, uo, uext[e, s])
                 for i in range(self.next, len(self.xf)):
@@ -137,15 +145,17 @@ class Twin:
             vals = np.zeros((len(self.xf), NV))
             for s in range(self.next):
                 f2, s2 = self.nbr[e, s]
-                ui, uo = uext[e, s], uext[f2, s2]
-                qi, qo = qat(e, self.xf[s]), qat(f2, self.xf[s2])
+                ui, uo = uext[e, s], uout(e, s)
+                qi = qat(e, self.xf[s])
+                qo = None if qi is None else (np.zeros_like(qi) if f2 < 0 else qat(f2, self.xf[s2]))
+                nout = -self.nphys[e, s] if f2 < 0 else self.nphys[f2, s2]   # the exterior's normal
                 col = lambda a: a[:, None]
                 colq = lambda a: None if a is None else a[:, :, None]
                 if self.left[e, s]:
                     F = phys.common_flux(ph, col(ui), col(uo), colq(qi), colq(qo), self.nphys[e, s])[:, 0]
                     vals[s] = self.scale[e, s] * F
                 else:
-                    F = phys.common_flux(ph, col(uo), col(ui), colq(qo), colq(qi), self.nphys[f2, s2])[:, 0]
+                    F = phys.common_flux(ph, col(uo), col(ui), colq(qo), colq(qi), nout)[:, 0]
                     vals[s] = -self.scale[e, s] * F
             for i in range(self.next, len(self.xf)):
                 u = self.interp(U[:, :, e], self.xf[i])[:, None]
@@ -281,3 +291,31 @@ def test_isentropic_vortex_design_order(etype, p):
     import math
     e1, e2 = _vortex_l2(etype, p, 20), _vortex_l2(etype, p, 40)
     assert abs(math.log2(e1 / e2) - (p + 1)) < 0.7, (e1, e2)
+
+
+# ----------------------------------------------------------------- far-field boundaries
+@pytest.mark.parametrize("etype,p", [("quad", 2), ("tri", 3), ("hex", 2), ("tet", 2)])
+@pytest.mark.parametrize("eq", ["linadvdiff", "euler", "ns"])
+def test_farfield_twin_and_freestream(etype, p, eq):
+    """Far-field boundaries (NEXT row N4): x-boundaries take a constant
+    exterior state, other axes periodic.  The definition-form twin (exterior = the far
+    field, zero exterior gradient, left/right by O14 re-derived) equals the matrix form,
+    and a constant state equal to the far field is preserved (residual ~ 0)."""
+    D = ND[etype]
+    ph = Physics(eq, D, c=(0.7, -0.4, 0.3)[:D], mu=0.05, gamma=1.4, Pr=0.71,
+                 beta=0.5 if eq != "euler" else 0.0, eta=0.1 if eq != "euler" else 0.0)
+    rng = np.random.default_rng(17)
+    per = (False,) + (True,) * (D - 1)
+    m = build_mesh(etype, p, (3,) + (2,) * (D - 1), [0.0] * D, [1.0 + 0.3 * d for d in range(D)], periodic=per)
+    nsol = len(reference_element(etype, p).xsol)
+    U = _state(ph, nsol, m.K, rng)
+    ff = U[0, :, 0].copy()
+    R = Residual(m, ph, farfield=ff)
+    r_mat = R(U)
+    r_twin = Twin(etype, p, m, ph, farfield=ff).residual(U)
+    nv = r_mat.shape[1]
+    groups = [[0]] if nv == 1 else [[0], list(range(1, nv - 1)), [nv - 1]]
+    for g in groups:
+        assert np.abs(r_twin[:, g] - r_mat[:, g]).max() <= 1e-11 * np.abs(r_mat[:, g]).max()
+    const = np.broadcast_to(ff[None, :, None], U.shape).copy()
+    assert np.abs(R(const)).max() <= 1e-12 * max(1.0, np.abs(ff).max())
