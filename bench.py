@@ -433,6 +433,16 @@ def main():
     if os.path.exists(tf):
         traffic = json.load(open(tf)).get(dom)
     kf = kernel_flops(cfg, K)
+    flops_source = "model (bench.kernel_flops)"
+    sc = os.path.join(ROOT, "profiles", "r02_sass_counts.json")
+    if os.path.exists(sc) and world == 1:
+        # executed fp64 flops of the tensor kernels from ncu SASS counts (2 DFMA + DMUL +
+        # DADD per launch, profiles/r02_sass_counts.json) replace the model
+        sass = json.load(open(sc)).get(cfg.name, {})
+        for kn, v in sass.items():
+            if kn.startswith("tensor_") and kn in kf:
+                kf[kn] = v["flops_per_launch"]
+                flops_source = f"ncu SASS counts (profiles/r02_sass_counts.json) for the tensor kernels"
     t_launch = dom_ms / dom_n * 1e-3 if dom else None
     gbs = kb[dom] / t_launch / 1e9 if dom in kb else None
     tfs = kf[dom] / t_launch / 1e12 if dom in kf else None
@@ -447,7 +457,7 @@ def main():
     else:
         roof = {"bound": "hbm", "kernel": dom, "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": f_hbm,
                 "traffic": traffic, "peak_source": peak_note}
-    roof.update({"bytes_per_launch": kb.get(dom), "flops_per_launch": kf.get(dom),
+    roof.update({"bytes_per_launch": kb.get(dom), "flops_per_launch": kf.get(dom), "flops_source": flops_source,
                  "hbm_frac": f_hbm, "fp64_frac": f_alu,
                  "avg_launch_ms": dom_ms / dom_n if dom else None,
                  "launches_per_step": dom_n / args.steps if dom else None,

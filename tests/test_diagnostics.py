@@ -30,7 +30,10 @@ def _diag(name, N):
 def test_tgv_initial_energy_and_pressure_dissipation(name, N):
     (E, eps2, eps3), mu = _diag(name, N)
     assert abs(E - 0.25) <= 1e-12
-    assert abs(eps3) <= 1e-12 * eps2
+    # eps3 = -<p div v> with div v = 0: round-off of an integrand p (~p_inf = 71.4) times
+    # a unit-size gradient, so the scale is p_inf, not eps2 (~mu = 1/1600)
+    pinf = 1.0 / (1.4 * 0.1 ** 2)
+    assert abs(eps3) <= 1e-13 * pinf
 
 
 @pytest.mark.parametrize("name,N1,N2,tol2", [("c4", 4, 8, 1e-5), ("c5", 3, 4, 2e-2)])
