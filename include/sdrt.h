@@ -45,8 +45,12 @@ typedef enum {
   SDRT_E_INTERNAL = -8
 } sdrt_status;
 
-/* element types (App. A); N_p = 1, 2, 1, 6 sub-cells per pattern (l.499) */
-typedef enum { SDRT_QUAD = 0, SDRT_TRI = 1, SDRT_HEX = 2, SDRT_TET = 3 } sdrt_etype;
+/* element types (App. A); N_p = 1, 2, 1, 6, 2 sub-cells per pattern (l.499).
+ * Prisms (NEXT row N3, l.2633-2737; p <= 3, SDRT scheme) mix triangular and
+ * quadrilateral faces: faces 0, 1 (z = -1, +1) carry (p+1)(p+2)/2 points, faces 2-4
+ * (p+1)^2; nfp reports the largest face and face_perm rows are padded with -1; they
+ * run on the generic operator path (no fused prism kernels). */
+typedef enum { SDRT_QUAD = 0, SDRT_TRI = 1, SDRT_HEX = 2, SDRT_TET = 3, SDRT_PRI = 4 } sdrt_etype;
 /* schemes: SDRT (the path); FR-SDRT and FR-DG flux reconstruction on the same data
  * (NEXT row N1): no internal flux points, solution-point fluxes
  * with the SDRT (FR-SDRT) or DG (FR-DG: Radau on tensor elements, DG lifting on

@@ -44,6 +44,10 @@ def tet_subcells():
 def subcell_vertices(etype):
     if etype == "tri":
         return [list(map(np.array, s)) for s in TRI_SUB]
+    if etype == "pri":
+        # the triangle split extruded in z: images of the reference vertices V0, V1, V2
+        # (z = -1) and of V0 at z = +1 (N_p = 2 prisms per hexahedron)
+        return [[np.array(v + (0,)) for v in s] + [np.array(s[0] + (1,))] for s in TRI_SUB]
     if etype == "tet":
         return [list(map(np.array, s)) for s in tet_subcells()]
     return None
@@ -127,11 +131,15 @@ def build_mesh(etype, p, N, lo, hi, periodic=None):
     L = hi - lo
     xr = ops.xext + 1.0
     xe = np.einsum("kij,sj->ksi", J, xr) + x0[:, None, :]     # K x N_ext x D
-    nf, nfp = ops.nfaces, ops.nfp
-    xe = xe.reshape(K, nf, nfp, D)
+    nf, nfp = ops.nfaces, ops.nfp                              # nfp: largest face
+    fp = np.asarray(ops.face_ptr, dtype=np.int64)              # face f: points fp[f]..fp[f+1]
+    nq = np.diff(fp)
+    # face points padded to nfp (NaN beyond a face's own count: prisms mix face types)
+    xe = np.stack([np.concatenate([xe[:, fp[f]:fp[f + 1]], np.full((K, nfp - nq[f], D), np.nan)], axis=1)
+                   for f in range(nf)], axis=1)                # K x nf x nfp x D
     tol = 1e-9 * float(np.min(h))
     # face key: centroid wrapped into the periodic box (periodic axes only), rounded
-    cen = xe.mean(axis=2)
+    cen = np.nanmean(xe, axis=2)
     cen = np.where(per, np.mod(cen - lo + 0.5 * tol, L) - 0.5 * tol, cen - lo)
     key = np.round(cen / (1e-6 * float(np.min(h)))).astype(np.int64).reshape(K * nf, D)
     order = np.lexsort(key.T[::-1])
@@ -173,15 +181,23 @@ def build_mesh(etype, p, N, lo, hi, periodic=None):
     pt = np.where(paired, partner, np.arange(K * nf))
     d = xf[pt][:, None, :, :] - xf[:, :, None, :]              # [face, q, q', D]
     d = d - np.where(per, L * np.round(d / L), 0.0)
-    dist = np.max(np.abs(d), axis=3)
+    dist = np.nan_to_num(np.max(np.abs(d), axis=3), nan=np.inf)
     perm_all = np.argmin(dist, axis=2)                         # [face, q] -> q'
-    if np.any(np.take_along_axis(dist, perm_all[..., None], axis=2)[paired] > tol):
+    valid = np.arange(nfp)[None, :] < np.tile(nq, K)[:, None]  # real points of each face
+    if np.any((np.take_along_axis(dist, perm_all[..., None], axis=2)[..., 0] > tol) & valid & paired[:, None]):
         raise ValueError("face point matching failed")
     perm_all[~paired] = -1
+    perm_all[~valid] = -1
     pe = np.where(paired, partner // nf, -1)
     pf = np.where(paired, partner % nf, -1)
-    nbr_elem = np.repeat(pe.reshape(K, nf), nfp, axis=1).T.copy()          # N_ext x K (-1: far field)
-    nbr_pt = np.where(perm_all < 0, -1, pf[:, None] * nfp + perm_all).reshape(K, nf * nfp).T.copy()
+    # per external point of each element: neighbour element and its matching point
+    nbr_elem = np.full((ops.next, K), -1, dtype=np.int64)
+    nbr_pt = np.full((ops.next, K), -1, dtype=np.int64)
+    pe2, pf2, pa2 = pe.reshape(K, nf), pf.reshape(K, nf), perm_all.reshape(K, nf, nfp)
+    for f in range(nf):
+        for q in range(nq[f]):
+            nbr_elem[fp[f] + q] = pe2[:, f]
+            nbr_pt[fp[f] + q] = np.where(pa2[:, f, q] < 0, -1, fp[np.maximum(pf2[:, f], 0)] + pa2[:, f, q])
     # faces in (element, local face) scan order: those whose left element this is, and
     # far-field faces (exterior side -1, listed from the interior element)
     lidx = np.nonzero(flat_left | ~paired)[0]

@@ -50,15 +50,30 @@ def _exps_homog(D, p):
 
 
 def sol_span(etype, p, D):
-    """Exponents of the solution modal space: P_p (simplex) or Q_p (tensor)."""
+    """Exponents of the solution modal space: P_p (simplex), Q_p (tensor), or
+    P_p(x, y) x P_p(z) (prism, l.2731-2733)."""
     if etype in ("tri", "tet"):
         return _exps_total(D, p)
+    if etype == "pri":
+        return [(a, b, c) for c in range(p + 1) for (a, b) in _exps_total(2, p)]
     return list(itertools.product(range(p + 1), repeat=D))
 
 
 def rt_span(etype, p, D):
     """RT modal space as vector polynomials: list of [(component, exponent), ...]."""
     out = []
+    if etype == "pri":
+        # [P_p(x,y)^2 (+) (x,y) P~_p(x,y)] P_p(z)  x  P_p(x,y) P_{p+1}(z)   (l.2640-2642)
+        for c in range(p + 1):
+            for cmp_ in range(2):
+                for (a, b) in _exps_total(2, p):
+                    out.append([(cmp_, (a, b, c))])
+            for (a, b) in _exps_homog(2, p):
+                out.append([(0, (a + 1, b, c)), (1, (a, b + 1, c))])
+        for c in range(p + 2):
+            for (a, b) in _exps_total(2, p):
+                out.append([(2, (a, b, c))])
+        return out
     if etype in ("tri", "tet"):
         for c in range(D):
             for e in _exps_total(D, p):
@@ -112,6 +127,10 @@ def _rt_div(terms, x):
 
 def _mono_integral(etype, e):
     """Exact integral of x^e over the reference element (rational, as Decimal)."""
+    if etype == "pri":
+        tri = _mono_integral("tri", e[:2])
+        zi = Fraction(2, e[2] + 1) if e[2] % 2 == 0 else 0
+        return tri * Decimal(zi.numerator) / Decimal(zi.denominator) if zi else Decimal(0)
     if etype in ("quad", "hex"):
         v = Fraction(1)
         for ei in e:
@@ -203,7 +222,7 @@ class Operators:
     nint: int
     nu: int
     nfaces: int
-    nfp: int
+    nfp: int            # points of the largest face (all faces but the prism's)
     M0: np.ndarray      # N_ext x N_sol
     M12: np.ndarray     # N_u x N_sol
     M13: np.ndarray     # N_sol x N_int
@@ -220,6 +239,7 @@ class Operators:
     xu: np.ndarray
     cond_flux: float    # 1-norm condition of V(f), diagnostics
     face_normals: np.ndarray
+    face_ptr: tuple = ()  # face f: ext points face_ptr[f] .. face_ptr[f+1]
 
 
 @lru_cache(maxsize=None)
@@ -294,6 +314,7 @@ def build_operators(etype, p):
         ext_normal=arr(ref.next_normal), ext_face=np.array(ref.ext_face, dtype=np.int64),
         xsol=arr(ref.xsol), xext=arr(ref.xext), xu=arr(ref.xu),
         cond_flux=cond_num * cond_den, face_normals=arr(ref.face_normals),
+        face_ptr=tuple(int(v) for v in ref.face_ptr),
     )
 
 

@@ -44,8 +44,8 @@ from .simplex_rules import simplex_rule
 
 mp.mp.dps = 40
 
-NDIM = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}
-NSUB = {"quad": 1, "tri": 2, "hex": 1, "tet": 6}  # N_p
+NDIM = {"quad": 2, "tri": 2, "hex": 3, "tet": 3, "pri": 3}
+NSUB = {"quad": 1, "tri": 2, "hex": 1, "tet": 6, "pri": 2}  # N_p
 
 TRI_V = [(-1, -1), (1, -1), (-1, 1)]
 TET_V = [(-1, -1, -1), (1, -1, -1), (-1, 1, -1), (-1, -1, 1)]
@@ -124,6 +124,7 @@ class RefElement:
     int_u: list                     # N_int: unique index of each internal point
     int_dir: list                   # N_int: axis d of the DOF normal e_d
     face_normals: list = field(default_factory=list)
+    face_ptr: list = field(default_factory=list)   # face f: ext points face_ptr[f] .. face_ptr[f+1]
 
     @property
     def nsol(self):
@@ -199,7 +200,7 @@ def _tensor(etype, p):
                         int_u.append(len(xu)); int_dir.append(d)
                         xu.append((axes[0][c0], axes[1][c1], axes[2][c2]))
     return RefElement(etype, p, D, xsol, xext, nrm, fid, 2 * D, n ** (D - 1),
-                      xu, int_u, int_dir, fnorms)
+                      xu, int_u, int_dir, fnorms, [f * n ** (D - 1) for f in range(2 * D + 1)])
 
 
 def _simplex(etype, p):
@@ -234,15 +235,64 @@ def _simplex(etype, p):
     for u in range(len(xu)):
         for d in range(D):
             int_u.append(u); int_dir.append(d)
-    return RefElement(etype, p, D, xsol, xext, nrm, fid, D + 1, nfp, xu, int_u, int_dir, fnorms)
+    return RefElement(etype, p, D, xsol, xext, nrm, fid, D + 1, nfp, xu, int_u, int_dir, fnorms,
+                      [f * nfp for f in range(D + 2)])
+
+
+def _prism(p):
+    """Triangular prism (App. A l.2633-2737): reference x, y >= -1, x + y <= 0,
+    z in [-1, 1].  Solution points: the triangle's solution points x (p+1) GL levels in z
+    (l.2731-2733).  External flux points: faces 0 (z = -1) and 1 (z = +1) carry the
+    triangle rule of (p+1)(p+2)/2 points (the tet-face rule of reading O1), faces 2 (y = -1),
+    3 (x + y = 0), 4 (x = -1) the (p+1)^2 GL points (edge GL x GL in z; l.2718-2720).
+    Internal flux points (l.2723-2729): set 1 = the triangle's interior rule x (p+1) GL
+    levels, two DOFs each (normals e_x, e_y); set 2 = the triangle-face rule x the p zeros
+    of P_p in z (reading O3 as for tensor elements), one DOF (e_z).  Orders: z level
+    slowest, triangle point fastest; internal points set 1 then set 2, each unique point's
+    DOFs in axis order."""
+    V = [tuple(mp.mpf(c) for c in v) for v in TRI_V]
+    g, _ = gauss_legendre(p + 1)
+    z, _ = gauss_legendre(p) if p >= 1 else ((), ())
+    tri_sol = [bary_to_x(l, V) for l in lattice(2, p)]
+    xsol = [(x[0], x[1], zz) for zz in g for x in tri_sol]
+    s2 = 1 / mp.sqrt(2)
+    z0 = mp.mpf(0)
+    fnorms = [(z0, z0, mp.mpf(-1)), (z0, z0, mp.mpf(1)), (z0, mp.mpf(-1), z0), (s2, s2, z0), (mp.mpf(-1), z0, z0)]
+    tface = [bary_to_x(l, V) for l in simplex_rule(2, (p + 1) * (p + 2) // 2)[0]]
+    xext, nrm, fid, fptr = [], [], [], [0]
+    for f, zz in ((0, mp.mpf(-1)), (1, mp.mpf(1))):
+        for x in tface:
+            xext.append((x[0], x[1], zz)); nrm.append(fnorms[f]); fid.append(f)
+        fptr.append(len(xext))
+    for f, (a, b) in zip((2, 3, 4), TRI_FACES):
+        for zz in g:
+            for t in g:
+                lam = (t + 1) / 2
+                xext.append(tuple(V[a][c] + lam * (V[b][c] - V[a][c]) for c in range(2)) + (zz,))
+                nrm.append(fnorms[f]); fid.append(f)
+        fptr.append(len(xext))
+    tint = [bary_to_x(l, V) for l in simplex_rule(2, p * (p + 1) // 2)[0]] if p >= 1 else []
+    xu, int_u, int_dir = [], [], []
+    for zz in g:                       # set 1: 2-D normals
+        for x in tint:
+            for d in range(2):
+                int_u.append(len(xu)); int_dir.append(d)
+            xu.append((x[0], x[1], zz))
+    for zz in z:                       # set 2: z normal
+        for x in tface:
+            int_u.append(len(xu)); int_dir.append(2)
+            xu.append((x[0], x[1], zz))
+    return RefElement("pri", p, 3, xsol, xext, nrm, fid, 5, (p + 1) ** 2, xu, int_u, int_dir, fnorms, fptr)
 
 
 @lru_cache(maxsize=None)
 def reference_element(etype, p):
-    if p < 1 or p > 4 or (etype == "tet" and p > 3):
-        raise ValueError("unsupported degree: quad/hex/tri p in [1,4], tet p in [1,3]")
+    if p < 1 or p > 4 or (etype in ("tet", "pri") and p > 3):
+        raise ValueError("unsupported degree: quad/hex/tri p in [1,4], tet/pri p in [1,3]")
     if etype in ("quad", "hex"):
         return _tensor(etype, p)
     if etype in ("tri", "tet"):
         return _simplex(etype, p)
+    if etype == "pri":
+        return _prism(p)
     raise ValueError(etype)

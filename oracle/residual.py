@@ -44,9 +44,10 @@ class Residual:
         nrm = np.linalg.norm(jn, axis=2)                          # N_ext x K
         self.s = np.concatenate([m.detJ[None, :] * nrm, np.zeros((o.next, 1))], axis=1)
         self.nphys = jn / nrm[..., None]                          # N_ext x K x D
-        # face-point lists (flattened over faces x face points); -1 (far field) -> ghost K
-        nfp = o.nfp
-        F = m.face_elem.shape[0]
+        # face-point lists (flattened over faces x face points); -1 (far field) -> ghost K.
+        # Face f's points are o.face_ptr[f] .. o.face_ptr[f+1] (prisms mix face sizes);
+        # face_perm rows are padded with -1 beyond a face's own count.
+        fptr = np.asarray(o.face_ptr, dtype=np.int64)
         fe = m.face_elem.astype(np.int64)
         fl = m.face_lface.astype(np.int64)
         gL, gR = fe[:, 0] < 0, fe[:, 1] < 0
@@ -54,16 +55,19 @@ class Residual:
         if self.ghost_faces and farfield is None:
             raise ValueError("the mesh has far-field faces: pass the far-field state")
         self.farfield = None if farfield is None else np.asarray(farfield, dtype=np.float64)
-        q = np.tile(np.arange(nfp), F)
-        perm = m.face_perm.astype(np.int64).reshape(-1)
-        self.fL = np.repeat(np.where(gL, K, fe[:, 0]), nfp)
-        self.fR = np.repeat(np.where(gR, K, fe[:, 1]), nfp)
+        inner = np.where(gL, fl[:, 1], fl[:, 0])                  # a real local face of each face
+        n_of = np.diff(fptr)[inner]                                 # points per face
+        rep = lambda a: np.repeat(a, n_of)
+        q = np.concatenate([np.arange(n) for n in n_of]) if len(n_of) else np.zeros(0, dtype=np.int64)
+        perm = m.face_perm.astype(np.int64)[rep(np.arange(len(fe))), q]
+        self.fL = rep(np.where(gL, K, fe[:, 0]))
+        self.fR = rep(np.where(gR, K, fe[:, 1]))
         # a ghost side takes the interior side's point index (ghost traces are constant)
-        self.pL = np.where(np.repeat(gL, nfp), fl[:, 1].repeat(nfp) * nfp + q, fl[:, 0].repeat(nfp) * nfp + q)
-        self.pR = np.where(np.repeat(gL, nfp), self.pL,
-                           np.where(np.repeat(gR, nfp), self.pL, fl[:, 1].repeat(nfp) * nfp + perm))
+        base_L = fptr[np.where(gL, fl[:, 1], fl[:, 0])]
+        self.pL = rep(base_L) + q
+        self.pR = np.where(rep(gL) | rep(gR), self.pL, fptr[np.maximum(rep(fl[:, 1]), 0)] + perm)
         # the left element's outward unit normal (ghost left: minus the interior's)
-        gl = np.repeat(gL, nfp)
+        gl = rep(gL)
         nin = self.nphys[np.where(gl, self.pR, self.pL), np.where(gl, self.fR, self.fL)]
         self.nL = np.where(gl[:, None], -nin, nin).T              # D x (F.nfp)
 

@@ -21,7 +21,7 @@ sdrt_status sdrt_mesh_create(int etype, int p, const int N[3], const double lo[3
     sdrt::set_error("null argument");
     return SDRT_E_INVALID_ARG;
   }
-  if (etype < 0 || etype > 3) {
+  if (etype < 0 || etype > 4) {
     sdrt::set_error("unsupported element type");
     return SDRT_E_UNSUPPORTED;
   }
@@ -120,8 +120,9 @@ sdrt_status sdrt_mesh_export_maps(const sdrt_mesh* mm, int32_t* face_elem, int8_
         face_lface[2 * F] = (int8_t)(L.left ? f : -1);
         face_lface[2 * F + 1] = (int8_t)(L.left ? (ff ? -1 : L.nface) : f);
       }
-      if (face_perm)
-        for (int q = 0; q < r.nfp; ++q) face_perm[F * r.nfp + q] = (int16_t)(ff ? -1 : L.perm[q]);
+      if (face_perm)  // rows of nfp (the largest face), -1 beyond this face's points
+        for (int q = 0; q < r.nfp; ++q)
+          face_perm[F * r.nfp + q] = (int16_t)((ff || q >= (int)L.perm.size()) ? -1 : L.perm[q]);
       ++F;
     }
   }
@@ -246,7 +247,7 @@ sdrt_status sdrt_operators_build(int etype, int p, int scheme, sdrt_operators** 
     sdrt::set_error("unsupported scheme");
     return SDRT_E_UNSUPPORTED;
   }
-  if (etype < 0 || etype > 3) {
+  if (etype < 0 || etype > 4) {
     sdrt::set_error("unsupported element type");
     return SDRT_E_UNSUPPORTED;
   }

@@ -36,6 +36,8 @@ struct GeomDev {
   int8_t off[MAXSUB][MAXF][3];
   int8_t nshape[MAXSUB][MAXF], nface[MAXSUB][MAXF], left[MAXSUB][MAXF];
   int8_t perm[MAXSUB][MAXF][MAXFP];
+  int16_t fptr[MAXF + 1];  // face f: ext points fptr[f] .. fptr[f+1] (prisms mix face sizes)
+  int8_t xface[MAXEXT];    // face of each ext point
   const int* tiles;       // optional tile list (interior / boundary subsets), nullptr = all
   int ntiles;
 };

@@ -95,9 +95,9 @@ __global__ void __launch_bounds__(256) k_common_value(GeomDev g, PhysDev ph, con
   const int e = blockIdx.y;
   if (n >= g.K) return;
   const int s = (int)(n % g.nsub);
-  const int f = e / g.nfp, q = e % g.nfp;
+  const int f = g.xface[e], q = e - g.fptr[f];
   const int64_t m = nbr_elem(g, n, s, f);
-  const int e2 = g.nface[s][f] * g.nfp + g.perm[s][f][q];
+  const int e2 = g.fptr[g.nface[s][f]] + g.perm[s][f][q];
   const bool left = g.left[s][f];
   const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(256) k_face_flux(GeomDev g, PhysDev ph, const 
   const int e = blockIdx.y;
   if (n >= g.K) return;
   const int s = (int)(n % g.nsub);
-  const int f = e / g.nfp, q = e % g.nfp;
+  const int f = g.xface[e], q = e - g.fptr[f];
   const int64_t m = nbr_elem(g, n, s, f);
-  const int e2 = g.nface[s][f] * g.nfp + g.perm[s][f][q];
+  const int e2 = g.fptr[g.nface[s][f]] + g.perm[s][f][q];
   const bool left = g.left[s][f];
   double um[NV], uo[NV], qm[D * NV], qo[D * NV];
 #pragma unroll
@@ -559,7 +559,8 @@ static PathKind choose_path(const Mesh& m, const sdrt_physics* ph) {
   const char* fg = getenv("SDRT_FORCE_GENERIC");
   if (fg && fg[0] == '1') return PATH_GENERIC;
   if (etype_tensor(m.etype)) return tensor_supported(m.nd, m.p, ph->eq) ? PATH_TENSOR : PATH_GENERIC;
-  return simplex_supported(m.nd, m.p, ph->eq) ? PATH_SIMPLEX : PATH_GENERIC;
+  if (m.etype == TRI || m.etype == TET) return simplex_supported(m.nd, m.p, ph->eq) ? PATH_SIMPLEX : PATH_GENERIC;
+  return PATH_GENERIC;  // prisms
 }
 
 static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph, std::vector<OpHost>* packed) {
@@ -599,7 +600,7 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   p.off_tu1 = o; o += tb;
   p.off_tg = o; o += tb;
   p.off_sops = o;
-  if (!etype_tensor(m.etype)) {
+  if (choose_path(m, ph) == PATH_SIMPLEX) {
     std::vector<OpHostF> s4;
     simplex_pack(O, D, &s4);
     for (auto& h : s4) o += align256(h.frag.size() * sizeof(double)) + align256(h.kmask.size() * sizeof(unsigned) + 4);
@@ -738,6 +739,8 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     }
     g.K = m.K;
     g.Kp = m.K_pad;
+    for (int f = 0; f <= r.nfaces; ++f) g.fptr[f] = (int16_t)r.face_ptr[f];
+    for (int e = 0; e < r.next; ++e) g.xface[e] = (int8_t)r.ext_face[e];
     for (int s = 0; s < m.nsub; ++s) {
       g.detJ[s] = m.detJ[s];
       for (int k = 0; k < 9; ++k) g.Jinv[s][k] = m.Jinv[s][k];
@@ -747,7 +750,7 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         g.nshape[s][f] = (int8_t)L.nshape;
         g.nface[s][f] = (int8_t)L.nface;
         g.left[s][f] = (int8_t)L.left;
-        for (int q = 0; q < r.nfp; ++q) g.perm[s][f][q] = (int8_t)L.perm[q];
+        for (int q = 0; q < (int)L.perm.size(); ++q) g.perm[s][f][q] = (int8_t)L.perm[q];
       }
     }
     g.Kt = m.Kt;
@@ -931,7 +934,7 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     c->d_cub = (double*)(base + p.off_cub);
     c->cub_cap = cub_points(r.etype, r.nd, 10);
     CUDA_OK(cudaStreamSynchronize(st));
-    set_diag_rule(c, r.etype, 10);
+    if (r.etype != PRI) set_diag_rule(c, r.etype, 10);  // diagnostics run on the fused paths (no prisms)
     // interior / boundary tile lists for the overlapped multi-rank stage:
     // a tile is interior if none of its elements lies in a pattern layer next to a
     // partition face (ghost neighbours only occur there)

@@ -22,6 +22,11 @@ static std::vector<std::vector<I3>> subcells(int etype) {
   if (etype == TRI) {
     out.push_back({I3{0, 0, 0}, I3{1, 0, 0}, I3{1, 1, 0}});
     out.push_back({I3{0, 0, 0}, I3{1, 1, 0}, I3{0, 1, 0}});
+  } else if (etype == PRI) {
+    // the triangle split extruded in z: images of the prism's reference vertices
+    // V0 V1 V2 (z = -1) then V3 V4 V5 (z = +1)  (N_p = 2)
+    out.push_back({I3{0, 0, 0}, I3{1, 0, 0}, I3{1, 1, 0}, I3{0, 0, 1}, I3{1, 0, 1}, I3{1, 1, 1}});
+    out.push_back({I3{0, 0, 0}, I3{1, 1, 0}, I3{0, 1, 0}, I3{0, 0, 1}, I3{1, 1, 1}, I3{0, 1, 1}});
   } else if (etype == TET) {
     int perm[3] = {0, 1, 2};
     do {
@@ -140,6 +145,7 @@ Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const doub
     if (etype_tensor(etype)) {
       for (int d = 0; d < D; ++d) { A[d][d] = m.h[d] / 2; Au[d][d] = 0.5; }
     } else {
+      // simplex: columns V_{k+1} - V0; prism: V1 - V0, V2 - V0, V3 - V0 (the same slots)
       for (int k = 0; k < D; ++k)
         for (int c = 0; c < D; ++c) {
           Au[c][k] = (sc[s][k + 1][c] - sc[s][0][c]) / 2.0;
@@ -223,9 +229,9 @@ Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const doub
       } else {
         const std::vector<I3>& P = sc[s];
         const auto& fv = r.face_verts[f];
-        int opp = -1;
-        for (int k = 0; k <= D; ++k)
-          if (std::find(fv.begin(), fv.end(), k) == fv.end()) opp = k;
+        int opp = -1;  // a vertex of the element off this face
+        for (int k = 0; k < (int)P.size(); ++k)
+          if (opp < 0 && std::find(fv.begin(), fv.end(), k) == fv.end()) opp = k;
         if (D == 2) {
           I3 a = P[fv[0]], b = P[fv[1]];
           nrm[0] = b[1] - a[1];
@@ -247,12 +253,14 @@ Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const doub
       for (int c = 0; c < D; ++c)
         if (nrm[c] != 0) { L.left = nrm[c] > 0; break; }
       // face point permutation by coordinate matching (unit cube, tol 1e-9)
-      L.perm.assign(r.nfp, -1);
-      for (int q = 0; q < r.nfp; ++q) {
-        auto x = ext_pos(s, f * r.nfp + q);
+      const int nq = r.face_nfp(f);
+      if (r.face_nfp(L.nface) != nq) throw std::runtime_error("face pairing failed: face sizes differ");
+      L.perm.assign(nq, -1);
+      for (int q = 0; q < nq; ++q) {
+        auto x = ext_pos(s, r.face_ptr[f] + q);
         double best = 1e30;
-        for (int q2 = 0; q2 < r.nfp; ++q2) {
-          auto y = ext_pos(L.nshape, L.nface * r.nfp + q2);
+        for (int q2 = 0; q2 < nq; ++q2) {
+          auto y = ext_pos(L.nshape, r.face_ptr[L.nface] + q2);
           double dist = 0;
           for (int c = 0; c < D; ++c) dist = std::max(dist, std::fabs(y[c] + L.off[c] - x[c]));
           if (dist < best) { best = dist; L.perm[q] = q2; }
@@ -280,13 +288,13 @@ Mesh build_mesh(int etype, int p, const int N[3], const double lo[3], const doub
       }
       nn = std::sqrt(nn);
       for (int i = 0; i < 3; ++i) nown[s * r.nfaces + f][i] = jn[i] / nn;
-      for (int q = 0; q < r.nfp; ++q) m.sscale[s * r.next + f * r.nfp + q] = m.detJ[s] * nn;
+      for (int q = 0; q < r.face_nfp(f); ++q) m.sscale[s * r.next + r.face_ptr[f] + q] = m.detJ[s] * nn;
     }
   for (int s = 0; s < m.nsub; ++s)
     for (int f = 0; f < r.nfaces; ++f) {
       const FaceLink& L = m.link[s * r.nfaces + f];
       auto n = L.left ? nown[s * r.nfaces + f] : nown[L.nshape * r.nfaces + L.nface];
-      for (int q = 0; q < r.nfp; ++q) m.nleft[s * r.next + f * r.nfp + q] = n;
+      for (int q = 0; q < r.face_nfp(f); ++q) m.nleft[s * r.next + r.face_ptr[f] + q] = n;
     }
   build_halo(m, false);
   return m;
@@ -352,8 +360,8 @@ void build_halo(Mesh& m, bool force_self_halo) {
               for (int c = 0; c < D; ++c)
                 if (c != d && L.off[c] != 0) facing = false;
               if (facing)
-                for (int q = 0; q < r.nfp; ++q) {
-                  S.send_row.push_back(f * r.nfp + q);
+                for (int q = 0; q < r.face_nfp(f); ++q) {
+                  S.send_row.push_back(r.face_ptr[f] + q);
                   S.send_col.push_back((int32_t)(lp * m.nsub + s));
                 }
               // the peer's element across MY `side` sends its faces facing -dir;
@@ -362,8 +370,8 @@ void build_halo(Mesh& m, bool force_self_halo) {
               for (int c = 0; c < D; ++c)
                 if (c != d && L.off[c] != 0) facing_back = false;
               if (facing_back)
-                for (int q = 0; q < r.nfp; ++q) {
-                  S.recv_row.push_back(f * r.nfp + q);
+                for (int q = 0; q < r.face_nfp(f); ++q) {
+                  S.recv_row.push_back(r.face_ptr[f] + q);
                   S.recv_col.push_back((int32_t)(m.gbase[d][side] + tang * m.nsub + s));
                 }
             }

@@ -379,16 +379,79 @@ static P3 bary(const std::vector<qd>& lam, const std::vector<P3>& verts) {
 
 static std::array<double, 3> to_d(const P3& x) { return {(double)x[0], (double)x[1], (double)x[2]}; }
 
+// Prism reference vertices (x, y >= -1, x + y <= 0, z in [-1, 1]) and faces:
+// 0 z = -1, 1 z = +1 (triangles), 2 y = -1, 3 x + y = 0, 4 x = -1 (quadrilaterals)
+static const int PRI_F[5][4] = {{0, 1, 2, -1}, {3, 4, 5, -1}, {0, 1, 4, 3}, {1, 2, 5, 4}, {2, 0, 3, 5}};
+
 static RefQ build_ref_q(int etype, int p) {
-  if (p < 1 || p > 4 || (etype == TET && p > 3))
-    throw std::runtime_error("unsupported degree: quad/hex/tri p in [1,4], tet p in [1,3]");
+  if (p < 1 || p > 4 || ((etype == TET || etype == PRI) && p > 3))
+    throw std::runtime_error("unsupported degree: quad/hex/tri p in [1,4], tet/pri p in [1,3]");
   RefQ R;
   RefElement& r = R.r;
   r.etype = etype;
   r.p = p;
   r.nd = etype_dim(etype);
   int D = r.nd;
-  if (etype_tensor(etype)) {
+  if (etype == PRI) {
+    // PAPER.md App. A l.2633-2737: triangle solution points x (p+1) GL levels; the
+    // triangle faces carry the tet-face triangle rule, the quadrilateral faces edge GL x
+    // GL; internal set 1 = triangle interior rule x (p+1) GL levels (normals e_x, e_y),
+    // set 2 = triangle-face rule x the p zeros of P_p (normal e_z).  z slowest.
+    std::vector<qd> g, gw, z, zw;
+    gauss_legendre(p + 1, g, gw);
+    gauss_legendre(p, z, zw);
+    std::vector<P3> V;
+    for (auto& v : TRI_V) V.push_back({(qd)v[0], (qd)v[1], 0});
+    std::vector<P3> tsol, tface, tint;
+    for (auto& lam : centroid_lattice(2, p)) tsol.push_back(bary(lam, V));
+    for (auto& lam : simplex_rule(2, (p + 1) * (p + 2) / 2)) tface.push_back(bary(lam, V));
+    for (auto& lam : simplex_rule(2, p * (p + 1) / 2)) tint.push_back(bary(lam, V));
+    for (auto zz : g)
+      for (auto& x : tsol) R.xsol.push_back({x[0], x[1], zz});
+    const qd s2 = 1 / sqrtq(2.0Q);
+    P3 fn[5] = {{0, 0, -1}, {0, 0, 1}, {0, -1, 0}, {s2, s2, 0}, {-1, 0, 0}};
+    r.nfaces = 5;
+    r.nfp = (p + 1) * (p + 1);
+    r.face_ptr.push_back(0);
+    for (int f = 0; f < 5; ++f) {
+      r.face_normal.push_back(to_d(fn[f]));
+      std::vector<int> fv;
+      for (int k = 0; k < 4; ++k)
+        if (PRI_F[f][k] >= 0) fv.push_back(PRI_F[f][k]);
+      r.face_verts.push_back(fv);
+      if (f < 2) {
+        for (auto& x : tface) {
+          R.xext.push_back({x[0], x[1], f == 0 ? (qd)-1 : (qd)1});
+          R.next_n.push_back(fn[f]);
+          r.ext_face.push_back(f);
+        }
+      } else {
+        const P3 &A = V[TRI_F[f - 2][0]], &B = V[TRI_F[f - 2][1]];
+        for (auto zz : g)
+          for (int t = 0; t <= p; ++t) {
+            qd lam = (g[t] + 1) / 2;
+            R.xext.push_back({A[0] + lam * (B[0] - A[0]), A[1] + lam * (B[1] - A[1]), zz});
+            R.next_n.push_back(fn[f]);
+            r.ext_face.push_back(f);
+          }
+      }
+      r.face_ptr.push_back((int)R.xext.size());
+    }
+    for (auto zz : g)
+      for (auto& x : tint) {
+        for (int d = 0; d < 2; ++d) {
+          r.int_u.push_back((int)R.xu.size());
+          r.int_dir.push_back(d);
+        }
+        R.xu.push_back({x[0], x[1], zz});
+      }
+    for (auto zz : z)
+      for (auto& x : tface) {
+        r.int_u.push_back((int)R.xu.size());
+        r.int_dir.push_back(2);
+        R.xu.push_back({x[0], x[1], zz});
+      }
+  } else if (etype_tensor(etype)) {
     std::vector<qd> g, gw, z, zw;
     gauss_legendre(p + 1, g, gw);
     gauss_legendre(p, z, zw);
@@ -493,6 +556,8 @@ static RefQ build_ref_q(int etype, int p) {
         r.int_dir.push_back(d);
       }
   }
+  if (r.face_ptr.empty())
+    for (int f = 0; f <= r.nfaces; ++f) r.face_ptr.push_back(f * r.nfp);
   r.nsol = (int)R.xsol.size();
   r.next = (int)R.xext.size();
   r.nu = (int)R.xu.size();
@@ -795,22 +860,40 @@ static Operators simplex_operators(int etype, int p) {
   O.ref = R.r;
   const RefElement& r = O.ref;
   int D = r.nd, ns = r.nsol;
-  // RT span: P_p^D (+) xi Pbar_p(xi)  (App. A l.2364; affine invariant)
+  // RT span: simplex P_p^D (+) xi Pbar_p(xi) (App. A l.2364; affine invariant);
+  // prism [P_p(xi0, xi1)^2 (+) (xi0, xi1) Pbar_p(xi0, xi1)] P_p(xi2) x P_p(xi0, xi1) P_{p+1}(xi2)
+  // (l.2640-2642; invariant under the affine x -> xi); solution span P_p (simplex) or
+  // P_p(xi0, xi1) P_p(xi2) (prism, l.2731-2733)
   struct VT { std::vector<std::pair<int, std::vector<int>>> terms; };
   std::vector<VT> span;
   std::vector<std::vector<int>> Ptot, Phom;
-  exps_total(D, p, Ptot);
-  exps_eq(D, p, Phom);
-  for (int c = 0; c < D; ++c)
-    for (auto& e : Ptot) span.push_back({{{c, e}}});
-  for (auto& e : Phom) {
-    VT v;
-    for (int c = 0; c < D; ++c) {
-      auto ee = e;
-      ee[c] += 1;
-      v.terms.push_back({c, ee});
+  if (etype == PRI) {
+    std::vector<std::vector<int>> T2, H2;
+    exps_total(2, p, T2);
+    exps_eq(2, p, H2);
+    for (int c = 0; c <= p; ++c)
+      for (auto& e : T2) Ptot.push_back({e[0], e[1], c});
+    for (int c = 0; c <= p; ++c) {
+      for (int k = 0; k < 2; ++k)
+        for (auto& e : T2) span.push_back({{{k, {e[0], e[1], c}}}});
+      for (auto& e : H2) span.push_back({{{0, {e[0] + 1, e[1], c}}, {1, {e[0], e[1] + 1, c}}}});
     }
-    span.push_back(v);
+    for (int c = 0; c <= p + 1; ++c)
+      for (auto& e : T2) span.push_back({{{2, {e[0], e[1], c}}}});
+  } else {
+    exps_total(D, p, Ptot);
+    exps_eq(D, p, Phom);
+    for (int c = 0; c < D; ++c)
+      for (auto& e : Ptot) span.push_back({{{c, e}}});
+    for (auto& e : Phom) {
+      VT v;
+      for (int c = 0; c < D; ++c) {
+        auto ee = e;
+        ee[c] += 1;
+        v.terms.push_back({c, ee});
+      }
+      span.push_back(v);
+    }
   }
   int nf = (int)span.size();
   if (nf != r.next + r.nint) throw std::runtime_error("RT span dimension mismatch");
@@ -899,25 +982,29 @@ static Operators simplex_operators(int etype, int p) {
         for (int k = 0; k < ns; ++k) v += Y[(size_t)k * ns + rr] * mono_dx(Ptot[k], R.xsol[s], d);
         O.Dsol[d](s, rr) = (double)v;
       }
-  // weights: int over reference simplex of xi^e = 2^D prod e_i! / (|e|+D)!
+  // weights: int over the reference simplex of xi^e = 2^D prod e_i! / (|e|+D)!; prism:
+  // the triangle's 4 e0! e1! / (e0+e1+2)! times int_{-1}^{1} xi2^e2 dz = 2 / (e2 + 1)
   O.w.assign(ns, 0.0);
+  const int DS = etype == PRI ? 2 : D;  // simplex factor dimension
   for (int rr = 0; rr < ns; ++rr) {
     qd v = 0;
     for (int k = 0; k < ns; ++k) {
       const auto& e = Ptot[k];
       qd num = 1;
-      int tot = D;
-      for (int c = 0; c < D; ++c) {
+      int tot = DS;
+      for (int c = 0; c < DS; ++c) {
         for (int m = 2; m <= e[c]; ++m) num *= m;
         tot += e[c];
       }
       qd den = 1;
       for (int m = 2; m <= tot; ++m) den *= m;
-      v += Y[(size_t)k * ns + rr] * num / den * (D == 2 ? 4 : 8);
+      qd val = num / den * (DS == 2 ? 4 : 8);
+      if (etype == PRI) val *= (qd)2 / (e[2] + 1);
+      v += Y[(size_t)k * ns + rr] * val;
     }
     O.w[rr] = (double)v;
   }
-  O.Mc = simplex_dg_lift(R, Y, Ptot);
+  if (etype != PRI) O.Mc = simplex_dg_lift(R, Y, Ptot);
   finish_gradient_ops(O);
   return O;
 }
@@ -927,6 +1014,7 @@ static Operators simplex_operators(int etype, int p) {
 // with degree/2 + 1 points per axis; simplex: collapsed (Duffy) Gauss-Legendre products
 // with (degree + D - 1)/2 + 1 points per direction, mapped affinely (|det| 4 tri, 8 tet).
 void cubature_interp(int etype, int p, int degree, std::vector<double>& w, Mat& B) {
+  if (etype == PRI) throw std::runtime_error("unsupported: diagnostics cubature on prisms");
   RefQ R = build_ref_q(etype, p);
   const RefElement& r = R.r;
   const int D = r.nd, ns = r.nsol;
@@ -990,9 +1078,10 @@ void cubature_interp(int etype, int p, int degree, std::vector<double>& w, Mat& 
 Operators build_operators(int etype, int p, int scheme) {
   Operators O;
   if (etype_tensor(etype)) O = tensor_operators(etype, p);
-  else if (etype == TRI || etype == TET) O = simplex_operators(etype, p);
+  else if (etype == TRI || etype == TET || etype == PRI) O = simplex_operators(etype, p);
   else throw std::runtime_error("unknown element type");
   if (scheme < 0 || scheme > 2) throw std::runtime_error("unsupported scheme");
+  if (etype == PRI && scheme != 0) throw std::runtime_error("unsupported: FR schemes on prisms");
   O.scheme = scheme;
   if (scheme == 1) O.Mc = O.M14;  // FR-SDRT: div g_nu = div psi_nu (l.407-413)
   return O;

@@ -7,10 +7,10 @@
 
 namespace sdrt {
 
-enum EType { QUAD = 0, TRI = 1, HEX = 2, TET = 3 };
+enum EType { QUAD = 0, TRI = 1, HEX = 2, TET = 3, PRI = 4 };
 
 inline int etype_dim(int et) { return (et == QUAD || et == TRI) ? 2 : 3; }
-inline int etype_nsub(int et) { return et == TRI ? 2 : (et == TET ? 6 : 1); }
+inline int etype_nsub(int et) { return (et == TRI || et == PRI) ? 2 : (et == TET ? 6 : 1); }
 inline bool etype_tensor(int et) { return et == QUAD || et == HEX; }
 
 // Dense row-major double matrix.
@@ -31,7 +31,9 @@ struct RefElement {
   std::vector<int> ext_face;                            // face id per ext point
   std::vector<int> int_u, int_dir;                      // per internal point
   std::vector<std::array<double, 3>> face_normal;       // per face
-  std::vector<std::vector<int>> face_verts;             // reference vertex ids per face (simplex)
+  std::vector<std::vector<int>> face_verts;             // reference vertex ids per face (simplex, prism)
+  std::vector<int> face_ptr;                            // face f: ext points face_ptr[f] .. face_ptr[f+1]
+  int face_nfp(int f) const { return face_ptr[f + 1] - face_ptr[f]; }
 };
 
 struct Operators {

@@ -19,7 +19,7 @@ if not os.path.exists(_LIBPATH):
                       "python paper_2105_08632_b200/build.py")
 lib = ctypes.CDLL(_LIBPATH)
 
-ETYPES = {"quad": 0, "tri": 1, "hex": 2, "tet": 3}
+ETYPES = {"quad": 0, "tri": 1, "hex": 2, "tet": 3, "pri": 4}
 EQS = {"linadv": 0, "linadvdiff": 1, "euler": 2, "ns": 3}
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "UNSUPPORTED", -3: "ILL_CONDITIONED", -4: "CUDA",
           -5: "NCCL", -6: "WORKSPACE", -7: "DIVERGED", -8: "INTERNAL"}

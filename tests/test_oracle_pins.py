@@ -24,8 +24,8 @@ from oracle import vonneumann as VN
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_tables.json")))
 ELEMS = [("quad", p) for p in range(1, 5)] + [("tri", p) for p in range(1, 5)] + \
-        [("hex", p) for p in range(1, 5)] + [("tet", p) for p in range(1, 4)]
-ND = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}
+        [("hex", p) for p in range(1, 5)] + [("tet", p) for p in range(1, 4)] + [("pri", p) for p in range(1, 4)]
+ND = {"quad": 2, "tri": 2, "hex": 3, "tet": 3, "pri": 3}
 
 
 def _eval_count(expr, p):
@@ -192,7 +192,19 @@ def _random_rt_field(etype, p, rng):
     """Random member of the RT space as written in App. A (l.2364, 2475, 2479)."""
     D = ND[etype]
     terms = []
-    if etype in ("tri", "tet"):
+    if etype == "pri":  # l.2640-2642, restated: [P_p^2 (+) (x,y) P~_p](x,y) P_p(z) x P_p(x,y) P_{p+1}(z)
+        tri = [e for e in itertools.product(range(p + 1), repeat=2) if sum(e) <= p]
+        for c in range(p + 1):
+            for k in range(2):
+                for (a, b) in tri:
+                    terms.append((rng.normal(), [(k, (a, b, c))]))
+            for (a, b) in tri:
+                if a + b == p:
+                    terms.append((rng.normal(), [(0, (a + 1, b, c)), (1, (a, b + 1, c))]))
+        for c in range(p + 2):
+            for (a, b) in tri:
+                terms.append((rng.normal(), [(2, (a, b, c))]))
+    elif etype in ("tri", "tet"):
         for c in range(D):
             for e in itertools.product(range(p + 1), repeat=D):
                 if sum(e) <= p:
@@ -259,7 +271,7 @@ def test_gradient_and_interpolation_exactness(etype, p):
     assert np.allclose(q, ex, atol=1e-10 * max(1, np.abs(ex).max()))
     # integral weights: sum w = |ref|, w^T M13 = 0 (internal RT functions carry no
     # boundary flux: divergence theorem)
-    vol = {"quad": 4.0, "hex": 8.0, "tri": 2.0, "tet": 4.0 / 3.0}[etype]
+    vol = {"quad": 4.0, "hex": 8.0, "tri": 2.0, "tet": 4.0 / 3.0, "pri": 4.0}[etype]
     assert abs(o.w.sum() - vol) < 1e-13
     assert np.abs(o.w @ o.M13).max() < 1e-11
 
@@ -341,7 +353,8 @@ def _random_state(ph, nsol, K, rng):
     return U
 
 
-@pytest.mark.parametrize("etype,p", [("quad", 2), ("tri", 3), ("hex", 2), ("tet", 2), ("tet", 3)])
+@pytest.mark.parametrize("etype,p", [("quad", 2), ("tri", 3), ("hex", 2), ("tet", 2), ("tet", 3), ("pri", 2),
+                                     ("pri", 3)])
 @pytest.mark.parametrize("eq", ["linadv", "linadvdiff", "euler", "ns"])
 def test_freestream_and_conservation(etype, p, eq):
     """Free-stream preservation on uniform affine meshes (l.170-172) and discrete
@@ -374,7 +387,8 @@ def test_linearity():
 
 
 @pytest.mark.parametrize("etype,p,N", [("quad", 1, 4), ("quad", 3, 4), ("tri", 1, 4), ("tri", 3, 4),
-                                       ("tri", 4, 3), ("hex", 1, 3), ("hex", 2, 3), ("tet", 1, 3), ("tet", 2, 3)])
+                                       ("tri", 4, 3), ("hex", 1, 3), ("hex", 2, 3), ("tet", 1, 3), ("tet", 2, 3),
+                                       ("pri", 1, 3), ("pri", 2, 3)])
 def test_spatial_stability(etype, p, N):
     """SDRT is linearly stable for p <= 4 on these elements (l.1192-1198): max Re
     lambda of the periodic upwind advection operator <= 1e-12 (c/h units)."""

@@ -22,10 +22,12 @@ from oracle.physics import Physics
 from oracle.points import reference_element
 from oracle.residual import Residual
 
-ND = {"quad": 2, "tri": 2, "hex": 3, "tet": 3}
+ND = {"quad": 2, "tri": 2, "hex": 3, "tet": 3, "pri": 3}
 
 
 def _sol_exps(etype, p, D):
+    if etype == "pri":
+        return [(a, b, c) for c in range(p + 1) for a in range(p + 1) for b in range(p + 1 - a)]
     if etype in ("tri", "tet"):
         return [e for e in itertools.product(range(p + 1), repeat=D) if sum(e) <= p]
     return list(itertools.product(range(p + 1), repeat=D))
@@ -34,6 +36,13 @@ def _sol_exps(etype, p, D):
 def _rt_basis(etype, p, D):
     """RT span of App. A (l.2364, 2475-2479) as lists of (component, exponent)."""
     out = []
+    if etype == "pri":  # l.2640-2642
+        tri = [e for e in itertools.product(range(p + 1), repeat=2) if sum(e) <= p]
+        for c in range(p + 1):
+            out += [[(k, (a, b, c))] for k in range(2) for (a, b) in tri]
+            out += [[(0, (a + 1, b, c)), (1, (a, b + 1, c))] for (a, b) in tri if a + b == p]
+        out += [[(2, (a, b, c))] for c in range(p + 2) for (a, b) in tri]
+        return out
     if etype in ("tri", "tet"):
         tot = [e for e in itertools.product(range(p + 1), repeat=D) if sum(e) <= p]
         for c in range(D):
@@ -181,7 +190,7 @@ def _state(ph, nsol, K, rng):
     return U
 
 
-CASES = [(e, p) for e in ("quad", "tri", "hex", "tet") for p in (1, 2, 3)]
+CASES = [(e, p) for e in ("quad", "tri", "hex", "tet", "pri") for p in (1, 2, 3)]
 
 
 @pytest.mark.parametrize("etype,p", CASES)
@@ -294,7 +303,7 @@ def test_isentropic_vortex_design_order(etype, p):
 
 
 # ----------------------------------------------------------------- far-field boundaries
-@pytest.mark.parametrize("etype,p", [("quad", 2), ("tri", 3), ("hex", 2), ("tet", 2)])
+@pytest.mark.parametrize("etype,p", [("quad", 2), ("tri", 3), ("hex", 2), ("tet", 2), ("pri", 2)])
 @pytest.mark.parametrize("eq", ["linadvdiff", "euler", "ns"])
 def test_farfield_twin_and_freestream(etype, p, eq):
     """Far-field boundaries (NEXT row N4): x-boundaries take a constant
