@@ -38,7 +38,7 @@ from sdrt_inputs import CONFIGS, initial_state  # noqa: E402
 
 METRIC = "SDRT residual GDOF-stage/s (fp64) and % of HBM roofline at 1/2/4/8 B200"  # BASELINE.json
 # reference-arm sample size (patterns per axis) so K steps of the oracle take ~1 s each
-REF_SUBBOX = {"c1": 8, "c2": 40, "c3": 6, "c4": 8, "c5": 4}
+REF_SUBBOX = {"c1": 8, "c2": 40, "c3": 6, "c4": 8, "c5": 4, "c4pri": 6}
 UNIT = "GDOF-stage/s"
 WORKLOADS = {
     "c1": "c1: 2D linear advection, quad p=2, 8^2 periodic",
@@ -46,6 +46,7 @@ WORKLOADS = {
     "c3": "c3: 3D linear advection-diffusion, hex p=4, 24^3",
     "c4": "c4: 3D Taylor-Green vortex NS, hex p=3, 32^3 (Re=1600, Ma=0.1)",
     "c5": "c5: 3D Taylor-Green vortex NS, tet p=3, 48^3x6",
+    "c4pri": "c4 on prisms (NEXT row N3): TGV NS, prism p=3, 32^3x2, generic operator path",
 }
 
 
@@ -65,6 +66,8 @@ def dims(cfg):
         ns, ne, nu = (p + 1) ** 3, 6 * (p + 1) ** 2, 3 * p * (p + 1) ** 2
     elif cfg.etype == "tri":
         ns, ne, nu = (p + 1) * (p + 2) // 2, 3 * (p + 1), p * (p + 1) // 2
+    elif cfg.etype == "pri":  # Tables A.3/A.4
+        ns, ne, nu = (p + 1) ** 2 * (p + 2) // 2, (p + 1) * (4 * p + 5), p * (p + 1) * (2 * p + 3) // 2
     else:
         ns, ne, nu = (p + 1) * (p + 2) * (p + 3) // 6, 2 * (p + 1) * (p + 2), p * (p + 1) * (p + 2) // 6
     return D, ns, ne, nu

@@ -40,7 +40,7 @@ class Config:
 
     @property
     def nsub(self):
-        return {"quad": 1, "hex": 1, "tri": 2, "tet": 6}[self.etype]
+        return {"quad": 1, "hex": 1, "tri": 2, "tet": 6, "pri": 2}[self.etype]
 
     @property
     def K(self):
@@ -82,6 +82,11 @@ CONFIGS = {
     "c5": Config("c5", "tet", 3, 48, (0.0,) * 3, (2 * math.pi,) * 3, "ns", mu=1.0 / TGV_RE, gamma=1.4,
                  Pr=0.71, beta=0.5, eta=0.1, dt=0.035 * _H5 / 11.0, steps=200, ic="tgv", nd=3),
 }
+
+# c4 on triangular prisms (NEXT row N3; PAPER.md's performance table covers prisms,
+# l.2982-2995): same TGV, mesh 32^3 hexahedra x 2 prisms, p=3, c4's dt (a bench workload,
+# not a BASELINE.json config)
+CONFIGS["c4pri"] = replace(CONFIGS["c4"], name="c4pri", etype="pri")
 
 # c2 dt literal: 0.1 * 0.25 / lambda_max, lambda_max = max(|v| + a) over the initial
 # solution points (written by tools/derive_dt.py, which calls only oracle/)

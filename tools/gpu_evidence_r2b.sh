@@ -1,0 +1,23 @@
+#!/bin/bash
+# Round-2 evidence (final code): GPU tests, smoke, bench lines for every config (+ the
+# prism workload and the paper's RK54 protocol on c4), the ncu launch list of the default
+# bench command, ncu --set full captures of the two kernels of c4 and c5, DMMA counters.
+O=gpurun_out/r2_fin; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err
+for c in c1 c2 c3 c5 c4pri; do
+  timeout 600 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err
+done
+timeout 600 python bench.py --config c4 --integrator rk54 --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_c4_rk54.json 2> $O/bench_c4_rk54.err
+cmd="python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline"
+$cmd > $O/plain_c4.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c4.csv $cmd > $O/ncu_launch.log 2>&1
+for c in c4 c5; do
+  case $c in c4) ks="kt_grad kt_stage";; *) ks="ks_grad ks_stage";; esac
+  cmd="python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline"
+  for k in $ks; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 8 -c 1 -o $O/prof_${c}_$k -f $cmd > $O/ncu_${c}_$k.log 2>&1
+  done
+done
+M=gpu__time_duration.sum,sm__inst_executed_pipe_tensor_subpipe_dmma.sum,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum
+timeout 900 ncu --metrics $M --clock-control none -k regex:"ks_" -s 6 -c 4 --csv --log-file $O/dmma_c5.csv python bench.py --config c5 --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_dmma.log 2>&1
