@@ -161,7 +161,7 @@ def tet_ops(p, face_pts, int_pts):
     return Operators("tet", p, D, nsol, next_, nint, len(xu), 4, len(face_pts),
                      lag(xext), lag(xu), M13, M14, M15, M16, P, M19P2, Cu @ ints,
                      np.array(nrm), np.array(fid), np.array(xsol), np.array(xext), np.array(xu),
-                     float(np.linalg.cond(Vf, 1)), np.array(fn))
+                     float(np.linalg.cond(Vf, 1)), np.array(fn), tuple(f * len(face_pts) for f in range(5)))
 
 
 def patch(ops):
