@@ -616,9 +616,9 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   // far-field ghost entries (row, col) int32 + the far-field state
   p.off_ff = o;
   o += align256(m.ff_row.size() * 2 * sizeof(int32_t)) + 256;
-  // interior / boundary tile lists of the fused paths (tiles of >= 8 elements)
+  // interior / boundary tile lists of the fused paths (tiles of >= 4 elements)
   p.off_tiles = o;
-  o += align256(((size_t)m.K / 8 + 2) * sizeof(int32_t));
+  o += align256(((size_t)m.K / 4 + 2) * sizeof(int32_t));
   // TGV diagnostics: per-tile partial sums (3 per tile of >= 8 elements) + weights w
   p.off_diag = o;
   o += align256((3 * ((size_t)m.K / 8 + 2) + r.nsol + 8) * sizeof(double));

@@ -107,6 +107,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SPLIT_INTFLUX
 #define SDRT_SPLIT_INTFLUX 0
 #endif
+#ifndef SDRT_S_E2D
+#define SDRT_S_E2D 4
+#endif
 __host__ __device__ constexpr int ngroup(int n) {
   return SDRT_NGR_MODE == 1   ? (n % 3 == 0 && n > 5 ? 3 : (n % 2 == 0 && n > 5 ? 2 : 1))
          : SDRT_NGR_MODE == 2 ? (n <= 15 ? n : (n % 5 == 0 ? 5 : 1))
@@ -994,7 +997,9 @@ template <int D, int P, int EQ>
 struct SCfg {
   static constexpr int NV = Phys<EQ, D>::NV;
   static constexpr bool VISC = Phys<EQ, D>::VISC;
-  static constexpr int E = 8;  // tile width: MMA rows hold NV E (a multiple of 8) columns
+  // tile width: MMA rows hold NV E (a multiple of 8) columns; 2-D systems (N_V = 4) may
+  // take 4-element tiles (SDRT_S_E2D): twice the CTAs for the small latency-bound meshes
+  static constexpr int E = (D == 2 && (NV * SDRT_S_E2D) % 8 == 0) ? SDRT_S_E2D : 8;
   static constexpr int THREADS = 256;
   static constexpr size_t SMEM_A = (size_t)SLayoutA<D, P, NV>::TOTAL * E * sizeof(double);
   static constexpr size_t SMEM_B = (size_t)SLayoutB<D, P, NV, !VISC>::TOTAL * E * sizeof(double);
@@ -1095,8 +1100,9 @@ static SFn spick(int D, int P, int eq, STmaFn* m) {
 }
 
 int simplex_tile_width(int D, int P, int eq) {
-  (void)D; (void)P; (void)eq;
-  return 8;  // SCfg<...>::E for every instantiation
+  (void)P;
+  const int nv = (eq == EQ_LINADV || eq == EQ_LINADVDIFF) ? 1 : D + 2;
+  return (D == 2 && (nv * SDRT_S_E2D) % 8 == 0) ? SDRT_S_E2D : 8;  // SCfg<...>::E
 }
 
 void simplex_launch_diag(int D, int P, const GeomDev& g, const SimplexOps& O, const PhysDev& ph, SimplexTma* tma,
