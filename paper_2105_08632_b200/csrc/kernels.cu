@@ -844,6 +844,13 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         t.gbase[d][1] = m.gbase[d][1];
       }
       t.detJ = m.detJ[0];
+      {
+        // one-sided flux publication (tensor.cu publish_F): NS with beta = +1/2 (the
+        // left element holds every input of a face's common flux) on meshes without
+        // far-field ghosts (a ghost is never a kernel-A element); SDRT_OSF=0 disables it
+        const char* ev = std::getenv("SDRT_OSF");
+        t.osf = ph->eq == EQ_NS && ph->beta == 0.5 && m.ff_row.empty() && !(ev && ev[0] == '0');
+      }
       for (int d = 0; d < 3; ++d) {
         t.jinv[d] = d < m.nd ? m.Jinv[0][d * 3 + d] : 0.0;
         t.sface[d] = d < m.nd ? m.detJ[0] * t.jinv[d] : 0.0;

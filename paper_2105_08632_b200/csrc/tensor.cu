@@ -205,26 +205,29 @@ struct GradNb {
   static constexpr int CI = (ITEMS + THREADS - 1) / THREADS;
   double nb[CI][2];
 
-  __device__ __forceinline__ void load(const TensorGeom& g, const double* __restrict__ Tu, const int (*sNb)[E],
-                                       int64_t e0) {
+  __device__ __forceinline__ void load(const TensorGeom& g, const PhysDev& ph, const double* __restrict__ Tu,
+                                       const int (*sNb)[E], int64_t e0) {
     constexpr int NL = T::NL;
     const int Kt = (int)g.Kt;
+    const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
     for (int k = 0; k < CI; ++k) {
       const int item = threadIdx.x + k * THREADS;
       nb[k][0] = nb[k][1] = 0.0;
       if (item < ITEMS) {
         const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
-        if (e0 + el < g.K) {
-          nb[k][0] = Tu[(((2 * d + 1) * NL + t) * NV + v) * Kt + sNb[2 * d][el]];
-          nb[k][1] = Tu[(((2 * d + 0) * NL + t) * NV + v) * Kt + sNb[2 * d + 1][el]];
+        if (e0 + el < g.K) {  // a neighbour whose LDG weight is 0 is not read (may be stale)
+          if (wl != 0.0) nb[k][0] = Tu[(((2 * d + 1) * NL + t) * NV + v) * Kt + sNb[2 * d][el]];
+          if (wr != 0.0) nb[k][1] = Tu[(((2 * d + 0) * NL + t) * NV + v) * Kt + sNb[2 * d + 1][el]];
         }
       }
     }
   }
 
+  // sNbR (OSF): the right neighbours' traces nb[.][1] are also stored to sNbR[d][t][v][el]
+  // for publish_F (the same (d, t, v, el) entries)
   __device__ __forceinline__ void compute(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
-                                          double* sQ, int64_t e0) const {
+                                          double* sQ, int64_t e0, double* sNbR = nullptr) const {
     constexpr int n = T::n, NL = T::NL, NS = T::NS;
     const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
@@ -233,14 +236,16 @@ struct GradNb {
       if (item >= ITEMS) break;
       const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
       if (e0 + el >= g.K) continue;
+      if (sNbR) sNbR[item] = nb[k][1];
       const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
       double u[n];
 #pragma unroll
       for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
       // common values at both ends (own trace recomputed bit-identically, neighbour read)
       const double own0 = interp_end<n>(L.Iend[0], u), own1 = interp_end<n>(L.Iend[1], u);
-      const double c0 = wl * nb[k][0] + wr * own0;  // face x_d = -1: this element is RIGHT
-      const double c1 = wl * own1 + wr * nb[k][1];  // face x_d = +1: this element is LEFT
+      // face x_d = -1: this element is RIGHT; face x_d = +1: this element is LEFT
+      const double c0 = wl != 0.0 ? wl * nb[k][0] + wr * own0 : own0;
+      const double c1 = wr != 0.0 ? wl * own1 + wr * nb[k][1] : own1;
       double ui[NI];
 #pragma unroll
       for (int a = 0; a < NI; ++a) {
@@ -277,10 +282,11 @@ struct GradNb2 {
   static constexpr int CI = (ITEMS + THREADS - 1) / THREADS;
   double nb[CI][2][2];  // [item][element of the pair][face side]
 
-  __device__ __forceinline__ void load(const TensorGeom& g, const double* __restrict__ Tu, const int (*sNb)[E],
-                                       int64_t e0) {
+  __device__ __forceinline__ void load(const TensorGeom& g, const PhysDev& ph, const double* __restrict__ Tu,
+                                       const int (*sNb)[E], int64_t e0) {
     constexpr int NL = T::NL;
     const int Kt = (int)g.Kt;
+    const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
     for (int k = 0; k < CI; ++k) {
       const int item = threadIdx.x + k * THREADS;
@@ -291,15 +297,15 @@ struct GradNb2 {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
           if (e0 + el0 + h < g.K) {
-            nb[k][h][0] = Tu[(((2 * d + 1) * NL + t) * NV + v) * Kt + sNb[2 * d][el0 + h]];
-            nb[k][h][1] = Tu[(((2 * d + 0) * NL + t) * NV + v) * Kt + sNb[2 * d + 1][el0 + h]];
+            if (wl != 0.0) nb[k][h][0] = Tu[(((2 * d + 1) * NL + t) * NV + v) * Kt + sNb[2 * d][el0 + h]];
+            if (wr != 0.0) nb[k][h][1] = Tu[(((2 * d + 0) * NL + t) * NV + v) * Kt + sNb[2 * d + 1][el0 + h]];
           }
       }
     }
   }
 
   __device__ __forceinline__ void compute(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
-                                          double* sQ, int64_t e0) const {
+                                          double* sQ, int64_t e0, double* = nullptr) const {
     constexpr int n = T::n, NL = T::NL, NS = T::NS;
     const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
@@ -320,8 +326,8 @@ struct GradNb2 {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double own0 = interp_end<n>(L.Iend[0], u[h]), own1 = interp_end<n>(L.Iend[1], u[h]);
-        const double c0 = wl * nb[k][h][0] + wr * own0;
-        const double c1 = wl * own1 + wr * nb[k][h][1];
+        const double c0 = wl != 0.0 ? wl * nb[k][h][0] + wr * own0 : own0;
+        const double c1 = wr != 0.0 ? wl * own1 + wr * nb[k][h][1] : own1;
         double ui[NI];
 #pragma unroll
         for (int a = 0; a < NI; ++a) {
@@ -390,8 +396,10 @@ __global__ void __launch_bounds__(256) kt_traces(TensorGeom g, Line1D L, const _
 }
 
 // kernel A keeps two internal-flux buffers when both fit two CTAs per SM
-__host__ __device__ constexpr bool tensor_a_dbuf(int D, int NS, int NL, int NV, int E, int NI) {
-  return (size_t)(NS * NV * E * (1 + D) + 2 * NL * NI * NV * E) * sizeof(double) <= 112 * 1024;
+// (OSF adds the [D][NL][NV][E] face buffer; two CTAs of <= 112.9 KB fit per SM)
+__host__ __device__ constexpr bool tensor_a_dbuf(int D, int NS, int NL, int NV, int E, int NI, bool osf = false) {
+  return (size_t)(NS * NV * E * (1 + D) + 2 * NL * NI * NV * E + (osf ? D * NL * NV * E : 0)) * sizeof(double) <=
+         112 * 1024;
 }
 
 // Kernel A phase helpers -----------------------------------------------------------
@@ -426,6 +434,63 @@ __device__ __forceinline__ void publish_g(const TensorGeom& g, const Line1D& L, 
   Ph::template visc_axis<d>(ph, u, q, 1.0, gv);  // canonical (left) normal +e_d
 #pragma unroll
   for (int v = 0; v < NV; ++v) Tg[((int64_t)ext * NV + v) * g.Kt + e] = gv[v];
+}
+
+// One-sided flux publication (OSF; beta = +1/2, the TGV settings of c4/c5, O15): with
+// LDG weights (1/2 + b, 1/2 - b) = (1, 0) the common viscous flux of a face is the LEFT
+// element's g alone (l.330-335), and the common value is the RIGHT element's trace
+// (l.282-291), so the left element holds every input of the face's whole common flux
+// F = Rusanov(u_L, u_R) + g_L + eta (u_L - u_R) (l.312-340) once it has its gradient:
+// kernel A evaluates F ONCE per face at its x_d = +1 ends (this element LEFT; u_R = the
+// right neighbour's published trace), publishes it in the g slot of T_g, and adds the
+// face's M14 term to R_int; kernel B only reads the left neighbours' F for its x_d = -1
+// faces.  Both sides apply the same stored number: D~_R = -D~_L bitwise (O28).
+template <int D, int P, int EQ, int E, int d>
+// sP [NL][NV][E] of direction d: on entry the right neighbours' x_d = -1 traces (stored by
+// GradNb), on exit sface F (read by the divergence of direction d)
+__device__ __forceinline__ void publish_F(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                          const double* sQ, const TensorBufs& b, double* sP, int64_t e0, int t,
+                                          int el) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
+  const int64_t e = e0 + el;
+  if (e >= g.K) return;
+  const int ext = (2 * d + 1) * NL + t;  // own x_d = +1 end
+  double uR[NV];  // the right neighbour's x_d = -1 trace
+#pragma unroll
+  for (int v = 0; v < NV; ++v) uR[v] = sP[(t * NV + v) * E + el];
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  double u[NV], q[D * NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double ul[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) ul[i] = sU[((lb + i * ls) * NV + v) * E + el];
+    u[v] = interp_end<n>(L.Iend[1], ul);
+#pragma unroll
+    for (int dd = 0; dd < D; ++dd) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) s = fma(L.Iend[1][i], sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el], s);
+      q[dd * NV + v] = s;
+    }
+  }
+  double gv[NV], F[NV];
+  Ph::template visc_axis<d>(ph, u, q, 1.0, gv);  // canonical (left) normal +e_d
+  Ph::template conv_common_axis<d>(ph, u, uR, F);
+  const double wl = 0.5 + ph.beta;  // = 1
+  const double sface = g.sface[d];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    F[v] = Ph::ldg_rn(F[v], __dmul_rn(wl, gv[v]), ph.eta, u[v], uR[v]);
+    b.Tg[((int64_t)ext * NV + v) * g.Kt + e] = F[v];
+    sP[(t * NV + v) * E + el] = sface * F[v];
+  }
+  if (b.Fexp) {  // O28 export (residual only): F at the own ext point
+#pragma unroll
+    for (int v = 0; v < NV; ++v) b.Fexp[((int64_t)ext * NV + v) * g.Kp + e] = F[v];
+  }
 }
 
 // internal transformed flux F~ = detJ (J^-1 (f^c - f^v))_d at internal point a of d-line t
@@ -706,7 +771,7 @@ __device__ __forceinline__ void visc_line_dmma(const TensorGeom& g, const Line1D
 // Phases after the gradient: [publish g + F_v(d=0)] [div(0) + F_v(1)] [div(1) + F_v(2)]
 // [div(2)], with the internal-flux buffer double-buffered so each phase has work for
 // every thread.
-template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI, bool OSF = false>
 __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
                                                     const __grid_constant__ TileMaps tm) {
   pdl_wait();
@@ -715,11 +780,13 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, NL = T::NL, NS = T::NS;
   constexpr int NFB = NL * NI * NV * E;  // one internal-flux buffer
-  constexpr bool DBUF = tensor_a_dbuf(D, NS, NL, NV, E, NI);
+  constexpr bool DBUF = tensor_a_dbuf(D, NS, NL, NV, E, NI, OSF);
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;
   double* sQ = smem + NS * NV * E;
   double* sF = sQ + D * NS * NV * E;  // 2 x [NL][P][NV][E]
+  // OSF: [D][NL][NV][E], the right neighbours' traces, then sface F at the x_d = +1 ends
+  double* sP = sF + (DBUF ? 2 : 1) * NFB;
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar;
   const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
@@ -735,11 +802,11 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   {
     constexpr bool GPAIR = SDRT_TA_GPAIR == 1 || (SDRT_TA_GPAIR == 2 && Ph::NV == 1);
     std::conditional_t<GPAIR, GradNb2<D, P, EQ, E, NT, NI>, GradNb<D, P, EQ, E, NT, NI>> gn;
-    gn.load(g, b.Tu, sNb, e0);
+    gn.load(g, ph, b.Tu, sNb, e0);
     mbar_wait(&bar, 0);
     __syncthreads();
   PH(0, 1)
-    gn.compute(g, L, ph, sU, sQ, e0);
+    gn.compute(g, L, ph, sU, sQ, e0, OSF ? sP : nullptr);
   }
   __syncthreads();
   PH(0, 2)
@@ -747,7 +814,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   // side 0 (right) if 1/2 - beta != 0
   const bool pub1 = (0.5 + ph.beta) != 0.0, pub0 = (0.5 - ph.beta) != 0.0;
   const int nsides = (pub0 ? 1 : 0) + (pub1 ? 1 : 0);
-  const int npub = D * nsides * NL * E;
+  const int npub = nsides * NL * E;  // published ends per direction (in that direction's phase)
   constexpr int NFI = NL * NI * E;   // internal-flux items per direction
   constexpr int NDI = NL * NV * E;  // divergence items per direction
 #pragma unroll 1
@@ -787,7 +854,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
       }
     }
     constexpr bool LDMMA = SDRT_TA_DMMA != 0 && E == 8 && Ph::VISC && NV > 1;
-    const int nA = (ph_ == 0 && !LDMMA && !LINE) ? npub : 0;
+    static_assert(!OSF || (!LDMMA && !LINE), "OSF runs on the per-point kernel-A items");
+    const int nA = (ph_ < D && !LDMMA && !LINE) ? npub : 0;
     constexpr bool PAIR = SDRT_TA_PAIR == 1 || (SDRT_TA_PAIR == 2 && NV == 1);
     const int nB = (ph_ < D && !LDMMA && !LINE) ? (PAIR ? NFI / 2 : NFI) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
@@ -804,6 +872,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         double f[NI];
 #pragma unroll
         for (int a = 0; a < NI; ++a) f[a] = f0[((t * NI + a) * NV + v) * E + el];
+        double fp = 0.0;  // OSF: the x_d = +1 face term (M14) joins R_int
+        if constexpr (OSF) fp = sP[((dd * NL + t) * NV + v) * E + el];
         double* dst = b.Rv + (int64_t)(lb * NV + v) * g.Kp + e0 + el;
 #pragma unroll
         for (int i = 0; i <= P; ++i) {
@@ -815,6 +885,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
           }
 #pragma unroll
           for (int a = 0; a < NI; ++a) acc = fma(L.Dfl[i][a + 1], f[a], acc);
+          if constexpr (OSF) acc = fma(L.Dfl[i][NI + 1], fp, acc);
           dst[(int64_t)i * ls * NV * g.Kp] = acc;
         }
       }
@@ -855,13 +926,20 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
       }
     }
     for (int item = threadIdx.x; item < nA + nB; item += blockDim.x) {
-      if (item < nA) {
+      if (item < nA) {  // published ends of direction ph_
         const int el = item % E, r = item / E;
-        const int t = r % NL, r2 = r / NL, k = r2 % nsides, d = r2 / nsides;
+        const int t = r % NL, k = r / NL;
         const int side = (nsides == 2) ? k : (pub1 ? 1 : 0);
-        if (d == 0) publish_g<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
-        else if (d == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
-        else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+        if constexpr (OSF) {
+          double* p1 = sP + ph_ * NL * NV * E;
+          if (ph_ == 0) publish_F<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b, p1, e0, t, el);
+          else if (ph_ == 1) publish_F<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b, p1, e0, t, el);
+          else if constexpr (D == 3) publish_F<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b, p1, e0, t, el);
+        } else {
+          if (ph_ == 0) publish_g<D, P, EQ, E, 0>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+          else if (ph_ == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+          else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
+        }
       } else if constexpr (PAIR) {
         constexpr int E2 = E / 2;
         const int i2 = item - nA, el = 2 * (i2 % E2), r = i2 / E2, a = r % NI, t = r / NI;
@@ -1138,6 +1216,142 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   PH(1, 15)
 }
 
+// Kernel B with one-sided flux publication (OSF, see publish_F): R_int already holds the
+// internal fluxes and the x_d = +1 faces (kernel A), so per tile this kernel gathers
+// the left neighbours' published F of its D x_d = -1 faces, completes
+// R~ = R_int + sum_d M14_(d,-) D~ in the RK update (l.2919-2925, l.347-350), and publishes
+// the x_d = -1 traces of the new state (the only traces kernel A reads with beta = 1/2).
+// The stage input is not read except where the RK formula needs it (RK4 stage 0, RK54).
+template <int D, int P, int EQ, int E, int NT, int MINB, bool FEXP = false>
+__global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
+                                                       double dt, const __grid_constant__ TileMaps tm) {
+  pdl_wait();
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
+  extern __shared__ __align__(128) double smem[];
+  const bool need_in = stage == 0 || stage >= RK54_STAGE0;
+  double* sR = smem;                    // R_int (kernel A)
+  double* sF = sR + NS * NV * E;        // [D][NL][NV][E] left neighbours' F at the x_d = -1 faces
+  double* sU = sF + D * NL * NV * E;    // new state (stage input first where the RK formula reads it)
+  double* sAcc = sU + NS * NV * E;
+  double* sUn = sAcc + (stage_reads_acc(stage) ? NS * NV * E : 0);
+  __shared__ int sNb[2 * D][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  constexpr unsigned TB = NS * NV * E * 8;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    const unsigned bytes = TB * (1 + (need_in ? 1 : 0) + (stage_reads_un(stage) ? 1 : 0) + (stage_reads_acc(stage) ? 1 : 0));
+    mbar_expect_tx(&bar, bytes);
+    tma_tile<NS * NV, E>(sR, &tm.rv, e0, &bar);
+    if (need_in) tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar);
+    if (stage_reads_un(stage)) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar);
+    if (stage_reads_acc(stage)) tma_tile<NS * NV, E>(sAcc, &tm.acc, e0, &bar);
+  }
+  fill_nbrs<D, E>(g, sNb, e0);
+  __syncthreads();
+  // gather F of the x_d = -1 faces: the left neighbour's x_d = +1 ext point, 8-byte
+  // cp.async straight into shared memory (element fastest: runs of consecutive columns)
+  for (int item = threadIdx.x; item < D * NL * NV * E; item += NT) {
+    const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
+    const int64_t m = e0 + el < g.K ? sNb[2 * d][el] : 0;
+    const double* src = b.Tg + ((int64_t)((2 * d + 1) * NL + t) * NV + v) * g.Kt + m;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sF + item);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src));
+  }
+  asm volatile("cp.async.commit_group;");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  if constexpr (FEXP) {  // O28 export (residual only): F at the own x_d = -1 ext points
+    for (int item = threadIdx.x; item < D * NL * NV * E; item += NT) {
+      const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = r2 / NL;
+      if (e0 + el < g.K) b.Fexp[((int64_t)((2 * d) * NL + t) * NV + v) * g.Kp + e0 + el] = sF[item];
+    }
+  }
+  // R~ = R_int + the x_d = -1 face terms (sface_d Dfl[.][0] F), dU/dt = -R~/detJ, RK update
+  // along x-lines (item = x-line t, variable, element); x = -1 trace from registers
+  const double idet = 1.0 / g.detJ;
+  for (int item = threadIdx.x; item < NL * NV * E; item += NT) {
+    const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int j = t % n, k = D == 3 ? t / n : 0;  // y (and z) position of x-line t
+    auto F = [&](int d, int tl) { return sF[((d * NL + tl) * NV + v) * E + el]; };
+    const double fx = g.sface[0] * F(0, t);
+    // y-line through (i, j[, k]): index i + n k, position j; z-line: index i + n j, position k
+    double cy = 0.0, cz = 0.0;
+#pragma unroll
+    for (int q = 0; q < n; ++q) {
+      if (q == j) cy = L.Dfl[q][0] * g.sface[1];
+      if (D == 3 && q == k) cz = L.Dfl[q][0] * g.sface[2];
+    }
+    const int p0 = n * t;
+    double un[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+      const int idx = ((p0 + i) * NV + v) * E + el;
+      const int64_t gi = (int64_t)((p0 + i) * NV + v) * g.Kp + e;
+      double R = fma(L.Dfl[i][0], fx, sR[idx]);
+      R = fma(cy, F(1, D == 3 ? i + n * k : i), R);
+      if constexpr (D == 3) R = fma(cz, F(2, i + n * j), R);
+      const double kk = -R * idet;
+      double nu;
+      switch (stage) {
+        case -1:
+          b.out[gi] = kk;
+          nu = 0.0;
+          break;
+        case 0: {
+          const double u0 = sU[idx];
+          b.ACC[gi] = fma(dt / 6.0, kk, u0);
+          nu = fma(0.5 * dt, kk, u0);
+          b.Us[gi] = nu;
+        } break;
+        case 1:
+          b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+          nu = fma(0.5 * dt, kk, sUn[idx]);
+          b.Us[gi] = nu;
+          break;
+        case 2:
+          b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+          nu = fma(dt, kk, sUn[idx]);
+          b.Us[gi] = nu;
+          break;
+        case 3:
+          nu = fma(dt / 6.0, kk, sAcc[idx]);
+          b.U[gi] = nu;
+          break;
+        default: {  // RK54 stage s (2N-storage, in place)
+          const int s5 = stage - RK54_STAGE0;
+          const double du = s5 == 0 ? dt * kk : fma(rk54_a(s5), sAcc[idx], dt * kk);
+          b.ACC[gi] = du;
+          nu = fma(rk54_b(s5), du, sU[idx]);
+          b.U[gi] = nu;
+        } break;
+      }
+      un[i] = nu;
+      sU[idx] = nu;
+    }
+    if (stage >= 0) b.Tu_next[((int64_t)(0 * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[0], un);
+  }
+  if (stage < 0) return;
+  __syncthreads();
+  // x_d = -1 traces of the new state on the faces normal to y (and z)
+  for (int item = threadIdx.x; item < (D - 1) * NL * NV * E; item += NT) {
+    const int el = item % E, r = item / E, v = r % NV, r2 = r / NV, t = r2 % NL, d = 1 + r2 / NL;
+    const int64_t e = e0 + el;
+    if (e >= g.K) continue;
+    const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+    double u[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
+    b.Tu_next[((int64_t)((2 * d) * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[0], u);
+  }
+}
+
 // TGV diagnostics (NEXT row N4): per tile the solution-point
 // quadrature sums of E* = rho v.v, S^d : S^d and p div v, with grad v from the LDG
 // gradient (GradNb) by the chain rule (reading O20).  part[3 tile + k] (fixed-order
@@ -1182,7 +1396,7 @@ __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph
   __syncthreads();
   {
     GradNb<D, P, EQ, E, NT, NI> gn;
-    gn.load(g, b.Tu, sNb, e0);
+    gn.load(g, ph, b.Tu, sNb, e0);
     mbar_wait(&bar, 0);
     __syncthreads();
     gn.compute(g, L, ph, sU, sQ, e0);
@@ -1229,8 +1443,15 @@ struct TCfg {
   static constexpr size_t TILEA = (size_t)NS * NV * EA * sizeof(double);
   // kernel A: tile, gradient, two internal-flux buffers of NI points per line (NI = p
   // for SDRT, p+1 solution points for FR)
-  static constexpr size_t smem_a(int ni) {
-    return TILEA * (1 + D) + (tensor_a_dbuf(D, NS, NL, NV, EA, ni) ? 2 : 1) * (size_t)NL * ni * NV * EA * sizeof(double);
+  static constexpr size_t smem_a(int ni, bool osf = false) {
+    return TILEA * (1 + D) + (tensor_a_dbuf(D, NS, NL, NV, EA, ni, osf) ? 2 : 1) * (size_t)NL * ni * NV * EA * sizeof(double) +
+           (osf ? (size_t)D * NL * NV * EA * sizeof(double) : 0);
+  }
+  // kernel B, one-sided flux publication: R_int, the x_d = -1 face fluxes, the state tile
+  // (stage input where read) and the RK registers the stage reads
+  static size_t smem_b_osf(int stage) {
+    return TILE * 2 + (size_t)D * NL * NV * E * sizeof(double) + (stage_reads_acc(stage) ? TILE : 0) +
+           (stage_reads_un(stage) ? TILE : 0);
   }
   // kernel B: sU, sR, flux-line slots, + the RK registers the stage reads (ACC: stages
   // 1..3, u_n: stages 1, 2)
@@ -1247,6 +1468,10 @@ template <int D, int P, int EQ>
 static void set_smem(const void* k, size_t bytes) {
   if (bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    // CTAs above ~98 KB: the whole 228 KB carve-out, so that two fit per SM (the default
+    // carve-out stops near 200 KB; measured: OSF kernel A at 112.6 KB ran 1 CTA / SM)
+    if (e == cudaSuccess && bytes > 98 * 1024)
+      e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA smem attr: ") + cudaGetErrorString(e));
   }
 }
@@ -1273,6 +1498,14 @@ static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph
     if constexpr (Phys<EQ, D>::VISC) {
       const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::EA - 1) / C::EA);
       if (grid == 0) return;
+      if constexpr (EQ == EQ_NS) {
+        if (g.osf) {
+          auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A, NI, true>;
+          set_smem<D, P, EQ>((const void*)ka, C::smem_a(NI, true));
+          CUDA_LAUNCH_OK(launch_pdl(ka, grid, C::NTA, C::smem_a(NI, true), st, g, L, ph, b, maps_for(tma, b, false)));
+          return;
+        }
+      }
       auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A, NI>;
       set_smem<D, P, EQ>((const void*)ka, C::smem_a(NI));
       CUDA_LAUNCH_OK(launch_pdl(ka, grid, C::NTA, C::smem_a(NI), st, g, L, ph, b, maps_for(tma, b, false)));
@@ -1280,6 +1513,14 @@ static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph
   } else {
     const unsigned grid = g.tiles ? (unsigned)g.ntiles : (unsigned)((g.K + C::E - 1) / C::E);
     if (grid == 0) return;
+    if constexpr (EQ == EQ_NS) {
+      if (g.osf) {
+        auto kb = b.Fexp ? kt_stage_osf<D, P, EQ, C::E, C::NTB, C::MINB_B, true> : kt_stage_osf<D, P, EQ, C::E, C::NTB, C::MINB_B>;
+        set_smem<D, P, EQ>((const void*)kb, C::smem_b_osf(2));
+        CUDA_LAUNCH_OK(launch_pdl(kb, grid, C::NTB, C::smem_b_osf(stage), st, g, L, ph, b, stage, dt, maps_for(tma, b, true)));
+        return;
+      }
+    }
     auto kb = b.Fexp ? kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI, true> : kt_stage<D, P, EQ, C::E, C::NTB, C::MINB_B, NI>;
     set_smem<D, P, EQ>((const void*)kb, C::smem_b(2, NI));
     CUDA_LAUNCH_OK(launch_pdl(kb, grid, C::NTB, C::smem_b(stage, NI), st, g, L, ph, b, stage, dt, maps_for(tma, b, true)));

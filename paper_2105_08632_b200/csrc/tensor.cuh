@@ -41,6 +41,8 @@ struct TensorGeom {
   double sface[3];    // detJ * 2 / h_d  (= detJ |J^-T n~| on faces normal to d)
   const int* tiles;   // optional tile list (interior / boundary subsets), nullptr = all tiles
   int ntiles;
+  int osf;            // one-sided flux publication (NS, beta = 1/2, no far-field axis): kernel A
+                      // publishes the whole common flux of its x_d = +1 faces (tensor.cu publish_F)
 };
 int tensor_tile_width(int D, int P, int eq);
 
@@ -52,7 +54,7 @@ struct TensorBufs {
   double* out;        // residual output (stage == -1)
   const double* Tu;   // traces of the stage input  [N_ext][N_V][Kp]
   double* Tu_next;    // traces of the stage output
-  double* Tg;         // published viscous normal-flux traces [N_ext][N_V][Kp]
+  double* Tg;         // published viscous normal-flux traces [N_ext][N_V][Kp] (OSF: the common flux F)
   double* Rv;         // viscous internal-flux divergence M13 F~_v [N_sol][N_V][Kp] (kernel A -> B)
   double* Fexp = nullptr;  // optional (residual only): common flux F per own ext point [N_ext][N_V][Kp]
 };
