@@ -40,6 +40,7 @@ struct GeomDev {
   int8_t xface[MAXEXT];    // face of each ext point
   const int* tiles;       // optional tile list (interior / boundary subsets), nullptr = all
   int ntiles;
+  int osf;                // fused simplex path: one-sided flux publication (simplex.cu ks_stage_osf)
 };
 
 // per (shape, ext point) metric: s scale and canonical normal (global memory)

@@ -922,6 +922,11 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         for (unsigned mk : h.kmask) dense = dense && mk == full;
         *dst[i] = SOpF{h.rows, h.cols, h.mt, h.kt, dval, dense ? nullptr : dmask};  // dense: no mask reads
       }
+      {
+        // one-sided flux publication (simplex.cu ks_stage_osf): as for the tensor path
+        const char* ev = std::getenv("SDRT_OSF");
+        c->g.osf = ph->eq == EQ_NS && ph->beta == 0.5 && m.ff_row.empty() && O.scheme == 0 && !(ev && ev[0] == '0');
+      }
       simplex_tma_init(&c->stma, m.nd, m.p, ph->eq, m.K_pad);
       c->Tu[0] = (double*)(base + p.off_tu0);
       c->Tu[1] = (double*)(base + p.off_tu1);

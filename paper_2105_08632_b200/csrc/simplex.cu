@@ -308,9 +308,10 @@ struct NbGather {
   static constexpr int CI = (ITEMS + NT - 1) / NT;
   double nb[CI][NV];
 
-  __device__ __forceinline__ void load(const GeomDev& g, const double* __restrict__ Tu, const int (*sNb)[E],
-                                       int64_t e0) {
+  __device__ __forceinline__ void load(const GeomDev& g, const PhysDev& ph, const double* __restrict__ Tu,
+                                       const int (*sNb)[E], int64_t e0) {
     const int Kp = (int)g.Kt;  // trace row stride
+    const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
     for (int k = 0; k < CI; ++k) {
       const int item = threadIdx.x + k * NT;
@@ -319,6 +320,9 @@ struct NbGather {
       for (int v = 0; v < NV; ++v) nb[k][v] = 0.0;
       if (item >= ITEMS || e0 + el >= g.K) continue;
       const int s = sNb[D + 1][el], f = rho / S::nfp, q = rho % S::nfp;
+      // the neighbour is u_R on a face where this element is left, else u_L; a neighbour
+      // whose LDG weight is 0 is not read (its trace may be stale under OSF)
+      if ((g.left[s][f] ? wr : wl) == 0.0) continue;
       const int m = sNb[f][el];
       const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][q];
 #pragma unroll
@@ -514,7 +518,11 @@ struct SLayoutA {
   static constexpr int TOTAL = X + UE + UU + Q;
 };
 
-template <int D, int P, int EQ, int E>
+// OSF (one-sided flux publication, NS with beta = +1/2; tensor.cu publish_F): at the
+// face points where this element is LEFT it evaluates the face's whole common flux
+// F = Rusanov(u_L, u_R) + g_L + eta (u_L - u_R) (l.312-340) and publishes F instead of g;
+// kernel B (ks_stage_osf) then applies M14 to +/- s F gathered from the two sides.
+template <int D, int P, int EQ, int E, bool OSF = false>
 __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, SimplexOps O, PhysDev ph, SimplexBufs b,
                                                const __grid_constant__ STileMaps tm) {
   pdl_wait();
@@ -541,7 +549,7 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   __syncthreads();
   SPH(0, 0)
   NbGather<D, P, NV, E, SDRT_SA_NT> gath;
-  gath.load(g, b.Tu, sNb, e0);
+  gath.load(g, ph, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
   // U_ext = M0 U, U_u = M12 U
   dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30, sX, sUu);
@@ -570,16 +578,39 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
     Mc.frag = O.M0.frag + (int64_t)(r0 / 8) * O.M0.kt * 32;
     if (Mc.kmask) Mc.kmask = O.M0.kmask + r0 / 8;
     if (r0 > 0) __syncthreads();  // the previous chunk's publish has read X
+    // OSF: u_R of this thread's left face points (the right neighbour's published trace)
+    // is pulled into L1 before the Q_ext product (no registers held across it)
+    constexpr int CP = OSF ? (S::next * E + SDRT_SA_NT - 1) / SDRT_SA_NT : 1;
+    static_assert(!OSF || Ly::QCH >= S::next, "OSF publishes in one chunk");
+    auto uR_at = [&](int item) -> const double* {
+      const int el = item % E, rho = item / E;
+      if (item >= S::next * E || e0 + el >= g.K) return nullptr;
+      const int s = sNb[D + 1][el], f = rho / S::nfp;
+      if (!g.left[s][f]) return nullptr;
+      const int m = sNb[f][el];
+      const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][rho % S::nfp];
+      return b.Tu + ((int64_t)rho2 * Kp + m) * NV;
+    };
+    if constexpr (OSF) {
+#pragma unroll
+      for (int k = 0; k < CP; ++k) {
+        const double* a = uR_at(threadIdx.x + k * SDRT_SA_NT);
+        if (a) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a + NV - 1));
+        }
+      }
+    }
     dmm_blocks<NV, S::kt_sol, E, D>(Mc, sQ, S::nsol * NV * E, sX);  // Q_ext [chunk][d][v]
     __syncthreads();
   SPH(0, 5)
-    for (int item = threadIdx.x; item < nr * E; item += blockDim.x) {
+    auto publish = [&](int item, const double* uR) {
       const int el = item % E, rl = item / E, rho = r0 + rl;
       const int64_t e = e0 + el;
-      if (e >= g.K) continue;
+      if (e >= g.K) return;
       const int s = sNb[D + 1][el], f = rho / S::nfp;
       const bool left = g.left[s][f];
-      if ((left && !pub_left) || (!left && !pub_right)) continue;
+      if ((left && !pub_left) || (!left && !pub_right)) return;
       double u[NV], q[D * NV];
 #pragma unroll
       for (int v = 0; v < NV; ++v) u[v] = sUe[(rho * NV + v) * E + el];
@@ -589,8 +620,35 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
       const double nl[3] = {mt.n0, mt.n1, mt.n2};
       double gv[NV];
       Ph::visc_dir(ph, u, q, nl, gv);
+      if constexpr (OSF) {  // left side: the whole common flux along n_L
+        double F[NV];
+        Ph::conv_common(ph, u, uR, nl, F);
+        const double wl = 0.5 + ph.beta;  // = 1
 #pragma unroll
-      for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
+        for (int v = 0; v < NV; ++v) {
+          F[v] = Ph::ldg_rn(F[v], __dmul_rn(wl, gv[v]), ph.eta, u[v], uR[v]);
+          b.Tg[((int64_t)rho * Kp + e) * NV + v] = F[v];
+          if (b.Fexp) b.Fexp[((int64_t)rho * NV + v) * g.Kp + e] = F[v];  // O28 export (residual only)
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
+      }
+    };
+    if constexpr (OSF) {
+#pragma unroll
+      for (int k = 0; k < CP; ++k) {
+        const int item = threadIdx.x + k * SDRT_SA_NT;
+        const double* a = uR_at(item);
+        if (a) {
+          double uR[NV];
+#pragma unroll
+          for (int v = 0; v < NV; ++v) uR[v] = a[v];
+          publish(item, uR);
+        }
+      }
+    } else {
+      for (int item = threadIdx.x; item < nr * E; item += blockDim.x) publish(item, nullptr);
     }
   }
   __syncthreads();
@@ -636,7 +694,7 @@ __global__ void __launch_bounds__(256, SDRT_SA_MINB) ks_grad_fr(GeomDev g, Simpl
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
   NbGather<D, P, NV, E, 256> gath;
-  gath.load(g, b.Tu, sNb, e0);
+  gath.load(g, ph, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
   dmm1<NV, S::kt_sol, E, false>(O.M0, sU, 1 << 30, sU, sW);  // U_ext
   __syncthreads();
@@ -936,6 +994,171 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   SPH(1, 7)
 }
 
+// Kernel B with one-sided flux publication (OSF, NS with beta = +1/2): the common flux
+// of every face point was evaluated once by the face's left element (ks_grad<OSF>) and
+// published in T_g; here D~ = +s F (own left faces) / -s F (right faces, gathered from
+// the left neighbour), R~ = R_int + M14 D~ (l.2919-2925), -R~/detJ, RK update, and the
+// traces of the new state at the faces where this element is RIGHT (the only ones
+// kernel A reads with beta = 1/2).  The stage input is read only where the RK formula
+// needs it (RK4 stage 0, RK54).
+template <int D, int P, int EQ, int E, bool FEXP = false>
+__global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage_osf(GeomDev g, SimplexOps O, PhysDev ph,
+                                                                    SimplexBufs b, int stage, double dt,
+                                                                    const __grid_constant__ STileMaps tm) {
+  pdl_wait();
+  using Ph = Phys<EQ, D>;
+  using S = SDims<D, P>;
+  using Ly = SLayoutB<D, P, Ph::NV, false>;
+  constexpr int NV = Ph::NV, NT = SDRT_SB_NT;
+  extern __shared__ __align__(128) double smem[];
+  double* sU = smem;
+  double* sR = sU + Ly::U * E;
+  double* sUn = sR + Ly::U * E;
+  double* sAcc = sUn + Ly::U * E;
+  double* sD = sAcc + Ly::U * E;  // D~ [next][NV][E]
+  __shared__ int sNb[D + 2][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  const bool need_in = stage == 0 || stage >= RK54_STAGE0;
+  constexpr unsigned TB = S::nsol * NV * E * 8;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, TB * (1 + (need_in ? 1 : 0) + (stage_reads_un(stage) ? 1 : 0) + (stage_reads_acc(stage) ? 1 : 0)));
+    tma_tile<S::nsol * NV, E>(sR, &tm.rint, e0, &bar);
+    if (need_in) tma_tile<S::nsol * NV, E>(sU, &tm.uin, e0, &bar);
+    if (stage_reads_un(stage)) tma_tile<S::nsol * NV, E>(sUn, &tm.un, e0, &bar);
+    if (stage_reads_acc(stage)) tma_tile<S::nsol * NV, E>(sAcc, &tm.acc, e0, &bar);
+  }
+  fill_neighbours<D, E>(g, sNb, e0);
+  __syncthreads();
+  // the published F of each of this thread's face points (own for left faces, the left
+  // neighbour's otherwise), requested before the tile wait
+  constexpr int ITEMS = S::next * E, CI = (ITEMS + NT - 1) / NT;
+  const int Kp = (int)g.Kt;
+  double Fv[CI][NV];
+#pragma unroll
+  for (int k = 0; k < CI; ++k) {
+    const int item = threadIdx.x + k * NT;
+    const int el = item % E, rho = item / E;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Fv[k][v] = 0.0;
+    if (item >= ITEMS || e0 + el >= g.K) continue;
+    const int s = sNb[D + 1][el], f = rho / S::nfp;
+    int64_t at;
+    if (g.left[s][f]) {
+      at = (int64_t)rho * Kp + e0 + el;
+    } else {
+      const int rho2 = g.nface[s][f] * S::nfp + g.perm[s][f][rho % S::nfp];
+      at = (int64_t)rho2 * Kp + sNb[f][el];
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Fv[k][v] = b.Tg[at * NV + v];
+  }
+#pragma unroll
+  for (int k = 0; k < CI; ++k) {
+    const int item = threadIdx.x + k * NT;
+    const int el = item % E, rho = item / E;
+    if (item >= ITEMS) continue;
+    const int64_t e = e0 + el;
+    double sc = 0.0;
+    if (e < g.K) {
+      const int s = sNb[D + 1][el], f = rho / S::nfp;
+      const ExtMetric mt = b.xm[s * S::next + rho];
+      sc = g.left[s][f] ? mt.s : -mt.s;
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      sD[(rho * NV + v) * E + el] = sc * Fv[k][v];
+      if (FEXP && e < g.K) b.Fexp[((int64_t)rho * NV + v) * g.Kp + e] = Fv[k][v];  // O28 export (residual only)
+    }
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  dmm1<NV, S::kt_ext, E, true>(O.M14, sD, 1 << 30, sD, sR);  // R~ = R_int + M14 D~
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < S::nsol * NV * E; idx += NT) {
+    const int el = idx % E, row = idx / E;
+    const int64_t e = e0 + el;
+    if (e >= g.K) {
+      sU[idx] = 0.0;
+      continue;
+    }
+    const int64_t gi = (int64_t)row * g.Kp + e;
+    const int s = sNb[D + 1][el];
+    const double kk = -sR[idx] / g.detJ[s];
+    double nu;
+    switch (stage) {
+      case -1: b.out[gi] = kk; nu = 0.0; break;
+      case 0: {
+        const double u0 = sU[idx];
+        b.ACC[gi] = fma(dt / 6.0, kk, u0);
+        nu = fma(0.5 * dt, kk, u0);
+        b.Us[gi] = nu;
+      } break;
+      case 1:
+        b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+        nu = fma(0.5 * dt, kk, sUn[idx]);
+        b.Us[gi] = nu;
+        break;
+      case 2:
+        b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+        nu = fma(dt, kk, sUn[idx]);
+        b.Us[gi] = nu;
+        break;
+      case 3:
+        nu = fma(dt / 6.0, kk, sAcc[idx]);
+        b.U[gi] = nu;
+        break;
+      default: {  // RK54 stage s (2N-storage, in place)
+        const int s5 = stage - RK54_STAGE0;
+        const double du = s5 == 0 ? dt * kk : fma(rk54_a(s5), sAcc[idx], dt * kk);
+        b.ACC[gi] = du;
+        nu = fma(rk54_b(s5), du, sU[idx]);
+        b.U[gi] = nu;
+      } break;
+    }
+    sU[idx] = nu;
+  }
+  if (stage < 0) return;
+  __syncthreads();
+  // traces of the new state M0 U at the right-side faces only (point-major)
+  using DM = Dmm<NV, E, S::kt_sol>;
+  const int warp = threadIdx.x >> 5, nw = NT >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < DM::jobs(O.M0); j += nw) {
+    const int m = j / DM::NG, ng = j % DM::NG;
+    const int n0 = ng * DM::NGR * 8 + (lane >> 2);
+    const double* af = O.M0.frag + (int64_t)m * S::kt_sol * 32 + lane;
+    const unsigned km = O.M0.kmask ? __ldg(O.M0.kmask + m) : 0xffffffffu;
+    double a[S::kt_sol];
+#pragma unroll
+    for (int k = 0; k < S::kt_sol; ++k) a[k] = (km >> k & 1u) ? __ldg(af + k * 32) : 0.0;
+    double c[DM::NGR][2];
+#pragma unroll
+    for (int q = 0; q < DM::NGR; ++q) c[q][0] = c[q][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < S::kt_sol; ++k) {
+      if (!(km >> k & 1u)) continue;
+      const int col = 4 * k + (lane & 3);
+      const bool ok = col < O.M0.cols;
+#pragma unroll
+      for (int q = 0; q < DM::NGR; ++q) dmma(c[q][0], c[q][1], a[k], ok ? sU[col * DM::N + n0 + 8 * q] : 0.0);
+    }
+    const int r = 8 * m + (lane >> 2);
+    if (r < O.M0.rows) {
+      const int f = r / S::nfp;
+#pragma unroll
+      for (int q = 0; q < DM::NGR; ++q) {
+        const int n = ng * DM::NGR * 8 + 8 * q + 2 * (lane & 3);  // column (w, el), el even
+        const int w = n / E, el = n % E;
+        double* gp = b.Tu_next + ((int64_t)r * g.Kt + e0 + el) * NV + w;
+        if (e0 + el < g.K && !g.left[sNb[D + 1][el]][f]) gp[0] = c[q][0];
+        if (e0 + el + 1 < g.K && !g.left[sNb[D + 1][el + 1]][f]) gp[NV] = c[q][1];
+      }
+    }
+  }
+}
+
 // TGV diagnostics (NEXT row N4): per tile the solution-point
 // quadrature sums (w_r detJ_s) of E* = rho v.v, S^d : S^d and p div v, grad v from the
 // LDG gradient (the prologue of kernel A) by the chain rule (reading O20).
@@ -965,7 +1188,7 @@ __global__ void __launch_bounds__(256) ks_diag(GeomDev g, SimplexOps O, PhysDev 
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
   NbGather<D, P, NV, E, NT> gath;
-  gath.load(g, b.Tu, sNb, e0);
+  gath.load(g, ph, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
   dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sU, 1 << 30, sU, sUe, O.M12, sU, 1 << 30, sU, sUu);
   __syncthreads();
@@ -1040,11 +1263,21 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
         CUDA_LAUNCH_OK(launch_pdl(k, grid, 256, sm, st, g, O, ph, b, smaps(tma, b, b.Uin, false)));
       } else {
         auto k = ks_grad<D, P, EQ, C::E>;
+        if constexpr (EQ == EQ_NS)
+          if (g.osf) k = ks_grad<D, P, EQ, C::E, true>;
         sset_smem((const void*)k, C::SMEM_A);
         CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SA_NT, C::SMEM_A, st, g, O, ph, b, smaps(tma, b, b.Uin, false)));
       }
     }
   } else if (which == 1) {
+    if constexpr (EQ == EQ_NS) {
+      if (g.osf && !O.fr) {
+        auto k = b.Fexp ? ks_stage_osf<D, P, EQ, C::E, true> : ks_stage_osf<D, P, EQ, C::E>;
+        sset_smem((const void*)k, C::SMEM_B);
+        CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SB_NT, C::SMEM_B, st, g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true)));
+        return;
+      }
+    }
     auto k = b.Fexp ? ks_stage<D, P, EQ, C::E, true> : ks_stage<D, P, EQ, C::E>;
     sset_smem((const void*)k, C::SMEM_B);
     CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SB_NT, C::SMEM_B, st, g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true)));
