@@ -887,6 +887,23 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
           for (int j = 0; j < n; ++j) L.Dfl[i][j + 1] = O.Dsol[0](i, j) - e0 * L.Iend[0][j] - e1 * L.Iend[1][j];
         }
       }
+      {
+        // composite gradient operator per axis (tensor.cuh Line1D::Gq), long double
+        const int NI = L.fr ? n : m.p;
+        const long double wl = 0.5L - (long double)ph->beta, wr = 0.5L + (long double)ph->beta;
+        for (int d = 0; d < m.nd; ++d) {
+          const long double jd = t.jinv[d];
+          for (int i = 0; i < n; ++i) {
+            for (int j = 0; j < n; ++j) {
+              long double a = (long double)L.Dfl[i][0] * wr * L.Iend[0][j] + (long double)L.Dfl[i][NI + 1] * wl * L.Iend[1][j];
+              for (int k = 0; k < NI; ++k) a += (long double)L.Dfl[i][k + 1] * L.Iint[k][j];
+              L.Gq[d][i][j] = (double)(jd * a);
+            }
+            L.H0[d][i] = (double)(jd * L.Dfl[i][0] * wl);
+            L.H1[d][i] = (double)(jd * L.Dfl[i][NI + 1] * wr);
+          }
+        }
+      }
       tensor_tma_init(&c->tma, m.nd, m.p, ph->eq, m.K_pad);
       c->Tu[0] = (double*)(base + p.off_tu0);
       c->Tu[1] = (double*)(base + p.off_tu1);

@@ -50,6 +50,11 @@
 #ifndef SDRT_TA_GPAIR
 #define SDRT_TA_GPAIR 2
 #endif
+// kernel A gradient through the composite per-axis operator Line1D::Gq (GradNb): 1 on, 0 the
+// step-by-step form (own traces, common values, U_int, then Dfl)
+#ifndef SDRT_TA_GQ
+#define SDRT_TA_GQ 1
+#endif
 // kernel A internal fluxes and published g by register-blocked line items (visc_line):
 // 0 off (per-point items), 1 on
 #ifndef SDRT_TA_LINE
@@ -241,6 +246,25 @@ struct GradNb {
       double u[n];
 #pragma unroll
       for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
+#if SDRT_TA_GQ
+      // composite operator (Line1D::Gq); d is warp-uniform (items are d-major), so the
+      // branches select compile-time coefficient sets
+      auto gq = [&](auto dc) {
+        constexpr int dd = decltype(dc)::value;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          double q = L.H0[dd][i] * nb[k][0];
+          q = fma(L.H1[dd][i], nb[k][1], q);
+#pragma unroll
+          for (int j = 0; j < n; ++j) q = fma(L.Gq[dd][i][j], u[j], q);
+          sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el] = q;
+        }
+      };
+      if (d == 0) gq(std::integral_constant<int, 0>{});
+      else if (d == 1) gq(std::integral_constant<int, 1>{});
+      else if constexpr (D == 3) gq(std::integral_constant<int, 2>{});
+      continue;
+#endif
       // common values at both ends (own trace recomputed bit-identically, neighbour read)
       const double own0 = interp_end<n>(L.Iend[0], u), own1 = interp_end<n>(L.Iend[1], u);
       // face x_d = -1: this element is RIGHT; face x_d = +1: this element is LEFT

@@ -23,10 +23,18 @@ constexpr int TMAXP = 4;  // max degree of the fused tensor path
 //   Iend[1] (discontinuous-flux derivative minus its end values times the correction
 //   derivatives), Dfl[.][0] / Dfl[.][p+2] = the correction derivatives -g_L', g_R'
 //   (FR-SDRT: the SDRT end values; FR-DG: Radau).
+//   Gq[d][i][j], H0[d][i], H1[d][i]: the gradient along axis d at solution point i of a
+//   line (l.282-302) as ONE composite operator on the line's solution values and the two
+//   neighbour traces: (2/h_d) Dfl . [C_-; Iint u; C_+] with C_- = wl nb_- + wr Iend0 u,
+//   C_+ = wl Iend1 u + wr nb_+ (wl = 1/2 - beta, wr = 1/2 + beta), i.e.
+//   q_i = sum_j Gq[d][i][j] u_j + H0[d][i] nb_- + H1[d][i] nb_+ (built on the host from the
+//   operators above, beta and J^-T; the same linear map in fewer operations).
 struct Line1D {
   double Iend[2][TMAXP + 1];
   double Iint[TMAXP + 1][TMAXP + 1];
   double Dfl[TMAXP + 1][TMAXP + 3];
+  double Gq[3][TMAXP + 1][TMAXP + 1];
+  double H0[3][TMAXP + 1], H1[3][TMAXP + 1];
   int fr;  // 0: SDRT (p internal flux points), 1: FR (p+1 solution points)
 };
 
