@@ -817,7 +817,8 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
     CUDA_OK(cudaMemcpyAsync(c->xm, xm.data(), xm.size() * sizeof(ExtMetric), cudaMemcpyHostToDevice, st));
     // zero the intermediate buffers (padding columns stay finite)
     CUDA_OK(cudaMemsetAsync(base, 0, p.off_ops, st));
-    c->ph = PhysDev{{ph->c[0], ph->c[1], ph->c[2]}, ph->mu, ph->gamma, ph->Pr, ph->beta, ph->eta};
+    c->ph = PhysDev{{ph->c[0], ph->c[1], ph->c[2]}, ph->mu, ph->gamma, ph->Pr, ph->beta, ph->eta,
+                    ph->mu * ph->gamma / ((ph->gamma - 1.0) * ph->Pr)};
     // fused tensor-product path (default for quad/hex; SDRT_FORCE_GENERIC=1 selects the
     // generic operator path, a test hook for cross-checking the two)
     c->etype = m.etype;

@@ -17,6 +17,7 @@ enum { EQ_LINADV = 0, EQ_LINADVDIFF = 1, EQ_EULER = 2, EQ_NS = 3 };
 struct PhysDev {
   double c[3];
   double mu, gamma, Pr, beta, eta;
+  double kappa;  // mu gamma / ((gamma - 1) Pr), formed once on the host (same IEEE ops)
 };
 
 template <int EQ, int D>
@@ -78,7 +79,7 @@ struct Phys {
       double div = 0.0;
 #pragma unroll
       for (int i = 0; i < D; ++i) div += dv[i][i];
-      const double kappa = ph.mu * g / ((g - 1.0) * ph.Pr);
+      const double kappa = ph.kappa;
       // tau_{id} w_d, heat flux . w
       out[0] = 0.0;
       double tw[D];
@@ -161,7 +162,7 @@ struct Phys {
         dvt[j] = j == D0 ? dvn[D0] : (q[j * NV + 1 + D0] - v[D0] * q[j * NV]) * ir;
         div += j == D0 ? dvn[D0] : (q[j * NV + 1 + j] - v[j] * q[j * NV]) * ir;
       }
-      const double kappa = ph.mu * g / ((g - 1.0) * ph.Pr);
+      const double kappa = ph.kappa;
       out[0] = 0.0;
       double tv = 0.0;
 #pragma unroll

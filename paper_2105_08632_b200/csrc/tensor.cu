@@ -50,6 +50,11 @@
 #ifndef SDRT_TA_GPAIR
 #define SDRT_TA_GPAIR 2
 #endif
+// kernel A internal-flux items ordered (a, t, el) with a compile-time point index per
+// warp-uniform branch (SDRT_TA_AUNI = 1) or (t, a, el) with a runtime index (0)
+#ifndef SDRT_TA_AUNI
+#define SDRT_TA_AUNI 0
+#endif
 // kernel A gradient through the composite per-axis operator Line1D::Gq (GradNb): 1 on, 0 the
 // step-by-step form (own traces, common values, U_int, then Dfl)
 #ifndef SDRT_TA_GQ
@@ -519,9 +524,10 @@ __device__ __forceinline__ void publish_F(const TensorGeom& g, const Line1D& L, 
 
 // internal transformed flux F~ = detJ (J^-1 (f^c - f^v))_d at internal point a of d-line t
 // (one normal component, B7; l.305-311) -> sF[t][a][v][el]
-template <int D, int P, int EQ, int E, int d, int NI>
+template <int D, int P, int EQ, int E, int d, int NI, int AC = -1>
 __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
-                                              const double* sU, const double* sQ, double* sF, int t, int a, int el) {
+                                              const double* sU, const double* sQ, double* sF, int t, int a_, int el) {
+  const int a = AC >= 0 ? AC : a_;  // AC: internal point index known at compile time
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NS = T::NS;
@@ -971,6 +977,24 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
         if (ph_ == 0) visc_internal2<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, t, a, el);
         else if (ph_ == 1) visc_internal2<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, t, a, el);
         else if constexpr (D == 3) visc_internal2<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, t, a, el);
+      } else if constexpr (SDRT_TA_AUNI != 0 && NI <= 4) {
+        // items (a, t, el), a slowest: a is warp-uniform (NL E is a multiple of 32), so the
+        // branches give each internal point its own compile-time coefficient set
+        const int i2 = item - nA, el = i2 % E, r = i2 / E, t = r % NL, a = r / NL;
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        auto run = [&](auto dc, auto ac) {
+          constexpr int d = decltype(dc)::value, A = decltype(ac)::value;
+          if constexpr (A < NI) visc_internal<D, P, EQ, E, d, NI, A>(g, L, ph, sU, sQ, f1, t, A, el);
+        };
+        auto by_a = [&](auto dc) {
+          if (a == 0) run(dc, std::integral_constant<int, 0>{});
+          else if (a == 1) run(dc, std::integral_constant<int, 1>{});
+          else if (a == 2) run(dc, std::integral_constant<int, 2>{});
+          else run(dc, std::integral_constant<int, 3>{});
+        };
+        if (ph_ == 0) by_a(std::integral_constant<int, 0>{});
+        else if (ph_ == 1) by_a(std::integral_constant<int, 1>{});
+        else if constexpr (D == 3) by_a(std::integral_constant<int, 2>{});
       } else {
         const int i2 = item - nA, el = i2 % E, r = i2 / E, a = r % NI, t = r / NI;
         double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
