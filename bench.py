@@ -40,6 +40,8 @@ METRIC = "SDRT residual GDOF-stage/s (fp64) and % of HBM roofline at 1/2/4/8 B20
 # reference-arm sample size (patterns per axis) so K steps of the oracle take ~1 s each
 REF_SUBBOX = {"c1": 8, "c2": 40, "c3": 6, "c4": 8, "c5": 4, "c4pri": 6}
 UNIT = "GDOF-stage/s"
+# ncu SASS fp64 counts of the tensor kernels at the current code (tools/sass_counts.py)
+SASS_COUNTS = "r02_sass_counts.json"
 WORKLOADS = {
     "c1": "c1: 2D linear advection, quad p=2, 8^2 periodic",
     "c2": "c2: 2D isentropic Euler vortex, tri p=3, 40^2x2",
@@ -73,11 +75,23 @@ def dims(cfg):
     return D, ns, ne, nu
 
 
+def osf(cfg):
+    """One-sided flux publication: NS with beta = +1/2 on a mesh without
+    far-field axes (the library's rule, kernels.cu; SDRT_OSF=0 disables it)."""
+    return cfg.eq == "ns" and cfg.beta == 0.5 and os.environ.get("SDRT_OSF", "1") != "0"
+
+
 def kernel_bytes(cfg, K):
     """Algorithmic bytes per launch of each kernel (each input array read once, each
-    output written once; fp64).  tensor_stage(B): stage input + RK registers (3 N_sol
-    rows on average over the 4 stages) + neighbour U traces + viscous traces + new
-    traces; tensor_grad(A): stage input + U traces + published viscous traces."""
+    output written once; fp64; the R_int hand-over between kernels A and B is design
+    overhead, not counted).  tensor_stage(B): stage input + RK registers (3 N_sol rows
+    on average over the 4 stages) + neighbour U traces + viscous traces + new traces;
+    tensor_grad(A): stage input + U traces + published viscous traces.  One-sided flux
+    publication (osf): A reads the stage input and the N_ext/2 right-neighbour traces and
+    writes N_ext/2 common fluxes; B reads/writes 3.25 N_sol RK rows on average (the stage
+    input only where the RK formula reads it), gathers the common fluxes of its faces
+    (tensor: the N_ext/2 x_d = -1 faces, the + faces went into R_int; simplex: all N_ext)
+    and writes the N_ext/2 traces kernel A reads."""
     D, ns, ne, nu = dims(cfg)
     V = cfg.nvars
     b = 8 * V * K
@@ -103,6 +117,10 @@ def kernel_bytes(cfg, K):
     out["simplex_traces"] = out["tensor_traces"]
     out["simplex_grad(A)"] = out["tensor_grad(A)"]
     out["simplex_stage(B)"] = out["tensor_stage(B)"]
+    if osf(cfg):
+        out["tensor_grad(A)"] = out["simplex_grad(A)"] = b * (ns + ne // 2 + ne // 2)
+        out["tensor_stage(B)"] = b * (3.25 * ns + ne // 2 + ne // 2)
+        out["simplex_stage(B)"] = b * (3.25 * ns + ne + ne // 2)
     return out
 
 
@@ -147,6 +165,9 @@ def kernel_flops(cfg, K):
         b = 2 * 2 * D * NL * V * n + D * NL * fr + 2 * D * NL * V * n * 2 + 4 * ns * V + 2 * 2 * D * NL * V * n
         if not visc:
             b += D * NL * p * (2 * V * n + fc) + m13
+        if osf(cfg):  # A: + common flux and its M14 term at the + ends; B: - faces' M14, RK, - traces
+            a += D * NL * fr + 2 * D * NL * V * n
+            b = 2 * D * NL * V * n + 4 * ns * V + 2 * D * NL * V * n
         out["tensor_grad(A)"] = K * a
         out["tensor_stage(B)"] = K * b
         out["tensor_traces"] = K * 2 * 2 * D * NL * V * n
@@ -158,6 +179,9 @@ def kernel_flops(cfg, K):
         b = 2 * ne * ns * V + (ne / 2) * fr + 2 * ns * ne * V + 4 * ns * V + 2 * ne * ns * V
         if not visc:
             b += 2 * nu * ns * V + nu * D * fc + 2 * ns * D * nu * V
+        if osf(cfg):  # A: + the common flux at the left faces; B: M14, RK, right-face traces
+            a += (ne / 2) * fr
+            b = 2 * ns * ne * V + 4 * ns * V + ne * ns * V
         out["simplex_grad(A)"] = K * a
         out["simplex_stage(B)"] = K * b
         out["simplex_traces"] = K * 2 * ne * ns * V
@@ -437,15 +461,15 @@ def main():
         traffic = json.load(open(tf)).get(dom)
     kf = kernel_flops(cfg, K)
     flops_source = "model (bench.kernel_flops)"
-    sc = os.path.join(ROOT, "profiles", "r02_sass_counts.json")
+    sc = os.path.join(ROOT, "profiles", SASS_COUNTS)
     if os.path.exists(sc) and world == 1:
         # executed fp64 flops of the tensor kernels from ncu SASS counts (2 DFMA + DMUL +
-        # DADD per launch, profiles/r02_sass_counts.json) replace the model
+        # DADD per launch, profiles/SASS_COUNTS) replace the model
         sass = json.load(open(sc)).get(cfg.name, {})
         for kn, v in sass.items():
             if kn.startswith("tensor_") and kn in kf:
                 kf[kn] = v["flops_per_launch"]
-                flops_source = f"ncu SASS counts (profiles/r02_sass_counts.json) for the tensor kernels"
+                flops_source = f"ncu SASS counts (profiles/{SASS_COUNTS}) for the tensor kernels"
     t_launch = dom_ms / dom_n * 1e-3 if dom else None
     gbs = kb[dom] / t_launch / 1e9 if dom in kb else None
     tfs = kf[dom] / t_launch / 1e12 if dom in kf else None
