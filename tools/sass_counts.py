@@ -37,7 +37,7 @@ def load(path):
         fl = 2 * d.get("smsp__sass_thread_inst_executed_op_dfma_pred_on.sum", 0) + \
             d.get("smsp__sass_thread_inst_executed_op_dmul_pred_on.sum", 0) + \
             d.get("smsp__sass_thread_inst_executed_op_dadd_pred_on.sum", 0)
-        dmma = d.get("smsp__inst_executed_op_dmma.sum", 0)
+        dmma = d.get("sm__inst_executed_pipe_tensor_subpipe_dmma.sum", 0)
         t = d.get("gpu__time_duration.sum", 0)
         tu = d.get("_unit_gpu__time_duration.sum", "ns")
         us = t / 1000.0 if tu == "ns" else (t * 1000.0 if tu == "ms" else t)
@@ -51,7 +51,7 @@ def load(path):
         o["us_per_launch_ncu"] += us
         o["dram_bytes_per_launch"] += by("dram__bytes_read.sum") + by("dram__bytes_write.sum")
         o["fp64_pipe_pct"] += d.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 0)
-        o["dmma_pipe_pct"] += d.get("sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active", 0)
+        o["dmma_pipe_pct"] += d.get("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", 0)
         o["launches"] += 1
     for o in out.values():
         n = o["launches"]
@@ -63,7 +63,7 @@ def load(path):
 
 if __name__ == "__main__":
     res = {"_how": "ncu --metrics gpu__time_duration.sum,smsp__sass_thread_inst_executed_op_{dfma,dadd,dmul}_pred_on.sum,"
-                   "smsp__inst_executed_op_dmma.sum,sm__pipe_fp64_cycles_active,sm__pipe_tensor_op_dmma_cycles_active,"
+                   "sm__inst_executed_pipe_tensor_subpipe_dmma.sum,sm__pipe_fp64_cycles_active,sm__pipe_tensor_op_dmma_cycles_active,"
                    "dram__bytes_{read,write}.sum --clock-control none -k regex:k[ts]_ -s 6 -c 6 (python bench.py "
                    "--config C --steps 2 --warmup 3); flops = 2 DFMA + DMUL + DADD per launch (fp64 pipe), "
                    "dmma_flops = DMMA instructions x 512 (8x8x4 FMA, zero padding included), averaged over the "
