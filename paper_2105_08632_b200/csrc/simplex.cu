@@ -104,6 +104,14 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SB_NT
 #define SDRT_SB_NT 160
 #endif
+#ifndef SDRT_SB_MINB_OSF
+#define SDRT_SB_MINB_OSF 4
+#endif
+// OSF kernel B: whole shared-memory carve-out (5 CTAs / SM instead of 4); measured slower
+// on c5 (B 1.49 -> 1.57 ms: the smaller L1 serves the flux gathers worse), off
+#ifndef SDRT_SB_CARVE
+#define SDRT_SB_CARVE 0
+#endif
 #ifndef SDRT_SPLIT_INTFLUX
 #define SDRT_SPLIT_INTFLUX 0
 #endif
@@ -1002,7 +1010,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
 // kernel A reads with beta = 1/2).  The stage input is read only where the RK formula
 // needs it (RK4 stage 0, RK54).
 template <int D, int P, int EQ, int E, bool FEXP = false>
-__global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage_osf(GeomDev g, SimplexOps O, PhysDev ph,
+__global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB_OSF) ks_stage_osf(GeomDev g, SimplexOps O, PhysDev ph,
                                                                     SimplexBufs b, int stage, double dt,
                                                                     const __grid_constant__ STileMaps tm) {
   pdl_wait();
@@ -1229,10 +1237,16 @@ struct SCfg {
   static constexpr size_t SMEM_T = (size_t)(SDims<D, P>::nsol + SDims<D, P>::next) * NV * E * sizeof(double);
 };
 
-static void sset_smem(const void* k, size_t bytes) {
+// carve: request the whole 228 KB shared-memory carve-out (kernels whose operator
+// fragments fit the remaining L1; the default carve-out stops short of 5 x 38 KB CTAs)
+static void sset_smem(const void* k, size_t bytes, bool carve = false) {
   if (bytes > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA smem attr: ") + cudaGetErrorString(e));
+  }
+  if (carve) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA carveout attr: ") + cudaGetErrorString(e));
   }
 }
 
@@ -1273,7 +1287,7 @@ static void srun(const GeomDev& g, const SimplexOps& O, const PhysDev& ph, Simpl
     if constexpr (EQ == EQ_NS) {
       if (g.osf && !O.fr) {
         auto k = b.Fexp ? ks_stage_osf<D, P, EQ, C::E, true> : ks_stage_osf<D, P, EQ, C::E>;
-        sset_smem((const void*)k, C::SMEM_B);
+        sset_smem((const void*)k, C::SMEM_B, SDRT_SB_CARVE != 0);
         CUDA_LAUNCH_OK(launch_pdl(k, grid, SDRT_SB_NT, C::SMEM_B, st, g, O, ph, b, stage, dt, smaps(tma, b, b.Uin, true)));
         return;
       }
