@@ -95,6 +95,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SA_QCH
 #define SDRT_SA_QCH 1024
 #endif
+// kernel A tiles formed in shared memory padded to a row stride of N + 4 (SLayoutA):
+// removes the 2-way bank conflicts of the B-fragment loads (c5: 169 M of 519 M shared
+// wavefronts), but the padded tiles need 75.8 KB per CTA (two CTAs per SM) or a
+// two-chunk Q_ext (three CTAs); measured on c5 kernel A: unpadded 3.13 ms, padded at two
+// CTAs / SM 3.13 ms (256 threads) / 3.63-3.66 ms (320 / 384), padded two-chunk 3.55 ms
+// (unpadded two-chunk 3.65 ms): off
+#ifndef SDRT_SA_PAD
+#define SDRT_SA_PAD 0
+#endif
+#ifndef SDRT_SA_QCHP
+#define SDRT_SA_QCHP 32
+#endif
 #ifndef SDRT_SA_NT
 #define SDRT_SA_NT 256
 #endif
@@ -128,7 +140,10 @@ __host__ __device__ constexpr int ngroup(int n) {
 // from X1 (row stride N = W E doubles); Y rows r < M.rows.  Warp jobs = (m-tile,
 // group of NGR n-tiles).  KT (k steps) is a compile-time constant: all A fragments
 // of a job are requested at once (one L1/L2 round trip per job), then the MMAs run.
-template <int W, int E, int KT, int YS = W * E>
+// XR: row stride of the X tiles (N, or N + 4 for the padded tiles of kernel A: with
+// N = 40 the four k-rows a half-warp reads for a 64-bit B fragment fall on the same 8
+// banks twice; a stride of 44 puts them on four disjoint bank windows)
+template <int W, int E, int KT, int YS = W * E, int XR = W * E>
 struct Dmm {
   static constexpr int N = W * E;
   static_assert(N % 8 == 0, "tile columns must be a multiple of 8");
@@ -158,7 +173,7 @@ struct Dmm {
     for (int k = 0; k < KT; ++k) {
       if (!(km >> k & 1u)) continue;
       const int col = 4 * k + (lane & 3);
-      const double* xr = col < split ? X0 + col * N : X1 + (col - split) * N;
+      const double* xr = col < split ? X0 + col * XR : X1 + (col - split) * XR;
       const bool ok = col < M.cols;
 #pragma unroll
       for (int q = 0; q < NGR; ++q) {
@@ -184,29 +199,30 @@ struct Dmm {
 
 // Y1 = M1 X1 (W1 per row, KT1 k steps) and Y2 = M2 X2 (W2, KT2) in one phase
 // (independent products; M2.frag == nullptr skips the second)
-template <int W1, int KT1, int W2, int KT2, int E, bool ACC1, bool ACC2>
+template <int W1, int KT1, int W2, int KT2, int E, bool ACC1, bool ACC2, int YS1 = W1 * E, int YS2 = W2 * E>
 __device__ __forceinline__ void dmm2(const SOpF& M1, const double* X1a, int s1, const double* X1b, double* Y1,
                                      const SOpF& M2, const double* X2a, int s2, const double* X2b, double* Y2) {
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int j1 = Dmm<W1, E, KT1>::jobs(M1), j2 = M2.frag ? Dmm<W2, E, KT2>::jobs(M2) : 0;
+  const int j1 = Dmm<W1, E, KT1, YS1>::jobs(M1), j2 = M2.frag ? Dmm<W2, E, KT2, YS2>::jobs(M2) : 0;
   for (int j = warp; j < j1 + j2; j += nw) {
-    if (j < j1) Dmm<W1, E, KT1>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
-    else Dmm<W2, E, KT2>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
+    if (j < j1) Dmm<W1, E, KT1, YS1>::template job<ACC1>(M1, j, X1a, s1, X1b, Y1);
+    else Dmm<W2, E, KT2, YS2>::template job<ACC2>(M2, j - j1, X2a, s2, X2b, Y2);
   }
 }
 
-template <int W, int KT, int E, bool ACC>
+template <int W, int KT, int E, bool ACC, int XR = W * E, int YS = W * E>
 __device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split, const double* X1, double* Y) {
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nj = Dmm<W, E, KT>::jobs(M);
-  for (int j = warp; j < nj; j += nw) Dmm<W, E, KT>::template job<ACC>(M, j, X0, split, X1, Y);
+  using DM = Dmm<W, E, KT, YS, XR>;
+  const int nj = DM::jobs(M);
+  for (int j = warp; j < nj; j += nw) DM::template job<ACC>(M, j, X0, split, X1, Y);
 }
 
 // the same operator on the ND row blocks of a [nd][rows][W][E] tile (block stride XS
 // doubles), written interleaved as Y[r][nd][W][E]: one job pool for all blocks
-template <int W, int KT, int E, int ND>
+template <int W, int KT, int E, int ND, int XR = W * E>
 __device__ __forceinline__ void dmm_blocks(const SOpF& M, const double* X, int XS, double* Y) {
-  using DM = Dmm<W, E, KT, ND * W * E>;
+  using DM = Dmm<W, E, KT, ND * W * E, XR>;
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int nj = DM::jobs(M);
   for (int j = warp; j < ND * nj; j += nw) {
@@ -218,10 +234,10 @@ __device__ __forceinline__ void dmm_blocks(const SOpF& M, const double* X, int X
 // Y = M X with the result rows written straight from the MMA fragments to global
 // memory, G[(r W + w) ld + e0 + el] (element-major ABI layout, 16-byte stores), for
 // e0 + el < K.  Saves the shared-memory round trip and a barrier for final products.
-template <int W, int KT, int E, bool POINT_MAJOR = false>
+template <int W, int KT, int E, bool POINT_MAJOR = false, int XR = W * E>
 __device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, double* __restrict__ Gout, int64_t ld,
                                             int64_t e0, int64_t K) {
-  using DM = Dmm<W, E, KT>;
+  using DM = Dmm<W, E, KT, W * E, XR>;
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   for (int j = warp; j < DM::jobs(M); j += nw) {
@@ -241,7 +257,7 @@ __device__ __forceinline__ void dmm1_global(const SOpF& M, const double* X, doub
       const int col = 4 * k + (lane & 3);
       const bool ok = col < M.cols;
 #pragma unroll
-      for (int q = 0; q < DM::NGR; ++q) dmma(c[q][0], c[q][1], a[k], ok ? X[col * DM::N + n0 + 8 * q] : 0.0);
+      for (int q = 0; q < DM::NGR; ++q) dmma(c[q][0], c[q][1], a[k], ok ? X[col * XR + n0 + 8 * q] : 0.0);
     }
     const int r = 8 * m + (lane >> 2);
     if (r < M.rows) {
@@ -338,6 +354,7 @@ struct NbGather {
     }
   }
 
+  template <int CR = NV * E>  // row stride of sC
   __device__ __forceinline__ void common_values(const GeomDev& g, const PhysDev& ph, const double* sUe,
                                                 const int (*sNb)[E], double* sC, int64_t e0) const {
     const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
@@ -348,7 +365,7 @@ struct NbGather {
       if (item >= ITEMS) break;
       if (e0 + el >= g.K) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) sC[(rho * NV + v) * E + el] = 0.0;
+        for (int v = 0; v < NV; ++v) sC[rho * CR + v * E + el] = 0.0;
         continue;
       }
       const int s = sNb[D + 1][el], f = rho / S::nfp;
@@ -357,7 +374,7 @@ struct NbGather {
       for (int v = 0; v < NV; ++v) {
         const double own = sUe[(rho * NV + v) * E + el];
         const double uL = left ? own : nb[k][v], uR = left ? nb[k][v] : own;
-        sC[(rho * NV + v) * E + el] = __fma_rn(wr, uR, __dmul_rn(wl, uL));  // explicit: same bits both sides
+        sC[rho * CR + v * E + el] = __fma_rn(wr, uR, __dmul_rn(wl, uL));  // explicit: same bits both sides
       }
     }
   }
@@ -417,7 +434,7 @@ struct FluxGather {
 };
 
 // Q = J^-T Q~ in place on sQ [D][nsol][NV][E]
-template <int D, int P, int NV, int E>
+template <int D, int P, int NV, int E, int QR = NV * E>  // QR: row stride of sQ
 __device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E], double* sQ) {
   using S = SDims<D, P>;
   for (int item = threadIdx.x; item < S::nsol * E; item += blockDim.x) {
@@ -427,13 +444,13 @@ __device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E
     for (int v = 0; v < NV; ++v) {
       double qt[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) qt[d] = sQ[((d * S::nsol + sp) * NV + v) * E + el];
+      for (int d = 0; d < D; ++d) qt[d] = sQ[(d * S::nsol + sp) * QR + v * E + el];
 #pragma unroll
       for (int i = 0; i < D; ++i) {
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < D; ++j) acc = fma(g.Jinv[s][j * 3 + i], qt[j], acc);
-        sQ[((i * S::nsol + sp) * NV + v) * E + el] = acc;
+        sQ[(i * S::nsol + sp) * QR + v * E + el] = acc;
       }
     }
   }
@@ -441,7 +458,7 @@ __device__ __forceinline__ void metric_grad(const GeomDev& g, const int (*sNb)[E
 
 // internal transformed fluxes for all D components (B7: simplices keep all) at the
 // unique internal points: F~[d][u] = detJ (J^-1 (f^c - f^v))_d -> sF [D][nu][NV][E]
-template <int D, int P, int EQ, int E>
+template <int D, int P, int EQ, int E, int UR = Phys<EQ, D>::NV * E, int FR = Phys<EQ, D>::NV * E>
 __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev& ph, const int (*sNb)[E],
                                                 const double* sUu, const double* sQu, double* sF, int64_t e0) {
   using Ph = Phys<EQ, D>;
@@ -455,13 +472,13 @@ __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev&
       for (int d = 0; d < D; ++d)
         if (ND == 1 || d == dsel)
 #pragma unroll
-          for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = 0.0;
+          for (int v = 0; v < NV; ++v) sF[(d * S::nu + u) * FR + v * E + el] = 0.0;
       continue;
     }
     const int s = sNb[D + 1][el];
     double uu[NV], qq[Ph::VISC ? D * NV : 1];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) uu[v] = sUu[(u * NV + v) * E + el];
+    for (int v = 0; v < NV; ++v) uu[v] = sUu[u * UR + v * E + el];
     if constexpr (Ph::VISC) {
 #pragma unroll
       for (int k = 0; k < D * NV; ++k) qq[k] = sQu[(u * D * NV + k) * E + el];
@@ -480,7 +497,7 @@ __device__ __forceinline__ void internal_fluxes(const GeomDev& g, const PhysDev&
         for (int v = 0; v < NV; ++v) fo[v] += fv[v];
       }
 #pragma unroll
-      for (int v = 0; v < NV; ++v) sF[((d * S::nu + u) * NV + v) * E + el] = fo[v];
+      for (int v = 0; v < NV; ++v) sF[(d * S::nu + u) * FR + v * E + el] = fo[v];
     }
   }
 }
@@ -513,16 +530,22 @@ __global__ void __launch_bounds__(256) ks_traces(GeomDev g, SimplexOps O, const 
 //   UE [max(next NV, nu D NV)]: U_ext, then Q_u
 //   UU [nu NV]: U_u
 //   Q  [nsol D NV]: Q, then R_int (nsol NV)
-template <int D, int P, int NV>
+template <int D, int P, int NV, int E>
 struct SLayoutA {
   using S = SDims<D, P>;
+  static constexpr int N = NV * E;  // columns (variable, element) of a tile row
+  // row stride of the tiles read as DMMA B operands after being formed in shared memory
+  // (C, U_u, Q, F~): N + 4 with SDRT_SA_PAD (conflict-free B fragments, see Dmm); the
+  // stage-input tile U arrives by TMA and keeps N
+  static constexpr int RS = SDRT_SA_PAD ? N + 4 : N;
   // Q_ext is formed and published in chunks of QCH external points (whole 8-row
-  // m-tiles of M0), so region X holds one chunk
-  static constexpr int QCH = cmin(SDRT_SA_QCH, (S::next + 7) / 8 * 8);
-  static constexpr int X = cmax(cmax(cmax(S::nsol * NV, S::next * NV), QCH * D * NV), S::nu * D * NV);
-  static constexpr int UE = cmax(S::next * NV, S::nu * D * NV);
-  static constexpr int UU = S::nu * NV;
-  static constexpr int Q = S::nsol * D * NV;
+  // m-tiles of M0), so region X holds one chunk (smaller with padding: 3 CTAs / SM)
+  static constexpr int QCH = cmin(SDRT_SA_PAD ? SDRT_SA_QCHP : SDRT_SA_QCH, (S::next + 7) / 8 * 8);
+  // region sizes in doubles per tile
+  static constexpr int X = cmax(cmax(cmax(S::nsol * N, S::next * RS), QCH * D * N), D * S::nu * RS);
+  static constexpr int UE = cmax(S::next * N, S::nu * D * N);
+  static constexpr int UU = S::nu * RS;
+  static constexpr int Q = D * S::nsol * RS;
   static constexpr int TOTAL = X + UE + UU + Q;
 };
 
@@ -537,13 +560,13 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   SPH_INIT
   using Ph = Phys<EQ, D>;
   using S = SDims<D, P>;
-  using Ly = SLayoutA<D, P, Ph::NV>;
-  constexpr int NV = Ph::NV;
+  using Ly = SLayoutA<D, P, Ph::NV, E>;
+  constexpr int NV = Ph::NV, RS = Ly::RS;
   extern __shared__ __align__(128) double smem[];
   double* sX = smem;
-  double* sUe = sX + Ly::X * E;
-  double* sUu = sUe + Ly::UE * E;
-  double* sQ = sUu + Ly::UU * E;
+  double* sUe = sX + Ly::X;
+  double* sUu = sUe + Ly::UE;
+  double* sQ = sUu + Ly::UU;
   __shared__ int sNb[D + 2][E];  // [f][el] neighbours, [D+1][el] shape
   __shared__ __align__(8) uint64_t bar;
   const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
@@ -560,16 +583,17 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   gath.load(g, ph, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
   // U_ext = M0 U, U_u = M12 U
-  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30, sX, sUu);
+  dmm2<NV, S::kt_sol, NV, S::kt_sol, E, false, false, NV * E, RS>(O.M0, sX, 1 << 30, sX, sUe, O.M12, sX, 1 << 30,
+                                                                   sX, sUu);
   __syncthreads();
   SPH(0, 1)
-  gath.common_values(g, ph, sUe, sNb, sX, e0);  // C into X (U is dead)
+  gath.template common_values<RS>(g, ph, sUe, sNb, sX, e0);  // C into X (U is dead)
   __syncthreads();
   SPH(0, 2)
-  dmm1<NV, S::kt_G, E, false>(O.G, sX, S::next, sUu, sQ);  // rows (d, s) -> [d][s][v]
+  dmm1<NV, S::kt_G, E, false, RS, RS>(O.G, sX, S::next, sUu, sQ);  // rows (d, s) -> [d][s][v]
   __syncthreads();
   SPH(0, 3)
-  metric_grad<D, P, NV, E>(g, sNb, sQ);
+  metric_grad<D, P, NV, E, RS>(g, sNb, sQ);
   __syncthreads();
   SPH(0, 4)
   // gradient at the external points (M0 on each of the D NV gradient rows) into X, one
@@ -588,11 +612,10 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
     if (r0 > 0) __syncthreads();  // the previous chunk's publish has read X
     // OSF: u_R of this thread's left face points (the right neighbour's published trace)
     // is pulled into L1 before the Q_ext product (no registers held across it)
-    constexpr int CP = OSF ? (S::next * E + SDRT_SA_NT - 1) / SDRT_SA_NT : 1;
-    static_assert(!OSF || Ly::QCH >= S::next, "OSF publishes in one chunk");
-    auto uR_at = [&](int item) -> const double* {
-      const int el = item % E, rho = item / E;
-      if (item >= S::next * E || e0 + el >= g.K) return nullptr;
+    constexpr int CP = OSF ? (Ly::QCH * E + SDRT_SA_NT - 1) / SDRT_SA_NT : 1;
+    auto uR_at = [&](int item) -> const double* {  // item over the chunk's (point, element)
+      const int el = item % E, rho = r0 + item / E;
+      if (item >= nr * E || e0 + el >= g.K) return nullptr;
       const int s = sNb[D + 1][el], f = rho / S::nfp;
       if (!g.left[s][f]) return nullptr;
       const int m = sNb[f][el];
@@ -609,7 +632,7 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
         }
       }
     }
-    dmm_blocks<NV, S::kt_sol, E, D>(Mc, sQ, S::nsol * NV * E, sX);  // Q_ext [chunk][d][v]
+    dmm_blocks<NV, S::kt_sol, E, D, RS>(Mc, sQ, S::nsol * RS, sX);  // Q_ext [chunk][d][v]
     __syncthreads();
   SPH(0, 5)
     auto publish = [&](int item, const double* uR) {
@@ -661,13 +684,13 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   }
   __syncthreads();
   SPH(0, 6)
-  dmm_blocks<NV, S::kt_sol, E, D>(O.M12, sQ, S::nsol * NV * E, sUe);  // Q_u = M18 Q [nu][d][v] into UE
+  dmm_blocks<NV, S::kt_sol, E, D, RS>(O.M12, sQ, S::nsol * RS, sUe);  // Q_u = M18 Q [nu][d][v] into UE
   __syncthreads();
   SPH(0, 7)
-  internal_fluxes<D, P, EQ, E>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
+  internal_fluxes<D, P, EQ, E, RS, RS>(g, ph, sNb, sUu, sUe, sX, e0);  // F~ [D][nu][NV] into X
   __syncthreads();
   SPH(0, 8)
-  dmm1_global<NV, S::kt_F, E>(O.M13F, sX, b.Rint, g.Kp, e0, g.K);  // R_int -> HBM
+  dmm1_global<NV, S::kt_F, E, false, RS>(O.M13F, sX, b.Rint, g.Kp, e0, g.K);  // R_int -> HBM
   SPH(0, 9)
   SPH(0, 10)
 }
@@ -1232,7 +1255,7 @@ struct SCfg {
   // take 4-element tiles (SDRT_S_E2D): twice the CTAs for the small latency-bound meshes
   static constexpr int E = (D == 2 && (NV * SDRT_S_E2D) % 8 == 0) ? SDRT_S_E2D : 8;
   static constexpr int THREADS = 256;
-  static constexpr size_t SMEM_A = (size_t)SLayoutA<D, P, NV>::TOTAL * E * sizeof(double);
+  static constexpr size_t SMEM_A = (size_t)SLayoutA<D, P, NV, E>::TOTAL * sizeof(double);
   static constexpr size_t SMEM_B = (size_t)SLayoutB<D, P, NV, !VISC>::TOTAL * E * sizeof(double);
   static constexpr size_t SMEM_T = (size_t)(SDims<D, P>::nsol + SDims<D, P>::next) * NV * E * sizeof(double);
 };
