@@ -463,6 +463,14 @@ struct sdrt_ctx {
   int rank = 0, nranks = 1;
   bool auto_halo = false;     // library performs the (loopback) exchange itself
   double* Fexp = nullptr;     // sdrt_face_flux: per-ext-point common flux export (residual only)
+  // slab-pipelined stages (fused tensor path, one-sided flux publication, single rank):
+  // the mesh is cut into `slabs` z-ranges; kernel A of slab k and kernel B of other
+  // slabs run concurrently on two streams, ordered by per-slab events (fused_steps_slabs)
+  int slabs = 0;
+  int slab_tile[17] = {};     // first tile of slab k (slab_tile[slabs] = number of tiles)
+  const int* d_iota = nullptr;  // tile ids 0 .. ntiles-1 (slab k = d_iota + slab_tile[k])
+  cudaStream_t sA = nullptr, sB = nullptr;
+  cudaEvent_t evA[16] = {}, evB[16] = {}, evStart = nullptr, evEnd = nullptr;
 };
 
 // Dense operator in DMMA fragment order (simplex.cuh SOpF): rows padded to 8, columns
@@ -994,6 +1002,40 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         CUDA_OK(cudaMemcpyAsync(dt, inner.data(), inner.size() * sizeof(int), cudaMemcpyHostToDevice, st));
       c->d_tiles = dt;
     }
+    // slab pipeline (fused_steps_slabs): 3-D fused tensor path with one-sided flux
+    // publication on one rank; slab k = whole z-planes [z_k, z_k+1) (every neighbour across
+    // an x or y face lies in the same slab, across a z face in slab k +- 1 mod S);
+    // SDRT_SLABS = S (4..16; default 0 = off: measured on c4, S = 4 / 8 / 16 give 27.4 / 24.9 /
+    // 24.1 GDOF-stage/s against 31.9 single-stream -- kernel A already fills every SM
+    // (two CTAs), the concurrent B CTAs displace it, and the 2S launches and events per
+    // stage add their own gaps)
+    if (c->fused && c->tg.osf && m.nd == 3 && !(m.halo[0] || m.halo[1] || m.halo[2])) {
+      const char* ev = std::getenv("SDRT_SLABS");
+      int S = ev ? std::atoi(ev) : 0;
+      const int E = tensor_tile_width(m.nd, m.p, ph->eq);
+      const int64_t plane = (int64_t)m.Nloc[0] * m.Nloc[1] * m.nsub;
+      if (S > m.Nloc[2]) S = m.Nloc[2];
+      if (S >= 4 && S <= 16 && plane % E == 0) {
+        const int64_t tpp = plane / E;  // tiles per z-plane
+        const int ntile = (int)(tpp * m.Nloc[2]);
+        std::vector<int> iota(ntile);
+        for (int i = 0; i < ntile; ++i) iota[i] = i;
+        int* di = (int*)(base + p.off_tiles);
+        CUDA_OK(cudaMemcpyAsync(di, iota.data(), iota.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+        c->d_iota = di;
+        c->slabs = S;
+        for (int k = 0; k <= S; ++k) c->slab_tile[k] = (int)(tpp * ((int64_t)m.Nloc[2] * k / S));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->sA, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->sB, cudaStreamNonBlocking));
+        for (int k = 0; k < S; ++k) {
+          CUDA_OK(cudaEventCreateWithFlags(&c->evA[k], cudaEventDisableTiming));
+          CUDA_OK(cudaEventCreateWithFlags(&c->evB[k], cudaEventDisableTiming));
+        }
+        CUDA_OK(cudaEventCreateWithFlags(&c->evStart, cudaEventDisableTiming));
+        CUDA_OK(cudaEventCreateWithFlags(&c->evEnd, cudaEventDisableTiming));
+      }
+    }
     CUDA_OK(cudaStreamSynchronize(st));  // host vectors go out of scope
     *out = c;
     return SDRT_OK;
@@ -1003,6 +1045,16 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
 void sdrt_ctx_destroy(sdrt_ctx* c) {
   if (!c) return;
   for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->slabs > 0) {
+    for (int k = 0; k < c->slabs; ++k) {
+      cudaEventDestroy(c->evA[k]);
+      cudaEventDestroy(c->evB[k]);
+    }
+    cudaEventDestroy(c->evStart);
+    cudaEventDestroy(c->evEnd);
+    cudaStreamDestroy(c->sA);
+    cudaStreamDestroy(c->sB);
+  }
   if (c->comm) nccl_comm_destroy(c->comm);
   delete c;
 }
@@ -1218,6 +1270,69 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
   }
 }
 
+// Slab-pipelined RK stages (fused tensor path, one-sided flux publication, one rank).
+// Per stage, kernel A of slab k runs on stream sA and kernel B of slab k on stream sB;
+// the dependencies of one stage on the previous are exactly
+//   A(s, k) after B(s-1, k) and B(s-1, k+1)   (its stage input, its +z neighbours' traces)
+//   B(s, k) after A(s, k) and A(s, k-1)       (R_int, its -z neighbours' common fluxes)
+// (indices mod S; the same per-element arithmetic as fused_stage, so the result is bitwise
+// the unsplit one).  Stream order supplies the lower slab of each pair, one event the
+// other: A(s, k) waits for evB[k+1] (evB[S-1] for the last slab), B(s, k) for evA[k]
+// (evA[S-1] for slab 0, whose -z neighbours are the last slab).  The write-after-read
+// hazards on the double-buffered traces, R_int and the published fluxes are covered by
+// the same chain for S >= 4.  While slab k's B streams from HBM, later
+// slabs' A (compute-bound) run on the other SMs.
+static void fused_steps_slabs(sdrt_ctx* c, double* U, double dt, int nsteps, const int* stages, int nst,
+                              cudaStream_t st) {
+  const int S = c->slabs;
+  CUDA_OK(cudaEventRecord(c->evStart, st));
+  CUDA_OK(cudaStreamWaitEvent(c->sA, c->evStart, 0));
+  CUDA_OK(cudaStreamWaitEvent(c->sB, c->evStart, 0));
+  bool first = true;
+  for (int step = 0; step < nsteps; ++step) {
+    for (int si = 0; si < nst; ++si) {
+      const int stage = stages[si];
+      TensorBufs b;
+      b.Uin = (stage == 0 || stage >= RK54_STAGE0) ? U : c->Us;
+      b.U = U;
+      b.Us = c->Us;
+      b.ACC = c->ACC;
+      b.out = nullptr;
+      b.Tu = c->Tu[c->cur];
+      b.Tu_next = c->Tu[c->cur ^ 1];
+      b.Tg = c->Tg;
+      b.Rv = c->R;
+      b.Fexp = nullptr;
+      for (int k = 0; k < S; ++k) {
+        if (!first) CUDA_OK(cudaStreamWaitEvent(c->sA, c->evB[k + 1 < S ? k + 1 : S - 1], 0));
+        TensorGeom tgp = c->tg;
+        tgp.tiles = c->d_iota + c->slab_tile[k];
+        tgp.ntiles = c->slab_tile[k + 1] - c->slab_tile[k];
+        {
+          Mark mk(c, c->sA, T_FA);
+          tensor_launch_grad(c->nd, c->p, c->eq, tgp, c->line, c->ph, &c->tma, b, c->sA);
+        }
+        CUDA_OK(cudaEventRecord(c->evA[k], c->sA));
+      }
+      for (int k = 0; k < S; ++k) {
+        CUDA_OK(cudaStreamWaitEvent(c->sB, c->evA[k == 0 ? S - 1 : k], 0));
+        TensorGeom tgp = c->tg;
+        tgp.tiles = c->d_iota + c->slab_tile[k];
+        tgp.ntiles = c->slab_tile[k + 1] - c->slab_tile[k];
+        {
+          Mark mk(c, c->sB, T_FB);
+          tensor_launch_flux(c->nd, c->p, c->eq, tgp, c->line, c->ph, &c->tma, b, stage, dt, c->sB);
+        }
+        CUDA_OK(cudaEventRecord(c->evB[k], c->sB));
+      }
+      c->cur ^= 1;
+      first = false;
+    }
+  }
+  CUDA_OK(cudaEventRecord(c->evEnd, c->sB));
+  CUDA_OK(cudaStreamWaitEvent(st, c->evEnd, 0));
+}
+
 static void sfused_traces(sdrt_ctx* c, const double* U, cudaStream_t st) {
   {
     Mark mk(c, st, T_STRACE);
@@ -1370,6 +1485,24 @@ sdrt_status sdrt_rk_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int ch
     ResFn res = pick_res(c->eq, c->nd);
     if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
     if (c->sfused && nsteps > 0) sfused_traces(c, d_U, st);
+    if (c->slabs > 0 && nsteps > 0) {
+      static const int rk4[4] = {0, 1, 2, 3};
+      for (int done = 0; done < nsteps;) {
+        const int n = check_every > 0 ? std::min(check_every, nsteps - done) : nsteps - done;
+        fused_steps_slabs(c, d_U, dt, n, rk4, 4, st);
+        done += n;
+        CUDA_OK(cudaGetLastError());
+        int64_t bad;
+        if (check_every > 0 && !pick_chk(c->eq, c->nd)(c, d_U, st, &bad)) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "diverged: element %lld non-finite or non-physical after step %d",
+                   (long long)bad, done);
+          set_error(buf);
+          return SDRT_E_DIVERGED;
+        }
+      }
+      return SDRT_OK;
+    }
     for (int step = 0; step < nsteps; ++step) {
       for (int s = 0; s < 4; ++s) {
         if (c->fused) fused_stage(c, s == 0 ? d_U : c->Us, d_U, s, dt, nullptr, st);
@@ -1430,6 +1563,21 @@ sdrt_status sdrt_rk54_step(sdrt_ctx* c, double* d_U, double dt, int nsteps, int 
     }
     if (c->fused && nsteps > 0) fused_traces(c, d_U, st);
     if (c->sfused && nsteps > 0) sfused_traces(c, d_U, st);
+    if (c->slabs > 0 && nsteps > 0) {
+      static const int rk54[5] = {RK54_STAGE0, RK54_STAGE0 + 1, RK54_STAGE0 + 2, RK54_STAGE0 + 3, RK54_STAGE0 + 4};
+      for (int done = 0; done < nsteps;) {
+        const int n = check_every > 0 ? std::min(check_every, nsteps - done) : nsteps - done;
+        fused_steps_slabs(c, d_U, dt, n, rk54, 5, st);
+        done += n;
+        CUDA_OK(cudaGetLastError());
+        int64_t bad;
+        if (check_every > 0 && !pick_chk(c->eq, c->nd)(c, d_U, st, &bad)) {
+          set_error("diverged after step " + std::to_string(done) + " (RK54)");
+          return SDRT_E_DIVERGED;
+        }
+      }
+      return SDRT_OK;
+    }
     for (int step = 0; step < nsteps; ++step) {
       for (int s = 0; s < 5; ++s) {
         if (c->fused) fused_stage(c, d_U, d_U, RK54_STAGE0 + s, dt, nullptr, st);
