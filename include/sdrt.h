@@ -186,6 +186,16 @@ sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void
  * products on tri/tet; default 10), 0 = the solution points with weights w_r = int l_r.
  * Synchronous host->device upload.  SDRT_E_INVALID_ARG outside 0..10. */
 sdrt_status sdrt_diagnostics_rule(sdrt_ctx* c, int degree);
+/* CUDA-graph replay of K-step runs (the run is PAPER.md's explicit RK stepping, l.351,
+ * l.1120): with mode 1 (or -1: on for meshes below 2^22 DOF; the default is 0, off, because
+ * the direct launches with programmatic dependent launch measured faster on every config)
+ * sdrt_rk_step / sdrt_rk54_step with check_every <= 0 capture their launch
+ * sequence once into a CUDA graph on a library-owned stream and replay it while the call
+ * repeats with the same d_U, dt, nsteps and integrator; results are bitwise those of the
+ * direct launches.  0 disables.  The graph is ordered after prior work on `stream` and
+ * later work on `stream` after it (events).  Not used with timing, a communicator or the
+ * slab schedule.  SDRT_E_INVALID_ARG for other modes. */
+sdrt_status sdrt_ctx_set_graph(sdrt_ctx* c, int mode);
 /* Per-kernel device timing (CUDA events recorded on the launching stream around each
  * kernel) for measurement: enable, run, then read per-kernel totals.  names receives
  * max_tags NUL-terminated strings of 64 bytes each (may be NULL); ms/counts get the

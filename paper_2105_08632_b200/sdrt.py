@@ -85,6 +85,7 @@ lib.sdrt_stage_flux.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_double, _vp, _v
 lib.sdrt_stage_grad_part.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_int, _vp]
 lib.sdrt_stage_flux_part.argtypes = [_vp, _vp, ctypes.c_int, ctypes.c_double, _vp, ctypes.c_int, _vp]
 lib.sdrt_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
+lib.sdrt_ctx_set_graph.argtypes = [_vp, ctypes.c_int]
 lib.sdrt_ctx_kernel_times.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, ctypes.POINTER(ctypes.c_int)]
 lib.sdrt_ctx_last_launches.argtypes = [_vp]
 lib.sdrt_ctx_last_launches.restype = ctypes.c_int64
@@ -98,7 +99,8 @@ EXPORTED = ["sdrt_abi_version", "sdrt_last_error", "sdrt_mesh_create", "sdrt_mes
             "sdrt_mesh_export_maps", "sdrt_mesh_sol_coords", "sdrt_mesh_detj", "sdrt_mesh_destroy",
             "sdrt_operators_build", "sdrt_operators_get", "sdrt_operators_destroy",
             "sdrt_ctx_workspace_bytes", "sdrt_ctx_create", "sdrt_residual", "sdrt_face_flux", "sdrt_rk_step",
-            "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_kernel_times",
+            "sdrt_ctx_last_launches", "sdrt_ctx_destroy", "sdrt_ctx_set_timing", "sdrt_ctx_set_graph",
+            "sdrt_ctx_kernel_times",
             "sdrt_mesh_set_halo", "sdrt_mesh_halo_lists", "sdrt_mesh_neighbor", "sdrt_halo_info",
             "sdrt_halo_pack", "sdrt_halo_unpack", "sdrt_stage_traces", "sdrt_stage_grad", "sdrt_stage_flux",
             "sdrt_comm_unique_id", "sdrt_ctx_attach_comm", "sdrt_ctx_set_farfield"]
@@ -269,6 +271,10 @@ def rk_step(ctx, U_ptr, dt, nsteps, check_every=0, stream=0):
 
 def ctx_set_timing(ctx, enable):
     _check(lib.sdrt_ctx_set_timing(ctx, int(bool(enable))))
+
+
+def ctx_set_graph(ctx, mode):
+    _check(lib.sdrt_ctx_set_graph(ctx, int(mode)))
 
 
 def ctx_kernel_times(ctx, max_tags=32):

@@ -98,6 +98,10 @@ class Solver:
     def set_timing(self, enable):
         sdrt.ctx_set_timing(self.ctx, enable)
 
+    def set_graph(self, mode):
+        """CUDA-graph replay of repeated K-step calls: -1 auto (small meshes), 0 off, 1 on."""
+        sdrt.ctx_set_graph(self.ctx, mode)
+
     def kernel_times(self):
         return sdrt.ctx_kernel_times(self.ctx)
 

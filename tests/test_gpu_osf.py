@@ -142,3 +142,28 @@ def test_slab_pipeline_bitwise(N, slabs, integrator):
     if integrator == "rk4":
         R = Residual(m, Physics(cfg.eq, cfg.nd, **cfg.physics_kwargs()))
         assert _rel(out[slabs], integrate(R, U0, cfg.dt, 3)) <= TOL
+
+
+@pytest.mark.parametrize("name,N,integrator,steps", [("c1", 5, "rk4", 7), ("c2", 4, "rk4", 3), ("c3", 3, "rk4", 2),
+                                                      ("c4", 3, "rk54", 3), ("c5", 3, "rk54", 1)])
+def test_graph_replay_bitwise(name, N, integrator, steps):
+    """CUDA-graph replay of repeated K-step calls (sdrt_ctx_set_graph) gives bitwise the
+    direct launches, also when an odd stage count flips the trace buffer between calls."""
+    cfg = CONFIGS[name]
+    Nt = (N,) * cfg.nd
+    from oracle.mesh import build_mesh
+    m = build_mesh(cfg.etype, cfg.p, Nt, cfg.lo, cfg.hi)
+    out = {}
+    for mode in (1, 0):
+        S = _solver_env(cfg, Nt, {})
+        S.set_graph(mode)
+        U0 = random_state(cfg, S.shape[0], m.K, seed=9, amp=0.2)
+        Ud = S.to_device(U0)
+        f = S.rk_step if integrator == "rk4" else S.rk54_step
+        for _ in range(3):  # capture, then two replays (RK54: alternating trace buffers)
+            f(Ud, cfg.dt, steps)
+        out[mode] = S.to_host(Ud)
+        torch.cuda.synchronize()
+        S.close()
+    assert np.isfinite(out[1]).all()
+    assert np.array_equal(out[1].view(np.int64), out[0].view(np.int64))
