@@ -461,7 +461,7 @@ def main():
     # the degree-10 quadrature, 24 bytes D2H, a synchronising read per step).  Reported
     # beside the state-through-host trajectory above, not instead of it.
     mon = None
-    if cfg.eq == "ns" and cfg.nd == 3 and world == 1:
+    if cfg.eq == "ns" and cfg.nd == 3 and cfg.etype in ("hex", "tet") and world == 1:  # fused paths
         U.copy_(pin, non_blocking=True)
         torch.cuda.synchronize(dev)
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
