@@ -95,6 +95,14 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SA_QCH
 #define SDRT_SA_QCH 1024
 #endif
+// OSF kernel A: publish items compacted to the tile's left-face points (1) or all face
+// points with the right-face lanes idle (0).  Measured on c5: compacted 3.78 ms vs 3.13 ms
+// per kernel-A launch -- the compacted lanes walk one element's points (shared-memory
+// stride N_V D E between lanes: bank conflicts on every gradient load) where the
+// uncompacted lanes read consecutive elements; off
+#ifndef SDRT_SA_PCOMP
+#define SDRT_SA_PCOMP 0
+#endif
 // kernel A tiles formed in shared memory padded to a row stride of N + 4 (SLayoutA):
 // removes the 2-way bank conflicts of the B-fragment loads (c5: 169 M of 519 M shared
 // wavefronts), but the padded tiles need 75.8 KB per CTA (two CTAs per SM) or a
@@ -579,6 +587,28 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
   fill_neighbours<D, E>(g, sNb, e0);
   __syncthreads();
   SPH(0, 0)
+  // OSF compacted publish items (SDRT_SA_PCOMP): per element slot the first item of its
+  // left-face points (sPref) and each shape's left faces (sLeftF), for the publish phase
+  __shared__ int sPref[E + 1];
+  __shared__ signed char sLeftF[MAXSUB][4];
+  if constexpr (OSF && SDRT_SA_PCOMP) {
+    if (threadIdx.x < g.nsub) {
+      int k = 0;
+      for (int f = 0; f < S::nfaces; ++f)
+        if (g.left[threadIdx.x][f]) sLeftF[threadIdx.x][k++] = (signed char)f;
+    }
+    if (threadIdx.x == 32) {
+      int acc = 0;
+      for (int el = 0; el < E; ++el) {
+        sPref[el] = acc;
+        if (e0 + el < g.K) {
+          const int s = sNb[D + 1][el];
+          for (int f = 0; f < S::nfaces; ++f) acc += g.left[s][f] ? S::nfp : 0;
+        }
+      }
+      sPref[E] = acc;
+    }
+  }
   NbGather<D, P, NV, E, SDRT_SA_NT> gath;
   gath.load(g, ph, b.Tu, sNb, e0);
   mbar_wait(&bar, 0);
@@ -666,7 +696,24 @@ __global__ void __launch_bounds__(SDRT_SA_NT, SDRT_SA_MINB) ks_grad(GeomDev g, S
         for (int v = 0; v < NV; ++v) b.Tg[((int64_t)rho * Kp + e) * NV + v] = gv[v];
       }
     };
-    if constexpr (OSF) {
+    if constexpr (OSF && SDRT_SA_PCOMP) {
+      // compacted: item i -> the i-th left-face point of the tile (element slot by the
+      // prefix sPref, face by the shape's left-face list): every lane carries a point
+      static_assert(Ly::QCH >= S::next, "compacted publish needs one chunk");
+      for (int i = threadIdx.x; i < sPref[E]; i += SDRT_SA_NT) {
+        int el = 0;
+#pragma unroll
+        for (int j = 1; j < E; ++j) el += (i >= sPref[j]) ? 1 : 0;
+        const int loc = i - sPref[el];
+        const int f = sLeftF[sNb[D + 1][el]][loc / S::nfp];
+        const int item = (f * S::nfp + loc % S::nfp) * E + el;
+        const double* a = uR_at(item);
+        double uR[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) uR[v] = a[v];
+        publish(item, uR);
+      }
+    } else if constexpr (OSF) {
 #pragma unroll
       for (int k = 0; k < CP; ++k) {
         const int item = threadIdx.x + k * SDRT_SA_NT;
