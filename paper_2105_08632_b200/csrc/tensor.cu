@@ -350,6 +350,29 @@ struct GradNb2 {
         u[0][i] = x.x;
         u[1][i] = x.y;
       }
+#if SDRT_TA_GQ
+      // composite operator (Line1D::Gq), d warp-uniform (items d-major): compile-time
+      // coefficient sets per branch
+      auto gq2 = [&](auto dc) {
+        constexpr int dd = decltype(dc)::value;
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          double q0 = L.H0[dd][i] * nb[k][0][0], q1 = L.H0[dd][i] * nb[k][1][0];
+          q0 = fma(L.H1[dd][i], nb[k][0][1], q0);
+          q1 = fma(L.H1[dd][i], nb[k][1][1], q1);
+#pragma unroll
+          for (int j = 0; j < n; ++j) {
+            q0 = fma(L.Gq[dd][i][j], u[0][j], q0);
+            q1 = fma(L.Gq[dd][i][j], u[1][j], q1);
+          }
+          *reinterpret_cast<double2*>(sQ + ((dd * NS + (lb + i * ls)) * NV + v) * E + el0) = make_double2(q0, q1);
+        }
+      };
+      if (d == 0) gq2(std::integral_constant<int, 0>{});
+      else if (d == 1) gq2(std::integral_constant<int, 1>{});
+      else if constexpr (D == 3) gq2(std::integral_constant<int, 2>{});
+      continue;
+#endif
       const double jd = g.jinv[d];
       double q2[2][n];
 #pragma unroll
