@@ -23,6 +23,11 @@
 #include <vector>
 
 #include "capi_internal.h"
+// TGV diagnostics on tensor elements: the degree-10 cubature interpolation applied
+// sum-factorised through its 1D factor (1) or as the dense N_q x N_sol matrix (0)
+#ifndef SDRT_DIAG_SF
+#define SDRT_DIAG_SF 1
+#endif
 #include "comm.h"
 #include "ctx.h"
 #include "tensor.cuh"
@@ -437,6 +442,7 @@ struct sdrt_ctx {
   double diag_vol = 0.0;     // sum_e detJ_e sum_r w_r
   double* d_cub = nullptr;   // cubature of the diagnostics: B [ncub][nsol], then weights [ncub]
   int ncub = 0;              // 0: solution-point quadrature
+  int nq1 = 0;               // tensor elements: cubature points per axis (1D factor stored after w)
   int cub_cap = 0;           // points reserved (the degree-10 rule)
   const int* d_tiles = nullptr;  // [n_int interior tiles][n_bnd boundary tiles]
   double* Tu[2] = {nullptr, nullptr};
@@ -649,7 +655,7 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   o += align256((3 * ((size_t)m.K / 8 + 2) + r.nsol + 8) * sizeof(double));
   // degree-10 cubature of the diagnostics (l.2075): interpolation matrix + weights
   p.off_cub = o;
-  o += align256((size_t)cub_points(r.etype, r.nd, 10) * (r.nsol + 1) * sizeof(double));
+  o += align256(((size_t)cub_points(r.etype, r.nd, 10) * (r.nsol + 1) + 64) * sizeof(double));  // + 1D factor
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -669,6 +675,15 @@ static void set_diag_rule(sdrt_ctx* c, int etype, int degree) {
   CUDA_OK(cudaMemcpy(c->d_cub, B.a.data(), B.a.size() * sizeof(double), cudaMemcpyHostToDevice));
   CUDA_OK(cudaMemcpy(c->d_cub + B.a.size(), w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice));
   c->ncub = (int)w.size();
+  c->nq1 = 0;
+  if (etype_tensor(etype)) {  // the 1D factor, after the weights (sum-factorised application)
+    std::vector<double> B1;
+    cubature_interp_1d(c->p, degree, B1);
+    if (B1.size() > 64) throw std::runtime_error("cubature 1D factor larger than reserved");
+    CUDA_OK(cudaMemcpy(c->d_cub + B.a.size() + w.size(), B1.data(), B1.size() * sizeof(double),
+                       cudaMemcpyHostToDevice));
+    c->nq1 = degree / 2 + 1;
+  }
 }
 
 extern "C" {
@@ -1748,7 +1763,9 @@ sdrt_status sdrt_diagnostics(sdrt_ctx* c, const double* d_U, double* d_out, void
       b.Uin = d_U;
       b.Tu = c->Tu[c->cur];
       tensor_launch_diag(c->nd, c->p, c->tg, c->line, c->ph, &c->tma, b, c->ncub ? c->d_cub + (size_t)c->ncub * c->nsol : c->d_w,
-                         c->ncub ? c->d_cub : nullptr, c->ncub, c->d_part, st);
+                         c->ncub ? c->d_cub : nullptr, c->ncub, c->d_part, st,
+                         c->ncub && c->nq1 && SDRT_DIAG_SF ? c->d_cub + (size_t)c->ncub * (c->nsol + 1) : nullptr,
+                         c->nq1);
       ntile = (c->g.K + tensor_tile_width(c->nd, c->p, c->eq) - 1) / tensor_tile_width(c->nd, c->p, c->eq);
     } else {
       sfused_traces(c, d_U, st);

@@ -1013,6 +1013,19 @@ static Operators simplex_operators(int etype, int p) {
 // the solution-basis interpolation B(q, r) = l_r(x_q).  Tensor: Gauss-Legendre products
 // with degree/2 + 1 points per axis; simplex: collapsed (Duffy) Gauss-Legendre products
 // with (degree + D - 1)/2 + 1 points per direction, mapped affinely (|det| 4 tri, 8 tet).
+// 1D factor of the tensor-element cubature interpolation: B1[q][t] = l_t(g_q), the
+// degree-p Lagrange basis on the p+1 Gauss-Legendre solution points at the degree/2+1
+// Gauss-Legendre cubature points, so that cubature_interp's B = B1 (x) B1 (x) B1 (x
+// fastest); row-major nq x (p+1)
+void cubature_interp_1d(int p, int degree, std::vector<double>& B1) {
+  std::vector<qd> g, gw, gs, gsw;
+  gauss_legendre(degree / 2 + 1, g, gw);
+  gauss_legendre(p + 1, gs, gsw);
+  B1.assign(g.size() * (p + 1), 0.0);
+  for (size_t q = 0; q < g.size(); ++q)
+    for (int t = 0; t <= p; ++t) B1[q * (p + 1) + t] = (double)lag(gs, t, g[q]);
+}
+
 void cubature_interp(int etype, int p, int degree, std::vector<double>& w, Mat& B) {
   if (etype == PRI) throw std::runtime_error("unsupported: diagnostics cubature on prisms");
   RefQ R = build_ref_q(etype, p);

@@ -55,6 +55,7 @@ Operators build_operators(int etype, int p, int scheme = 0);
 // Cubature exact to `degree` on the reference element (weights w) and the solution-basis
 // interpolation B(q, r) = l_r(x_q) (TGV diagnostics, l.2075).
 void cubature_interp(int etype, int p, int degree, std::vector<double>& w, Mat& B);
+void cubature_interp_1d(int p, int degree, std::vector<double>& B1);
 
 // Reference vertices of the simplices (x~ of vertex k), used by mesh code.
 void simplex_ref_vertices(int etype, std::vector<std::array<double, 3>>& V);

@@ -55,6 +55,11 @@
 #ifndef SDRT_TA_AUNI
 #define SDRT_TA_AUNI 0
 #endif
+// sum-factorised diagnostics: elements per pass for p <= 3 (38.4 KB of shared memory per
+// element at p = 3; p = 4 takes one element per pass)
+#ifndef SDRT_DIAG_G
+#define SDRT_DIAG_G 1
+#endif
 // kernel A gradient through the composite per-axis operator Line1D::Gq (GradNb): 1 on, 0 the
 // step-by-step form (own traces, common values, U_int, then Dfl)
 #ifndef SDRT_TA_GQ
@@ -1443,10 +1448,62 @@ __device__ __forceinline__ void block_sum3(double (&a)[3], double* red, double* 
     for (int k = 0; k < 3; ++k) out[k] = red[k * NT];
 }
 
+// Degree-10 cubature of one element (tensor, 3-D) applied sum-factorised through the 1D
+// factor B1 [nq][n] of Bq = B1 (x) B1 (x) B1 (x fastest; refel.cpp cubature_interp_1d):
+// per component c (u_v, then q[j][v]), Y1 = B1 along x, Y2 = B1 along y (shared memory),
+// then every cubature point contracts along z and evaluates the integrands -- the same
+// polynomial values as the dense Bq rows, 3 (nq n^3 + ...) instead of
+// nq^3 n^3 multiply-adds per component.  Returns nothing; accumulates into acc.
+template <int D, int P, int NV, int E, int NT, int G>
+__device__ __forceinline__ void tgv_element_sf(const PhysDev& ph, const double* sU, const double* sQ,
+                                               const double* sB1, int nq, const double* __restrict__ w,
+                                               double detj, int el0, int ng, double* sY1, double* sY2,
+                                               double (&acc)[3]) {
+  // G element slots el0 .. el0 + ng - 1 at a time (element slot fastest in every item)
+  constexpr int n = P + 1, NS = n * n * n, NC = NV + D * NV;
+  auto X = [&](int c, int s, int el) {  // component c at solution point s of element el
+    return c < NV ? sU[(s * NV + c) * E + el] : sQ[(((c - NV) / NV * NS + s) * NV + (c - NV) % NV) * E + el];
+  };
+  // Y1[c][rz][ry][qx][g] = sum_rx B1[qx][rx] X_c(rx, ry, rz)
+  for (int it = threadIdx.x; it < NC * n * n * nq * G; it += NT) {
+    const int gi = it % G, r0 = it / G, qx = r0 % nq, r = r0 / nq, ry = r % n, r2 = r / n, rz = r2 % n, c = r2 / n;
+    if (gi >= ng) continue;
+    double a = 0.0;
+#pragma unroll
+    for (int rx = 0; rx < n; ++rx) a = fma(sB1[qx * n + rx], X(c, rx + n * (ry + n * rz), el0 + gi), a);
+    sY1[it] = a;
+  }
+  __syncthreads();
+  // Y2[c][rz][qy][qx][g] = sum_ry B1[qy][ry] Y1[c][rz][ry][qx][g]
+  for (int it = threadIdx.x; it < NC * n * nq * nq * G; it += NT) {
+    const int gi = it % G, r0 = it / G, qx = r0 % nq, r = r0 / nq, qy = r % nq, r2 = r / nq, rz = r2 % n, c = r2 / n;
+    if (gi >= ng) continue;
+    double a = 0.0;
+#pragma unroll
+    for (int ry = 0; ry < n; ++ry) a = fma(sB1[qy * n + ry], sY1[(((c * n + rz) * n + ry) * nq + qx) * G + gi], a);
+    sY2[it] = a;
+  }
+  __syncthreads();
+  // every cubature point (qx, qy, qz) of every element: contract along z, then the integrands
+  for (int it = threadIdx.x; it < nq * nq * nq * G; it += NT) {
+    const int gi = it % G, q = it / G, qx = q % nq, qy = (q / nq) % nq, qz = q / (nq * nq);
+    if (gi >= ng) continue;
+    double v[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      double a = 0.0;
+#pragma unroll
+      for (int rz = 0; rz < n; ++rz) a = fma(sB1[qz * n + rz], sY2[((((c * n + rz) * nq + qy) * nq + qx)) * G + gi], a);
+      v[c] = a;
+    }
+    tgv_point<D, NV>(ph, v, v + NV, __ldg(w + q) * detj, acc);
+  }
+}
+
 template <int D, int P, int EQ, int E, int NT, int NI>
 __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, const double* w,
                                               const double* Bq, int nq, double* part,
-                                              const __grid_constant__ TileMaps tm) {
+                                              const __grid_constant__ TileMaps tm, const double* B1, int nq1) {
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, NS = T::NS;
@@ -1474,8 +1531,25 @@ __global__ void __launch_bounds__(NT) kt_diag(TensorGeom g, Line1D L, PhysDev ph
   }
   __syncthreads();
   double acc[3] = {0.0, 0.0, 0.0};
-  if constexpr (NV == D + 2)
+  if constexpr (NV == D + 2 && D == 3) {
+    if (B1) {  // sum-factorised cubature, one element at a time
+      __shared__ double sB1[64];
+      for (int i = threadIdx.x; i < nq1 * (P + 1); i += NT) sB1[i] = B1[i];
+      constexpr int G = P >= 4 ? 1 : SDRT_DIAG_G;  // elements per pass (shared-memory bound)
+      double* sY1 = sQ + D * NS * NV * E;
+      double* sY2 = sY1 + (NV + D * NV) * (P + 1) * (P + 1) * 6 * G;
+      __syncthreads();
+      for (int el = 0; el < E; el += G) {
+        if (e0 + el >= g.K) break;
+        const int ng = (int)(g.K - (e0 + el) < G ? g.K - (e0 + el) : G);
+        tgv_element_sf<D, P, NV, E, NT, G>(ph, sU, sQ, sB1, nq1, w, g.detJ, el, ng, sY1, sY2, acc);
+      }
+    } else {
+      tgv_tile<D, NV, E, NS>(ph, sU, sQ, w, Bq, nq, e0, g.K, [&](int) { return g.detJ; }, acc);
+    }
+  } else if constexpr (NV == D + 2) {
     tgv_tile<D, NV, E, NS>(ph, sU, sQ, w, Bq, nq, e0, g.K, [&](int) { return g.detJ; }, acc);
+  }
   block_sum3<NT>(acc, red, part + 3 * blockIdx.x);
 }
 
@@ -1620,13 +1694,17 @@ static void run_traces(const TensorGeom& g, const Line1D& L, TensorTma* tma, con
 
 template <int D, int P, int EQ>
 static void run_diag(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
-                     const double* w, const double* Bq, int nq, double* part, cudaStream_t st) {
+                     const double* w, const double* Bq, int nq, double* part, cudaStream_t st, const double* B1,
+                     int nq1) {
   using C = TCfg<D, P, EQ>;
   const unsigned grid = (unsigned)((g.K + C::E - 1) / C::E);
   auto k = L.fr ? kt_diag<D, P, EQ, C::E, 256, P + 1> : kt_diag<D, P, EQ, C::E, 256, P>;
-  const size_t sm = C::TILE * (1 + D);
+  if (B1 && nq1 > 6) B1 = nullptr;  // the shared-memory buffers are sized for degree <= 10
+  constexpr int NC = C::NV + D * C::NV, n = P + 1;
+  constexpr int G = P >= 4 ? 1 : SDRT_DIAG_G;
+  const size_t sm = C::TILE * (1 + D) + (size_t)NC * n * 6 * (n + 6) * G * sizeof(double);
   set_smem<D, P, EQ>((const void*)k, sm);
-  k<<<grid, 256, sm, st>>>(g, L, ph, b, w, Bq, nq, part, maps_for(tma, b, false));
+  k<<<grid, 256, sm, st>>>(g, L, ph, b, w, Bq, nq, part, maps_for(tma, b, false), B1, nq1);
 }
 
 template <int D, int P, int EQ>
@@ -1731,13 +1809,13 @@ void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D&
 
 void tensor_launch_diag(int D, int P, const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
                         const TensorBufs& b, const double* w, const double* Bq, int nq, double* part,
-                        cudaStream_t st) {
+                        cudaStream_t st, const double* B1, int nq1) {
   if (D != 3) throw std::runtime_error("unsupported: TGV diagnostics need a 3-D NS context");
   switch (P) {
-    case 1: run_diag<3, 1, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
-    case 2: run_diag<3, 2, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
-    case 3: run_diag<3, 3, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
-    default: run_diag<3, 4, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st); break;
+    case 1: run_diag<3, 1, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st, B1, nq1); break;
+    case 2: run_diag<3, 2, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st, B1, nq1); break;
+    case 3: run_diag<3, 3, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st, B1, nq1); break;
+    default: run_diag<3, 4, EQ_NS>(g, L, ph, tma, b, w, Bq, nq, part, st, B1, nq1); break;
   }
 }
 

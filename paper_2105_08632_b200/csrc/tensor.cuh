@@ -91,8 +91,10 @@ void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D&
 bool tensor_supported(int D, int P, int eq);
 // TGV diagnostics partial sums (3 per tile: rho v.v, S^d:S^d, p div v, solution-point
 // weighted); NS only
+// B1 (optional, with Bq): the nq1 x (P+1) 1D factor of Bq = B1 (x) B1 (x) B1, applied
+// sum-factorised (3 contractions of 4 x 6 instead of the dense 216 x 64 per component)
 void tensor_launch_diag(int D, int P, const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
                         const TensorBufs& b, const double* w, const double* Bq, int nq, double* part,
-                        cudaStream_t st);
+                        cudaStream_t st, const double* B1 = nullptr, int nq1 = 0);
 
 }  // namespace sdrt
