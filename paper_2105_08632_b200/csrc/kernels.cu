@@ -571,6 +571,14 @@ static void simplex_pack(const Operators& O, int D, std::vector<OpHostF>* out) {
   out->push_back(pack_frag(G));
   out->push_back(pack_frag(O.scheme != 0 ? O.Mc : O.M14));
   out->push_back(pack_frag(M13F));
+  // [M14 | M13 M19 P2] on [D~; F~] (inviscid kernel B: the whole divergence in one product)
+  const Mat& Mf = O.scheme != 0 ? O.Mc : O.M14;
+  Mat MF(ns, r.next + M13F.cols);
+  for (int s2 = 0; s2 < ns; ++s2) {
+    for (int e = 0; e < r.next; ++e) MF(s2, e) = Mf(s2, e);
+    for (int j = 0; j < M13F.cols; ++j) MF(s2, r.next + j) = M13F(s2, j);
+  }
+  out->push_back(pack_frag(MF));
 }
 
 static int nvars(int eq, int D) { return (eq == SDRT_EQ_LINADV || eq == SDRT_EQ_LINADVDIFF) ? 1 : D + 2; }
@@ -967,8 +975,8 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
       std::vector<OpHostF> s4;
       simplex_pack(O, m.nd, &s4);
       size_t so = p.off_sops;
-      SOpF* dst[5] = {&c->sops.M0, &c->sops.M12, &c->sops.G, &c->sops.M14, &c->sops.M13F};
-      for (int i = 0; i < 5; ++i) {
+      SOpF* dst[6] = {&c->sops.M0, &c->sops.M12, &c->sops.G, &c->sops.M14, &c->sops.M13F, &c->sops.M14F};
+      for (int i = 0; i < 6; ++i) {
         OpHostF& h = s4[i];
         double* dval = (double*)(base + so);
         CUDA_OK(cudaMemcpyAsync(dval, h.frag.data(), h.frag.size() * sizeof(double), cudaMemcpyHostToDevice, st));

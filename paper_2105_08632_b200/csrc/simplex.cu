@@ -63,6 +63,8 @@ struct SDims {
   static constexpr int kt_F = (D * nu + 3) / 4;          // M13 M19 P2
   static constexpr int kt_GF = (next + nsol + 3) / 4;    // FR-SDRT [M16 | Dsol - M16 M0]
   static constexpr int kt_FF = (D * nsol + 3) / 4;       // FR-SDRT divergence on F[s][d]
+  static constexpr int kt_EF = (next + D * nu + 3) / 4;   // [M14 | M13F]
+  static constexpr int kt_EFF = (next + D * nsol + 3) / 4;  // FR-SDRT [M14 | M13F]
 };
 
 template <typename T>
@@ -123,6 +125,10 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #endif
 #ifndef SDRT_SB_NT
 #define SDRT_SB_NT 160
+#endif
+// inviscid kernel B: the divergence as one [M14 | M13F] product (1) or two (0)
+#ifndef SDRT_SB_ONEPRODUCT
+#define SDRT_SB_ONEPRODUCT 1
 #endif
 #ifndef SDRT_SB_MINB_OSF
 #define SDRT_SB_MINB_OSF 4
@@ -1010,11 +1016,18 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   SPH(1, 2)
   // R~ = R_int + M14 D~ [+ M13 M19 P2 F~]
   if constexpr (INT) {
+#if SDRT_SB_ONEPRODUCT
+    // one product [M14 | M13F] on [D~; F~] (no intermediate barrier or accumulate pass)
+    if (O.fr) dmm1<NV, S::kt_EFF, E, false>(O.M14F, sUe, S::next, sF, sR);
+    else dmm1<NV, S::kt_EF, E, false>(O.M14F, sUe, S::next, sF, sR);
+  SPH(1, 3)
+#else
     dmm1<NV, S::kt_ext, E, false>(O.M14, sUe, 1 << 30, sUe, sR);
     __syncthreads();
   SPH(1, 3)
     if (O.fr) dmm1<NV, S::kt_FF, E, true>(O.M13F, sF, 1 << 30, sF, sR);
     else dmm1<NV, S::kt_F, E, true>(O.M13F, sF, 1 << 30, sF, sR);
+#endif
   } else {
     dmm1<NV, S::kt_ext, E, true>(O.M14, sUe, 1 << 30, sUe, sR);
   }

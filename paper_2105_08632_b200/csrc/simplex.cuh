@@ -29,6 +29,7 @@ struct SimplexOps {
   SOpF M14;   // N_sol x N_ext
   SOpF M13F;  // N_sol x (D N_u): M13 M19 P2, columns (d, u)
               //   FR-SDRT: N_sol x (D N_sol), Dsol - M14 (n^ . M0), columns (d, s)
+  SOpF M14F;  // [M14 | M13F]: the whole divergence on [D~; F~] (inviscid kernel B)
   int fr;     // 1: FR-SDRT (NEXT row N1), fluxes at the solution points
 };
 
