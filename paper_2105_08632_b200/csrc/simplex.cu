@@ -126,6 +126,13 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SB_NT
 #define SDRT_SB_NT 160
 #endif
+// kernel B: the RK update as the epilogue of the last divergence product (1) or a separate
+// pass over the R~ tile after a barrier (0).  Measured: c5 kernel B 1.47 -> 1.74 ms, c2
+// 16.1 -> 11.6 GDOF-stage/s with the epilogue -- the product has only N_sol/8 x 1 warp
+// jobs (3 for tet p = 3), so the RK update of the tile lands on 3 of the CTA's warps: off
+#ifndef SDRT_SB_EPI
+#define SDRT_SB_EPI 0
+#endif
 // inviscid kernel B: the divergence as one [M14 | M13F] product (1) or two (0)
 #ifndef SDRT_SB_ONEPRODUCT
 #define SDRT_SB_ONEPRODUCT 1
@@ -230,6 +237,91 @@ __device__ __forceinline__ void dmm1(const SOpF& M, const double* X0, int split,
   using DM = Dmm<W, E, KT, YS, XR>;
   const int nj = DM::jobs(M);
   for (int j = warp; j < nj; j += nw) DM::template job<ACC>(M, j, X0, split, X1, Y);
+}
+
+// Y = M X (+ Yacc) with the result handed to an epilogue per lane output pair instead of
+// shared memory: epi(r, n, y_n, y_n+1) for row r and the even column n (fused GEMM
+// epilogue: the RK update runs on the product's registers, one barrier and the R~ tile
+// round trip fewer)
+template <int W, int KT, int E, bool ACC, class Epi>
+__device__ __forceinline__ void dmm1_epi(const SOpF& M, const double* X0, int split, const double* X1,
+                                         const double* Yacc, Epi&& epi) {
+  using DM = Dmm<W, E, KT>;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int j = warp; j < DM::jobs(M); j += nw) {
+    const int m = j / DM::NG, ng = j % DM::NG;
+    const int n0 = ng * DM::NGR * 8 + (lane >> 2);
+    const unsigned km = M.kmask ? __ldg(M.kmask + m) : 0xffffffffu;
+    const double* af = M.frag + (int64_t)m * KT * 32 + lane;
+    double a[KT];
+#pragma unroll
+    for (int k = 0; k < KT; ++k) a[k] = (km >> k & 1u) ? __ldg(af + k * 32) : 0.0;
+    double c[DM::NGR][2];
+#pragma unroll
+    for (int q = 0; q < DM::NGR; ++q) c[q][0] = c[q][1] = 0.0;
+#pragma unroll
+    for (int k = 0; k < KT; ++k) {
+      if (!(km >> k & 1u)) continue;
+      const int col = 4 * k + (lane & 3);
+      const double* xr = col < split ? X0 + col * DM::N : X1 + (col - split) * DM::N;
+      const bool ok = col < M.cols;
+#pragma unroll
+      for (int q = 0; q < DM::NGR; ++q) dmma(c[q][0], c[q][1], a[k], ok ? xr[n0 + 8 * q] : 0.0);
+    }
+    const int r = 8 * m + (lane >> 2);
+    if (r < M.rows) {
+#pragma unroll
+      for (int q = 0; q < DM::NGR; ++q) {
+        const int n = ng * DM::NGR * 8 + 8 * q + 2 * (lane & 3);
+        double y0 = c[q][0], y1 = c[q][1];
+        if (ACC) {
+          const double2 o = *reinterpret_cast<const double2*>(Yacc + r * DM::N + n);
+          y0 = o.x + y0;
+          y1 = o.y + y1;
+        }
+        epi(r, n, y0, y1);
+      }
+    }
+  }
+}
+
+// RK update of one value (rk.cuh stage codes): kk = dU/dt, idx its tile entry, gi its
+// global entry; returns the new stage value (0 for the residual-only stage -1)
+__device__ __forceinline__ double rk_value(const SimplexBufs& b, int stage, double dt, double kk, int64_t gi,
+                                           const double* sU, const double* sAcc, const double* sUn, int idx) {
+  double nu;
+  switch (stage) {
+    case -1: b.out[gi] = kk; nu = 0.0; break;
+    case 0: {
+      const double u0 = sU[idx];
+      b.ACC[gi] = fma(dt / 6.0, kk, u0);
+      nu = fma(0.5 * dt, kk, u0);
+      b.Us[gi] = nu;
+    } break;
+    case 1:
+      b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+      nu = fma(0.5 * dt, kk, sUn[idx]);
+      b.Us[gi] = nu;
+      break;
+    case 2:
+      b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
+      nu = fma(dt, kk, sUn[idx]);
+      b.Us[gi] = nu;
+      break;
+    case 3:
+      nu = fma(dt / 6.0, kk, sAcc[idx]);
+      b.U[gi] = nu;
+      break;
+    default: {  // RK54 stage s (2N-storage, in place)
+      const int s5 = stage - RK54_STAGE0;
+      const double du = s5 == 0 ? dt * kk : fma(rk54_a(s5), sAcc[idx], dt * kk);
+      b.ACC[gi] = du;
+      nu = fma(rk54_b(s5), du, sU[idx]);
+      b.U[gi] = nu;
+    } break;
+  }
+  return nu;
 }
 
 // the same operator on the ND row blocks of a [nd][rows][W][E] tile (block stride XS
@@ -1014,6 +1106,31 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
   mbar_wait(&bar[1], 0);  // R_int and the RK registers have landed
   __syncthreads();
   SPH(1, 2)
+#if SDRT_SB_EPI && SDRT_SB_ONEPRODUCT
+  // R~ = [M14 | M13F][D~; F~] (inviscid) or R_int + M14 D~, -R~/detJ and the RK update
+  // as the product's epilogue (l.2919-2925, l.347-350)
+  auto rk_epi = [&](int r, int n, double y0, double y1) {
+    const int v = n / E, el = n % E;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = (r * NV + v) * E + el + h;
+      const int64_t e = e0 + el + h;
+      if (e >= g.K) {
+        sU[idx] = 0.0;
+        continue;
+      }
+      const double kk = -(h ? y1 : y0) / g.detJ[sNb[D + 1][el + h]];
+      sU[idx] = rk_value(b, stage, dt, kk, (int64_t)(r * NV + v) * g.Kp + e, sU, sAcc, sUn, idx);
+    }
+  };
+  if constexpr (INT) {
+    if (O.fr) dmm1_epi<NV, S::kt_EFF, E, false>(O.M14F, sUe, S::next, sF, nullptr, rk_epi);
+    else dmm1_epi<NV, S::kt_EF, E, false>(O.M14F, sUe, S::next, sF, nullptr, rk_epi);
+  } else {
+    dmm1_epi<NV, S::kt_ext, E, true>(O.M14, sUe, 1 << 30, sUe, sR, rk_epi);
+  }
+  SPH(1, 4)
+#else
   // R~ = R_int + M14 D~ [+ M13 M19 P2 F~]
   if constexpr (INT) {
 #if SDRT_SB_ONEPRODUCT
@@ -1077,6 +1194,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB) ks_stage(GeomDev g, 
     }
     sU[idx] = nu;
   }
+#endif
   if (stage < 0) return;
   __syncthreads();
   SPH(1, 5)
@@ -1166,6 +1284,23 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB_OSF) ks_stage_osf(Geo
   }
   mbar_wait(&bar, 0);
   __syncthreads();
+#if SDRT_SB_EPI
+  // R~ = R_int + M14 D~ with the RK update as the product's epilogue (l.2919-2925, l.347-350)
+  dmm1_epi<NV, S::kt_ext, E, true>(O.M14, sD, 1 << 30, sD, sR, [&](int r, int n, double y0, double y1) {
+    const int v = n / E, el = n % E;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = (r * NV + v) * E + el + h;
+      const int64_t e = e0 + el + h;
+      if (e >= g.K) {
+        sU[idx] = 0.0;
+        continue;
+      }
+      const double kk = -(h ? y1 : y0) / g.detJ[sNb[D + 1][el + h]];
+      sU[idx] = rk_value(b, stage, dt, kk, (int64_t)(r * NV + v) * g.Kp + e, sU, sAcc, sUn, idx);
+    }
+  });
+#else
   dmm1<NV, S::kt_ext, E, true>(O.M14, sD, 1 << 30, sD, sR);  // R~ = R_int + M14 D~
   __syncthreads();
   for (int idx = threadIdx.x; idx < S::nsol * NV * E; idx += NT) {
@@ -1211,6 +1346,7 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB_OSF) ks_stage_osf(Geo
     }
     sU[idx] = nu;
   }
+#endif
   if (stage < 0) return;
   __syncthreads();
   // traces of the new state M0 U at the right-side faces only (point-major)
