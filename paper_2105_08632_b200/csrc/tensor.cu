@@ -60,6 +60,12 @@
 #ifndef SDRT_DIAG_G
 #define SDRT_DIAG_G 1
 #endif
+// OSF kernel B: R_int and u_n read from global memory in the update (1) or staged by TMA (0).
+// Measured on c4: 147 us (direct, three CTAs per SM) vs 97 us (TMA, two): the TMA tiles are
+// requested at the CTA start and land while the flux gather runs; off
+#ifndef SDRT_TB_DIRECT
+#define SDRT_TB_DIRECT 0
+#endif
 // kernel A gradient through the composite per-axis operator Line1D::Gq (GradNb): 1 on, 0 the
 // step-by-step form (own traces, common values, U_int, then Dfl)
 #ifndef SDRT_TA_GQ
@@ -1307,8 +1313,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
   constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
   extern __shared__ __align__(128) double smem[];
   const bool need_in = stage == 0 || stage >= RK54_STAGE0;
-  double* sR = smem;                    // R_int (kernel A)
-  double* sF = sR + NS * NV * E;        // [D][NL][NV][E] left neighbours' F at the x_d = -1 faces
+  // SDRT_TB_DIRECT: R_int and u_n are read straight from global memory in the update (one
+  // read per value, coalesced rows of E elements) instead of being staged by TMA, so the
+  // CTA needs 55 KB of shared memory instead of 95 KB (3 CTAs per SM in every stage)
+  constexpr bool DIRECT = SDRT_TB_DIRECT != 0;
+  double* sR = smem;                                  // R_int (kernel A); unused if DIRECT
+  double* sF = sR + (DIRECT ? 0 : NS * NV * E);       // [D][NL][NV][E] left neighbours' F (x_d = -1 faces)
   double* sU = sF + D * NL * NV * E;    // new state (stage input first where the RK formula reads it)
   double* sAcc = sU + NS * NV * E;
   double* sUn = sAcc + (stage_reads_acc(stage) ? NS * NV * E : 0);
@@ -1319,11 +1329,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_fence_init();
-    const unsigned bytes = TB * (1 + (need_in ? 1 : 0) + (stage_reads_un(stage) ? 1 : 0) + (stage_reads_acc(stage) ? 1 : 0));
+    const unsigned bytes = TB * ((DIRECT ? 0 : 1) + (need_in ? 1 : 0) + (!DIRECT && stage_reads_un(stage) ? 1 : 0) +
+                                 (stage_reads_acc(stage) ? 1 : 0));
     mbar_expect_tx(&bar, bytes);
-    tma_tile<NS * NV, E>(sR, &tm.rv, e0, &bar);
+    if (!DIRECT) tma_tile<NS * NV, E>(sR, &tm.rv, e0, &bar);
     if (need_in) tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar);
-    if (stage_reads_un(stage)) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar);
+    if (!DIRECT && stage_reads_un(stage)) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar);
     if (stage_reads_acc(stage)) tma_tile<NS * NV, E>(sAcc, &tm.acc, e0, &bar);
   }
   fill_nbrs<D, E>(g, sNb, e0);
@@ -1370,7 +1381,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
     for (int i = 0; i < n; ++i) {
       const int idx = ((p0 + i) * NV + v) * E + el;
       const int64_t gi = (int64_t)((p0 + i) * NV + v) * g.Kp + e;
-      double R = fma(L.Dfl[i][0], fx, sR[idx]);
+      double R = fma(L.Dfl[i][0], fx, DIRECT ? b.Rv[gi] : sR[idx]);
       R = fma(cy, F(1, D == 3 ? i + n * k : i), R);
       if constexpr (D == 3) R = fma(cz, F(2, i + n * j), R);
       const double kk = -R * idet;
@@ -1388,12 +1399,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
         } break;
         case 1:
           b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
-          nu = fma(0.5 * dt, kk, sUn[idx]);
+          nu = fma(0.5 * dt, kk, DIRECT ? b.U[gi] : sUn[idx]);
           b.Us[gi] = nu;
           break;
         case 2:
           b.ACC[gi] = fma(dt / 3.0, kk, sAcc[idx]);
-          nu = fma(dt, kk, sUn[idx]);
+          nu = fma(dt, kk, DIRECT ? b.U[gi] : sUn[idx]);
           b.Us[gi] = nu;
           break;
         case 3:
@@ -1595,6 +1606,7 @@ struct TCfg {
   // kernel B, one-sided flux publication: R_int, the x_d = -1 face fluxes, the state tile
   // (stage input where read) and the RK registers the stage reads
   static size_t smem_b_osf(int stage) {
+    if (SDRT_TB_DIRECT) return TILE + (size_t)D * NL * NV * E * sizeof(double) + (stage_reads_acc(stage) ? TILE : 0);
     return TILE * 2 + (size_t)D * NL * NV * E * sizeof(double) + (stage_reads_acc(stage) ? TILE : 0) +
            (stage_reads_un(stage) ? TILE : 0);
   }
@@ -1660,7 +1672,8 @@ static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph
     if (grid == 0) return;
     if constexpr (EQ == EQ_NS) {
       if (g.osf) {
-        auto kb = b.Fexp ? kt_stage_osf<D, P, EQ, C::E, C::NTB, C::MINB_B, true> : kt_stage_osf<D, P, EQ, C::E, C::NTB, C::MINB_B>;
+        constexpr int MB = SDRT_TB_DIRECT ? 3 : C::MINB_B;
+        auto kb = b.Fexp ? kt_stage_osf<D, P, EQ, C::E, C::NTB, MB, true> : kt_stage_osf<D, P, EQ, C::E, C::NTB, MB>;
         set_smem<D, P, EQ>((const void*)kb, C::smem_b_osf(2));
         CUDA_LAUNCH_OK(launch_pdl(kb, grid, C::NTB, C::smem_b_osf(stage), st, g, L, ph, b, stage, dt, maps_for(tma, b, true)));
         return;
