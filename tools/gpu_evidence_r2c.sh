@@ -4,7 +4,7 @@
 # the ncu launch list of the default bench command, SASS / DMMA / DRAM counters of the
 # fused kernels (-> profiles/r02_sass_counts.json via tools/sass_counts.py) and ncu
 # --set full summaries of the two kernels of c4 and c5 (reports removed: 64 MiB cap).
-O=gpurun_out/r2c; mkdir -p $O
+O=${O:-gpurun_out/r2c}; mkdir -p $O
 git_commit=$(cat .commit 2>/dev/null)
 if [ "$PART" != prof ]; then
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
