@@ -121,6 +121,8 @@ def kernel_bytes(cfg, K):
         out["tensor_grad(A)"] = out["simplex_grad(A)"] = b * (ns + ne // 2 + ne // 2)
         out["tensor_stage(B)"] = b * (3.25 * ns + ne // 2 + ne // 2)
         out["simplex_stage(B)"] = b * (3.25 * ns + ne + ne // 2)
+    # fused RK stage (kernel A + kernel B in one launch, SDRT_FUSE=1): both kernels' arrays
+    out["tensor_fused(A+B)"] = out["tensor_grad(A)"] + out["tensor_stage(B)"]
     return out
 
 
@@ -503,6 +505,8 @@ def main():
             if kn.startswith("tensor_") and kn in kf:
                 kf[kn] = v["flops_per_launch"]
                 flops_source = f"ncu SASS counts (profiles/{SASS_COUNTS}) for the tensor kernels"
+    if "tensor_grad(A)" in kf and "tensor_stage(B)" in kf:  # the fused launch runs both kernels' work
+        kf["tensor_fused(A+B)"] = kf["tensor_grad(A)"] + kf["tensor_stage(B)"]
     t_launch = dom_ms / dom_n * 1e-3 if dom else None
     gbs = kb[dom] / t_launch / 1e9 if dom in kb else None
     tfs = kf[dom] / t_launch / 1e12 if dom in kf else None

@@ -371,7 +371,7 @@ static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 struct Plan {
   size_t off_uext, off_xg, off_q, off_qext, off_qu, off_xd, off_r, off_us, off_acc, off_ops, off_xm,
       off_bad, off_tu0, off_tu1, off_tg, off_sops, off_halo, halo_entries, off_ff, off_tiles, off_diag, off_cub,
-      total;
+      off_fuse, total;
   size_t ops_bytes;
 };
 
@@ -408,12 +408,13 @@ static void build_ops(const Operators& O, int D, Mat ops[5]) {
 using namespace sdrt;
 
 enum KTag { T_M0 = 0, T_M12, T_CV, T_GRAD, T_METRIC, T_QEXT, T_QU, T_IFLUX, T_FFLUX, T_DIV, T_RK,
-            T_TRACE, T_FA, T_FB, T_STRACE, T_SA, T_SB, T_NTAGS };
+            T_TRACE, T_FA, T_FB, T_STRACE, T_SA, T_SB, T_FAB, T_NTAGS };
 static const char* KTAG_NAMES[T_NTAGS] = {"interp_ext(M0)", "interp_int(M12)", "common_value", "gradient(M16|M15P)",
                                           "metric_grad", "grad_interp_ext(M5)", "grad_interp_int(M18)",
                                           "int_flux", "face_flux", "divergence(M14|M13M19P2)", "rk_update",
                                           "tensor_traces", "tensor_grad(A)", "tensor_stage(B)",
-                                          "simplex_traces", "simplex_grad(A)", "simplex_stage(B)"};
+                                          "simplex_traces", "simplex_grad(A)", "simplex_stage(B)",
+                                          "tensor_fused(A+B)"};
 
 struct sdrt_ctx {
   bool timing = false;
@@ -473,6 +474,9 @@ struct sdrt_ctx {
   // the mesh is cut into `slabs` z-ranges; kernel A of slab k and kernel B of other
   // slabs run concurrently on two streams, ordered by per-slab events (fused_steps_slabs)
   int slabs = 0;
+  // fused RK stage (tensor.cu kt_fused): kernel A + kernel B in one persistent launch
+  bool fuse = false;
+  FuseSched fsd{};
   int slab_tile[17] = {};     // first tile of slab k (slab_tile[slabs] = number of tiles)
   const int* d_iota = nullptr;  // tile ids 0 .. ntiles-1 (slab k = d_iota + slab_tile[k])
   cudaStream_t sA = nullptr, sB = nullptr;
@@ -664,6 +668,10 @@ static Plan make_plan(const Mesh& m, const Operators& O, const sdrt_physics* ph,
   // degree-10 cubature of the diagnostics (l.2075): interpolation matrix + weights
   p.off_cub = o;
   o += align256(((size_t)cub_points(r.etype, r.nd, 10) * (r.nsol + 1) + 64) * sizeof(double));  // + 1D factor
+  // fused RK stage (tensor path, tiles of >= 8 elements): job list (2 per tile),
+  // dependency table (FUSE_DEPS per tile), per-tile flags, 4 counters
+  p.off_fuse = o;
+  if (etype_tensor(m.etype) && ph->eq == EQ_NS) o += align256((((size_t)m.K / 8 + 2) * (3 + FUSE_DEPS) + 4) * sizeof(int32_t));
   p.total = o;
   if (packed) *packed = pk;
   return p;
@@ -1077,6 +1085,35 @@ sdrt_status sdrt_ctx_create(const sdrt_mesh* mm, const sdrt_operators* oo, const
         CUDA_OK(cudaEventCreateWithFlags(&c->evEnd, cudaEventDisableTiming));
       }
     }
+    // fused RK stage (kt_fused): 3-D fused tensor NS path with one-sided flux publication
+    // on one periodic rank, SDRT operators; SDRT_FUSE=1 enables it, SDRT_FUSE_LAG = the lag
+    // in tiles between a B job's last dependency and its place in the job list (default
+    // 2 x the resident CTAs)
+    if (c->fused && c->tg.osf && !c->line.fr && !(m.halo[0] || m.halo[1] || m.halo[2]) && c->slabs == 0) {
+      const char* ev = std::getenv("SDRT_FUSE");
+      const int E = tensor_tile_width(m.nd, m.p, ph->eq);
+      const int nctas = (ev && ev[0] == '1' && E >= 8) ? tensor_fuse_ctas(m.nd, m.p, ph->eq) : 0;
+      if (nctas > 0) {
+        const char* el = std::getenv("SDRT_FUSE_LAG");
+        const int lag = el ? std::atoi(el) : 2 * nctas;
+        std::vector<int> jobs, deps;
+        if (tensor_fuse_plan(m.nd, m.Nloc, m.K, E, lag, &jobs, &deps)) {
+          const int64_t nt = (m.K + E - 1) / E;
+          int* fb = (int*)(base + p.off_fuse);
+          CUDA_OK(cudaMemcpyAsync(fb, jobs.data(), jobs.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+          CUDA_OK(cudaMemcpyAsync(fb + 2 * nt, deps.data(), deps.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+          int* ctr = fb + 2 * nt + FUSE_DEPS * nt;
+          CUDA_OK(cudaMemsetAsync(ctr, 0, (4 + nt) * sizeof(int), st));
+          c->fsd.jobs = fb;
+          c->fsd.deps = fb + 2 * nt;
+          c->fsd.ctr = ctr;
+          c->fsd.flags = (unsigned*)(ctr + 4);
+          c->fsd.njobs = (int)jobs.size();
+          c->fuse = true;
+          CUDA_OK(cudaStreamSynchronize(st));
+        }
+      }
+    }
     CUDA_OK(cudaStreamSynchronize(st));  // host vectors go out of scope
     *out = c;
     return SDRT_OK;
@@ -1310,6 +1347,14 @@ static void fused_stage(sdrt_ctx* c, const double* Uin, double* U, int stage, do
   b.Tg = c->Tg;
   b.Rv = c->R;
   b.Fexp = stage < 0 ? c->Fexp : nullptr;
+  if (c->fuse && stage >= 0 && !c->auto_halo) {
+    {
+      Mark mk(c, st, T_FAB);
+      tensor_launch_fused(c->nd, c->p, c->eq, c->tg, c->line, c->ph, &c->tma, b, stage, dt, c->fsd, st);
+    }
+    c->cur ^= 1;
+    return;
+  }
   if (c->visc) {
     {
       Mark mk(c, st, T_FA);

@@ -835,10 +835,13 @@ __device__ __forceinline__ void visc_line_dmma(const TensorGeom& g, const Line1D
 // Phases after the gradient: [publish g + F_v(d=0)] [div(0) + F_v(1)] [div(1) + F_v(2)]
 // [div(2)], with the internal-flux buffer double-buffered so each phase has work for
 // every thread.
-template <int D, int P, int EQ, int E, int NT, int MINB, int NI, bool OSF = false>
-__global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
-                                                    const __grid_constant__ TileMaps tm) {
-  pdl_wait();
+// Kernel A body for the tile starting at element e0 (kt_grad: one tile per CTA; kt_fused:
+// the A jobs of the persistent schedule).  bar: the CTA's TMA mbarrier, already
+// initialised when init == false; par: the phase parity this use waits for.
+template <int D, int P, int EQ, int E, int NT, int NI, bool OSF>
+__device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const TensorBufs& b,
+                                          const TileMaps& tm, int64_t e0, int (*sNb)[E], uint64_t* barp, bool init,
+                                          unsigned par) {
   PH_INIT
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
@@ -851,14 +854,13 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   double* sF = sQ + D * NS * NV * E;  // 2 x [NL][P][NV][E]
   // OSF: [D][NL][NV][E], the right neighbours' traces, then sface F at the x_d = +1 ends
   double* sP = sF + (DBUF ? 2 : 1) * NFB;
-  __shared__ int sNb[2 * D][E];
-  __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   if (threadIdx.x == 0) {  // the stage-input tile by TMA
-    mbar_init(&bar, 1);
-    mbar_fence_init();
-    mbar_expect_tx(&bar, NS * NV * E * 8);
-    tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar);
+    if (init) {
+      mbar_init(barp, 1);
+      mbar_fence_init();
+    }
+    mbar_expect_tx(barp, NS * NV * E * 8);
+    tma_tile<NS * NV, E>(sU, &tm.uin, e0, barp);
   }
   fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
     constexpr bool GPAIR = SDRT_TA_GPAIR == 1 || (SDRT_TA_GPAIR == 2 && Ph::NV == 1);
     std::conditional_t<GPAIR, GradNb2<D, P, EQ, E, NT, NI>, GradNb<D, P, EQ, E, NT, NI>> gn;
     gn.load(g, ph, b.Tu, sNb, e0);
-    mbar_wait(&bar, 0);
+    mbar_wait(barp, par);
     __syncthreads();
   PH(0, 1)
     gn.compute(g, L, ph, sU, sQ, e0, OSF ? sP : nullptr);
@@ -1043,6 +1045,16 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
     __syncthreads();
   PH(0, 3 + ph_)
   }
+}
+
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI, bool OSF = false>
+__global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
+                                                    const __grid_constant__ TileMaps tm) {
+  pdl_wait();
+  __shared__ int sNb[2 * D][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  grad_tile<D, P, EQ, E, NT, NI, OSF>(g, L, ph, b, tm, e0, sNb, &bar, true, 0);
 }
 
 // Kernel B: common fluxes at the line ends (Rusanov / upwind + the published viscous
@@ -1304,10 +1316,12 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
 // R~ = R_int + sum_d M14_(d,-) D~ in the RK update (l.2919-2925, l.347-350), and publishes
 // the x_d = -1 traces of the new state (the only traces kernel A reads with beta = 1/2).
 // The stage input is not read except where the RK formula needs it (RK4 stage 0, RK54).
-template <int D, int P, int EQ, int E, int NT, int MINB, bool FEXP = false>
-__global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
-                                                       double dt, const __grid_constant__ TileMaps tm) {
-  pdl_wait();
+// Kernel B (OSF) body for the tile starting at element e0 (kt_stage_osf: one tile per
+// CTA; kt_fused: the B jobs of the persistent schedule); bar / init / par as grad_tile.
+template <int D, int P, int EQ, int E, int NT, bool FEXP>
+__device__ __forceinline__ void stage_osf_tile(const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                                               const TensorBufs& b, int stage, double dt, const TileMaps& tm,
+                                               int64_t e0, int (*sNb)[E], uint64_t* barp, bool init, unsigned par) {
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, n = T::n, NL = T::NL, NS = T::NS;
@@ -1322,13 +1336,13 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
   double* sU = sF + D * NL * NV * E;    // new state (stage input first where the RK formula reads it)
   double* sAcc = sU + NS * NV * E;
   double* sUn = sAcc + (stage_reads_acc(stage) ? NS * NV * E : 0);
-  __shared__ int sNb[2 * D][E];
-  __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   constexpr unsigned TB = NS * NV * E * 8;
+  uint64_t& bar = *barp;
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    mbar_fence_init();
+    if (init) {
+      mbar_init(&bar, 1);
+      mbar_fence_init();
+    }
     const unsigned bytes = TB * ((DIRECT ? 0 : 1) + (need_in ? 1 : 0) + (!DIRECT && stage_reads_un(stage) ? 1 : 0) +
                                  (stage_reads_acc(stage) ? 1 : 0));
     mbar_expect_tx(&bar, bytes);
@@ -1350,7 +1364,7 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
   }
   asm volatile("cp.async.commit_group;");
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  mbar_wait(&bar, 0);
+  mbar_wait(&bar, par);
   __syncthreads();
   if constexpr (FEXP) {  // O28 export (residual only): F at the own x_d = -1 ext points
     for (int item = threadIdx.x; item < D * NL * NV * E; item += NT) {
@@ -1436,6 +1450,117 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
 #pragma unroll
     for (int i = 0; i < n; ++i) u[i] = sU[((lb + i * ls) * NV + v) * E + el];
     b.Tu_next[((int64_t)((2 * d) * NL + t) * NV + v) * g.Kt + e] = interp_end<n>(L.Iend[0], u);
+  }
+}
+
+template <int D, int P, int EQ, int E, int NT, int MINB, bool FEXP = false>
+__global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
+                                                       double dt, const __grid_constant__ TileMaps tm) {
+  pdl_wait();
+  __shared__ int sNb[2 * D][E];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  stage_osf_tile<D, P, EQ, E, NT, FEXP>(g, L, ph, b, stage, dt, tm, e0, sNb, &bar, true, 0);
+}
+
+// Fused RK stage: kernel A and kernel B (OSF) of one stage as the jobs of ONE persistent
+// launch (FuseSched, tensor.cuh).  A job = grad_tile on one tile, then a release of the
+// tile's flag; B job = acquire the flags of the tiles it reads (its own R_int and the
+// published common fluxes of its x_d = -1 neighbours), then stage_osf_tile.  Jobs are taken
+// in list order from an atomic ticket, and every dependency of a B job is an A job earlier
+// in the list, so a waiting CTA only waits for A jobs that running CTAs already hold (A
+// jobs never wait): no deadlock whatever the number of resident CTAs.  Per element the
+// arithmetic is exactly kernel A's and kernel B's, so the stage is bitwise the two-kernel
+// one; R_int is read back a few hundred tiles after it was written (L2, not HBM), and the
+// B jobs' HBM streams overlap the A jobs' shared-memory-bound work on the same SMs.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// SDRT_FUSE_NOINLINE: the two job bodies as separate (non-inlined) functions, each with its
+// own register allocation (the inlined pair spills ~100 bytes at 128 registers)
+#ifndef SDRT_FUSE_NOINLINE
+#define SDRT_FUSE_NOINLINE 0
+#endif
+template <int D, int P, int EQ, int E, int NT, int NI>
+__device__ __noinline__ void grad_job(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const TensorBufs& b,
+                                      const TileMaps& tm, int64_t e0, int (*sNb)[E], uint64_t* barp, unsigned par) {
+  grad_tile<D, P, EQ, E, NT, NI, true>(g, L, ph, b, tm, e0, sNb, barp, false, par);
+}
+template <int D, int P, int EQ, int E, int NT>
+__device__ __noinline__ void stage_job(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const TensorBufs& b,
+                                       int stage, double dt, const TileMaps& tm, int64_t e0, int (*sNb)[E],
+                                       uint64_t* barp, unsigned par) {
+  stage_osf_tile<D, P, EQ, E, NT, false>(g, L, ph, b, stage, dt, tm, e0, sNb, barp, false, par);
+}
+
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
+__global__ void __launch_bounds__(NT, MINB) kt_fused(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b, int stage,
+                                                     double dt, const __grid_constant__ TileMaps tm, FuseSched fs) {
+  pdl_wait();
+  __shared__ int sNb[2 * D][E];
+  __shared__ __align__(8) uint64_t barA, barB;
+  // loop state in shared memory (nothing held in registers across a job body: the A body
+  // uses all 128)
+  __shared__ int sJob;
+  __shared__ unsigned sEpoch, sPar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&barA, 1);
+    mbar_init(&barB, 1);
+    mbar_fence_init();
+    // this launch's epoch: one more than the last launch's (ctr[2] advances when the last
+    // CTA of a launch exits, after every CTA has read it), so a CUDA-graph replay works too
+    sEpoch = (unsigned)ld_acquire_u32((const unsigned*)fs.ctr + 2) + 1u;
+    sPar[0] = sPar[1] = 0;
+  }
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) sJob = atomicAdd(fs.ctr, 1);
+    __syncthreads();
+    if (sJob >= fs.njobs) break;
+    const int code = fs.jobs[sJob];
+    if ((code & 1) == 0) {
+      grad_tile<D, P, EQ, E, NT, NI, true>(g, L, ph, b, tm, (int64_t)(code >> 1) * E, sNb, &barA, false, sPar[0]);
+      // this thread's R_int / published-flux stores before the B job's TMA reads of them
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        st_release_u32(fs.flags + (fs.jobs[sJob] >> 1), sEpoch);
+        sPar[0] ^= 1u;
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        const int* dl = fs.deps + (int64_t)(code >> 1) * FUSE_DEPS;
+        for (int k = 0; k < FUSE_DEPS; ++k) {
+          const int t = dl[k];
+          if (t < 0) break;
+          while ((int)(ld_acquire_u32(fs.flags + t) - sEpoch) < 0) __nanosleep(100);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      __syncthreads();
+      stage_osf_tile<D, P, EQ, E, NT, false>(g, L, ph, b, stage, dt, tm, (int64_t)(code >> 1) * E, sNb, &barB, false,
+                                             sPar[1]);
+      __syncthreads();
+      if (threadIdx.x == 0) sPar[1] ^= 1u;
+    }
+    // this job's shared-memory accesses before the next job's TMA writes into the buffers
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(fs.ctr + 1, 1) == (int)gridDim.x - 1) {  // last CTA: reset for the next launch
+      fs.ctr[0] = 0;
+      fs.ctr[1] = 0;
+      __threadfence();
+      atomicAdd(fs.ctr + 2, 1);
+    }
   }
 }
 
@@ -1647,6 +1772,17 @@ static TileMaps maps_for(TensorTma* t, const TensorBufs& b, bool full) {
   return m;
 }
 
+// dynamic shared memory of the fused stage kernel: the larger of kernel A's (OSF) and
+// kernel B's (OSF, any stage) layouts
+template <int D, int P, int EQ>
+static size_t fuse_smem() {
+  using C = TCfg<D, P, EQ>;
+  size_t sm = C::smem_a(P, true);
+  for (int s : {0, 1, 2, 3, RK54_STAGE0, RK54_STAGE0 + 1})
+    if (C::smem_b_osf(s) > sm) sm = C::smem_b_osf(s);
+  return sm;
+}
+
 template <int D, int P, int EQ, int NI>
 static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,
                          const TensorBufs& b, int stage, double dt, cudaStream_t st, int which) {
@@ -1818,6 +1954,105 @@ void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D&
   TmaFn m;
   pick_all(D, P, eq, &s, &t, &m);
   s(g, L, ph, tma, b, stage, dt, st, 1);
+}
+
+template <int D, int P, int EQ>
+static int fuse_ctas_t() {
+  if constexpr (EQ == EQ_NS) {
+    using C = TCfg<D, P, EQ>;
+    auto k = kt_fused<D, P, EQ, C::EA, C::NTA, C::MINB_A, P>;
+    const size_t sm = fuse_smem<D, P, EQ>();
+    set_smem<D, P, EQ>((const void*)k, sm);
+    int nb = 0, dev = 0, nsm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, C::NTA, sm) != cudaSuccess) return 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return nb * nsm;
+  }
+  return 0;
+}
+
+template <int D, int P, int EQ>
+static void run_fused_t(const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma, const TensorBufs& b,
+                        int stage, double dt, const FuseSched& fs, cudaStream_t st) {
+  if constexpr (EQ == EQ_NS) {
+    using C = TCfg<D, P, EQ>;
+    static const int nctas = fuse_ctas_t<D, P, EQ>();
+    if (nctas <= 0) throw std::runtime_error("internal: fused stage kernel has no resident CTA");
+    auto k = kt_fused<D, P, EQ, C::EA, C::NTA, C::MINB_A, P>;
+    CUDA_LAUNCH_OK(launch_pdl(k, (unsigned)nctas, C::NTA, fuse_smem<D, P, EQ>(), st, g, L, ph, b, stage, dt,
+                              maps_for(tma, b, true), fs));
+  } else {
+    throw std::runtime_error("internal: fused stage kernel is NS-only");
+  }
+}
+
+int tensor_fuse_ctas(int D, int P, int eq) {
+  if (eq != EQ_NS) return 0;
+  if (D == 2) return P == 1 ? fuse_ctas_t<2, 1, EQ_NS>() : P == 2 ? fuse_ctas_t<2, 2, EQ_NS>() : P == 3 ? fuse_ctas_t<2, 3, EQ_NS>() : fuse_ctas_t<2, 4, EQ_NS>();
+  return P == 1 ? fuse_ctas_t<3, 1, EQ_NS>() : P == 2 ? fuse_ctas_t<3, 2, EQ_NS>() : P == 3 ? fuse_ctas_t<3, 3, EQ_NS>() : fuse_ctas_t<3, 4, EQ_NS>();
+}
+
+void tensor_launch_fused(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                         TensorTma* tma, const TensorBufs& b, int stage, double dt, const FuseSched& fs,
+                         cudaStream_t st) {
+  if (eq != EQ_NS || L.fr || g.tiles || b.Fexp || stage < 0) throw std::runtime_error("internal: fused stage misuse");
+  if (D == 2) {
+    switch (P) {
+      case 1: run_fused_t<2, 1, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+      case 2: run_fused_t<2, 2, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+      case 3: run_fused_t<2, 3, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+      default: run_fused_t<2, 4, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+    }
+  } else {
+    switch (P) {
+      case 1: run_fused_t<3, 1, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+      case 2: run_fused_t<3, 2, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+      case 3: run_fused_t<3, 3, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+      default: run_fused_t<3, 4, EQ_NS>(g, L, ph, tma, b, stage, dt, fs, st); break;
+    }
+  }
+}
+
+// Job list of the fused stage on a periodic single-rank pattern mesh (element order x
+// fastest, tiles of E consecutive elements): deps[t] = t and the tiles holding the x_d - 1
+// neighbours of t's elements; B(t) is placed after A(min(max deps[t] + lag, ntiles - 1)).
+bool tensor_fuse_plan(int D, const int N[3], int64_t K, int E, int lag, std::vector<int>* jobs,
+                      std::vector<int>* deps) {
+  const int64_t nt = (K + E - 1) / E;
+  deps->assign((size_t)nt * FUSE_DEPS, -1);
+  std::vector<std::vector<int>> after((size_t)nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    int* dl = deps->data() + t * FUSE_DEPS;
+    int nd = 0;
+    int64_t last = t;
+    auto add = [&](int64_t u) {
+      for (int k = 0; k < nd; ++k)
+        if (dl[k] == (int)u) return true;
+      if (nd == FUSE_DEPS) return false;
+      dl[nd++] = (int)u;
+      last = u > last ? u : last;
+      return true;
+    };
+    add(t);
+    for (int64_t e = t * E; e < (t + 1) * E && e < K; ++e) {
+      const int64_t c[3] = {e % N[0], (e / N[0]) % N[1], D == 3 ? e / ((int64_t)N[0] * N[1]) : 0};
+      for (int d = 0; d < D; ++d) {
+        int64_t cc[3] = {c[0], c[1], c[2]};
+        cc[d] = (cc[d] + N[d] - 1) % N[d];
+        const int64_t m = cc[0] + (int64_t)N[0] * (cc[1] + (int64_t)N[1] * cc[2]);
+        if (!add(m / E)) return false;
+      }
+    }
+    const int64_t at = last + lag < nt - 1 ? last + lag : nt - 1;
+    after[(size_t)at].push_back((int)t);
+  }
+  jobs->clear();
+  for (int64_t a = 0; a < nt; ++a) {
+    jobs->push_back((int)(a * 2));
+    for (int t : after[(size_t)a]) jobs->push_back(t * 2 + 1);
+  }
+  return true;
 }
 
 void tensor_launch_diag(int D, int P, const TensorGeom& g, const Line1D& L, const PhysDev& ph, TensorTma* tma,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "physics.cuh"
 
@@ -89,6 +90,28 @@ void tensor_launch_grad(int D, int P, int eq, const TensorGeom& g, const Line1D&
 void tensor_launch_flux(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
                         TensorTma* tma, const TensorBufs& b, int stage, double dt, cudaStream_t st);
 bool tensor_supported(int D, int P, int eq);
+
+// Fused RK stage (kernel A + kernel B in ONE persistent launch; one-sided flux
+// publication, one rank, periodic, SDRT; tensor.cu kt_fused).  CTAs take jobs in the
+// order of a host-built list: every tile's A job in tile order, and each tile's B job
+// after the A jobs of the tiles it reads (its own R_int, its left neighbours' published
+// fluxes) plus a lag, so a B job rarely waits and reads R_int back from L2.
+constexpr int FUSE_DEPS = 8;  // max tiles a B job depends on
+struct FuseSched {
+  const int* jobs;   // [njobs] tile << 1 | (1: B job)
+  const int* deps;   // [ntiles][FUSE_DEPS] tiles whose A job the tile's B job reads (-1: none)
+  int* ctr;          // [4]: next job, CTAs done, launch epoch (zeroed once)
+  unsigned* flags;   // [ntiles]: epoch of the tile's last finished A job (zeroed once)
+  int njobs;
+};
+// job list + dependency table (false: a tile depends on more than FUSE_DEPS tiles)
+bool tensor_fuse_plan(int D, const int N[3], int64_t K, int E, int lag, std::vector<int>* jobs,
+                      std::vector<int>* deps);
+// whether the fused stage kernel exists for (D, P, eq) and its persistent grid size
+int tensor_fuse_ctas(int D, int P, int eq);
+void tensor_launch_fused(int D, int P, int eq, const TensorGeom& g, const Line1D& L, const PhysDev& ph,
+                         TensorTma* tma, const TensorBufs& b, int stage, double dt, const FuseSched& fs,
+                         cudaStream_t st);
 // TGV diagnostics partial sums (3 per tile: rho v.v, S^d:S^d, p div v, solution-point
 // weighted); NS only
 // B1 (optional, with Bq): the nq1 x (P+1) 1D factor of Bq = B1 (x) B1 (x) B1, applied
