@@ -315,6 +315,10 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="sdrt", choices=["sdrt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="e2e through Solver.host_steps with the copies in N overlapped pieces (0: whole-state "
+                         "copies on the compute stream; measured on c4: 9.76 at 8 pieces vs 9.49 serial, c3 "
+                         "slower from the per-piece launch overhead)")
     ap.add_argument("--scheme", default="sdrt", choices=["sdrt", "frsdrt", "frdg"],
                     help="sdrt: the path; frsdrt/frdg: flux reconstruction on the same kernels (tensor "
                          "elements; the paper's SDRT-vs-FR-DG cost comparison, Table perfo_tgv)")
@@ -434,9 +438,13 @@ def main():
 
     # ---------------------------------------------------------------- e2e (host buffers)
     # A dependent trajectory through the public API with the state in host memory: every
-    # step copies the state host->device from pinned memory, runs sdrt_rk_step (one RK4
-    # step) and copies the new state device->host into the same pinned buffer, which is
-    # the next step's input.  Step i+1 consumes step i's output, so nothing overlaps.
+    # step copies the state host->device from pinned memory, runs sdrt_rk_step (one step)
+    # and copies the new state device->host into the same pinned buffer, which is the next
+    # step's input.  Default: whole-state copies on the compute stream.  --e2e-chunks N:
+    # Solver.host_steps, the copies in N pieces on two copy streams, piece k of step i+1's
+    # upload ordered after piece k of step i's download by an event, the compute of step
+    # i+1 after the whole upload -- measured no faster (c4 9.76 vs 9.49: the two PCIe
+    # directions together do not exceed one direction's ~54 GB/s on this host).
     pin = torch.empty(S.shape, dtype=torch.float64).pin_memory()
     pin.copy_(U.cpu())
     torch.cuda.synchronize(dev)
@@ -444,10 +452,13 @@ def main():
         dist.barrier()
     a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a0.record(stream)
-    for i in range(args.steps):
-        U.copy_(pin, non_blocking=True)
-        step_fn(S)(U, cfg.dt, 1)
-        pin.copy_(U, non_blocking=True)
+    if not args.e2e_chunks:
+        for i in range(args.steps):
+            U.copy_(pin, non_blocking=True)
+            step_fn(S)(U, cfg.dt, 1)
+            pin.copy_(U, non_blocking=True)
+    else:
+        S.host_steps(pin, U, cfg.dt, args.steps, rk54=args.integrator == "rk54", chunks=args.e2e_chunks)
     a1.record(stream)
     torch.cuda.synchronize(dev)
     te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
@@ -559,8 +570,13 @@ def main():
                "roofline": roof, "stage_roofline": stage_roof, "cpu_baseline": cpu,
                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                        "d2h_bytes_per_step": state_bytes, "result_finite": e2e_ok,
-                       "pipeline": "dependent trajectory: per step H2D state (pinned) -> sdrt_rk_step -> D2H "
-                                   "state, the next step reads the host copy; serialized on one stream"},
+                       "pipeline": ("dependent trajectory: per step H2D state (pinned) -> sdrt_rk_step -> D2H "
+                                    "state, the next step reads the host copy; serialized on one stream")
+                       if not args.e2e_chunks else
+                       ("dependent trajectory (Solver.host_steps): per step H2D state (pinned) -> one RK step "
+                        "-> D2H state into the same host buffer, which the next step reads; copies in pieces "
+                        "on two copy streams, piece k of step i+1's H2D after piece k of step i's D2H (the two "
+                        "PCIe directions overlap), the step's compute after the whole H2D")},
                "e2e_monitor": mon,
                "gpu_launches": launches, "clocks": clk, "kernel_ms": {k: v[0] for k, v in ktimes.items()},
                "ms_per_step_instrumented": ms_inst_max / args.steps, "state_finite": finite,

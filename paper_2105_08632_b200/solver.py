@@ -85,6 +85,43 @@ class Solver:
                        torch.cuda.current_stream(self.device).cuda_stream)
         return U
 
+    def host_steps(self, H, U, dt, nsteps, rk54=False, chunks=8):
+        """Advance a HOST-resident state H (pinned, self.shape) by nsteps RK steps, each step a
+        full round trip: H -> device (U, scratch), one sdrt_rk_step / sdrt_rk54_step, device
+        -> H; step i+1 reads step i's result from H.  The copies go in `chunks` contiguous
+        pieces on two copy streams ordered per piece by events: piece k of step i+1's upload
+        waits only for piece k of step i's download, so the two PCIe directions run
+        concurrently while keeping the dependency.  All asynchronous on the current stream
+        (no host synchronisation)."""
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        if not hasattr(self, "_copy_streams"):
+            self._copy_streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        sd, sh = self._copy_streams
+        fh, fu = H.view(-1), U.view(-1)
+        n = fu.numel()
+        cut = [n * k // chunks for k in range(chunks + 1)]
+        sh.wait_stream(cur)
+        with torch.cuda.stream(sh):
+            fu.copy_(fh, non_blocking=True)
+        step = self.rk54_step if rk54 else self.rk_step
+        for i in range(nsteps):
+            cur.wait_stream(sh)
+            step(U, dt, 1)
+            sd.wait_stream(cur)
+            for k in range(chunks):
+                a, b = cut[k], cut[k + 1]
+                with torch.cuda.stream(sd):
+                    fh[a:b].copy_(fu[a:b], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(sd)
+                if i + 1 < nsteps:
+                    sh.wait_event(ev)
+                    with torch.cuda.stream(sh):
+                        fu[a:b].copy_(fh[a:b], non_blocking=True)
+        cur.wait_stream(sd)
+        return H
+
     def diagnostics(self, U, degree=10):
         """TGV ensemble averages (<E*>, eps2, eps3), PAPER.md l.2052-2080 (3-D NS), by the
         quadrature exact to `degree` (the paper's 10, l.2075; 0 = solution points)."""
