@@ -73,6 +73,11 @@
 #endif
 // kernel A internal fluxes and published g by register-blocked line items (visc_line):
 // 0 off (per-point items), 1 on
+// streamed line items for the internal fluxes on the one-sided publication path (NS):
+// visc_sline instead of per-point visc_internal items
+#ifndef SDRT_TA_SLINE
+#define SDRT_TA_SLINE 0
+#endif
 #ifndef SDRT_TA_LINE
 #define SDRT_TA_LINE 1
 #endif
@@ -598,6 +603,58 @@ __device__ __forceinline__ void visc_internal(const TensorGeom& g, const Line1D&
   for (int v = 0; v < NV; ++v) sF[((t * NI + a) * NV + v) * E + el] = fc[v] + fv[v];
 }
 
+// Streamed line item (SDRT_TA_SLINE, one-sided flux publication path): one item = all NI
+// internal flux points of one d-line t of one element.  Each component the axis physics
+// reads (u_v; q[d][.]; q[j][0], q[j][1+d], q[j][1+j] for j != d) is loaded from shared
+// memory ONCE (n values) and interpolated to the NI points from registers, instead of
+// once per point (visc_internal: NI x the loads).  A compiler memory fence after each
+// component keeps the next component's loads from being hoisted (at most n loads in
+// flight), so the NI points' inputs (NI x 16 values) plus the physics fit the 128
+// registers of two 256-thread CTAs per SM.  The interpolation sums are the same fma
+// chains as visc_internal's (bitwise the per-point items).
+template <int D, int P, int EQ, int E, int d, int NI>
+__device__ __forceinline__ void visc_sline(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                           const double* sQ, double* sF, int t, int el) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NS = T::NS;
+  static_assert(NI < n, "streamed line items: SDRT internal points only");
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  double ua[NI][NV], qa[NI][D * NV];
+#pragma unroll
+  for (int c = 0; c < NV + D * NV; ++c) {
+    const int dd = c < NV ? -1 : (c - NV) / NV, v = c < NV ? c : (c - NV) % NV;
+    if (dd >= 0 && !(dd == d || v == 0 || v == 1 + d || v == 1 + dd)) {
+#pragma unroll
+      for (int a = 0; a < NI; ++a) qa[a][dd * NV + v] = 0.0;  // not read by visc_axis<d>
+      continue;
+    }
+    const double* base = dd < 0 ? sU + (lb * NV + v) * E + el : sQ + ((dd * NS + lb) * NV + v) * E + el;
+    double x[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) x[i] = base[i * ls * NV * E];
+#pragma unroll
+    for (int a = 0; a < NI; ++a) {
+      double s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < n; ++i) s2 = fma(L.Iint[a][i], x[i], s2);
+      if (dd < 0) ua[a][v] = s2;
+      else qa[a][dd * NV + v] = s2;
+    }
+    asm volatile("" ::: "memory");
+  }
+  const double wf = g.detJ * g.jinv[d];
+#pragma unroll
+  for (int a = 0; a < NI; ++a) {
+    double fc[NV], fv[NV];
+    Ph::template conv_axis<d>(ph, ua[a], wf, fc);
+    Ph::template visc_axis<d>(ph, ua[a], qa[a], wf, fv);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) sF[((t * NI + a) * NV + v) * E + el] = fc[v] + fv[v];
+    asm volatile("" ::: "memory");
+  }
+}
+
 // visc_internal for the element pair (el0, el0 + 1): 16-byte shared-memory loads
 // (SDRT_TA_PAIR), the physics evaluated per element
 template <int D, int P, int EQ, int E, int d, int NI>
@@ -923,7 +980,8 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     static_assert(!OSF || (!LDMMA && !LINE), "OSF runs on the per-point kernel-A items");
     const int nA = (ph_ < D && !LDMMA && !LINE) ? npub : 0;
     constexpr bool PAIR = SDRT_TA_PAIR == 1 || (SDRT_TA_PAIR == 2 && NV == 1);
-    const int nB = (ph_ < D && !LDMMA && !LINE) ? (PAIR ? NFI / 2 : NFI) : 0;
+    constexpr bool SLINE = OSF && SDRT_TA_SLINE != 0 && NV > 1 && NI < T::n;
+    const int nB = (ph_ < D && !LDMMA && !LINE) ? (SLINE ? NL * E : (PAIR ? NFI / 2 : NFI)) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
     // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
     auto divergence = [&]() {
@@ -1006,6 +1064,12 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
           else if (ph_ == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
           else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
         }
+      } else if constexpr (SLINE) {
+        const int i2 = item - nA, el = i2 % E, t = i2 / E;
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        if (ph_ == 0) visc_sline<D, P, EQ, E, 0, NI>(g, L, ph, sU, sQ, f1, t, el);
+        else if (ph_ == 1) visc_sline<D, P, EQ, E, 1, NI>(g, L, ph, sU, sQ, f1, t, el);
+        else if constexpr (D == 3) visc_sline<D, P, EQ, E, 2, NI>(g, L, ph, sU, sQ, f1, t, el);
       } else if constexpr (PAIR) {
         constexpr int E2 = E / 2;
         const int i2 = item - nA, el = 2 * (i2 % E2), r = i2 / E2, a = r % NI, t = r / NI;
