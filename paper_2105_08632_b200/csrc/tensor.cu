@@ -73,10 +73,13 @@
 #endif
 // kernel A internal fluxes and published g by register-blocked line items (visc_line):
 // 0 off (per-point items), 1 on
-// streamed line items for the internal fluxes on the one-sided publication path (NS):
-// visc_sline instead of per-point visc_internal items
+// line items on the one-sided publication path (NS), instead of per-point visc_internal
+// and publish_F items: 0 off; 1 one item per d-line for its internal points (visc_sline;
+// measured on c4: kernel A 252 vs 242 us, phase imbalance against the publish items and
+// spills); 2 (default) two half-line items per d-line, the second carrying the published
+// end (visc_hline; c4 kernel A 242 -> 220 us, 31.8 -> 34.1 GDOF-stage/s)
 #ifndef SDRT_TA_SLINE
-#define SDRT_TA_SLINE 0
+#define SDRT_TA_SLINE 2
 #endif
 #ifndef SDRT_TA_LINE
 #define SDRT_TA_LINE 1
@@ -655,6 +658,91 @@ __device__ __forceinline__ void visc_sline(const TensorGeom& g, const Line1D& L,
   }
 }
 
+// Half-line items (SDRT_TA_SLINE = 2, one-sided flux publication): the outputs of a d-line
+// -- its NI internal flux points and its published x_d = +1 end -- split over TWO items of
+// (almost) equal work: H = 0 the first ceil(NI/2) internal points, H = 1 the others plus
+// the end (publish_F's common flux).  Each item loads every component it needs once and
+// interpolates it to its two outputs from registers (half the loads of per-point items,
+// 2 x 16 live inputs).  Same arithmetic as visc_internal / publish_F (bitwise).
+template <int D, int P, int EQ, int E, int d, int NI, int H>
+__device__ __forceinline__ void visc_hline(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
+                                           const double* sQ, double* sF, const TensorBufs& b, double* sP,
+                                           int64_t e0, int t, int el) {
+  using Ph = Phys<EQ, D>;
+  using T = TDims<D, P>;
+  constexpr int NV = Ph::NV, n = T::n, NS = T::NS, NL = T::NL;
+  static_assert(NI < n, "half-line items: SDRT internal points only");
+  constexpr int A0 = H == 0 ? 0 : (NI + 1) / 2;           // first internal point
+  constexpr int NA = H == 0 ? (NI + 1) / 2 : NI - A0;     // internal points of this item
+  constexpr int NO = NA + H;                              // + the published end (H = 1)
+  const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  double uo[NO][NV], qo[NO][D * NV];
+#pragma unroll
+  for (int c = 0; c < NV + D * NV; ++c) {
+    const int dd = c < NV ? -1 : (c - NV) / NV, v = c < NV ? c : (c - NV) % NV;
+    if (dd >= 0 && !(dd == d || v == 0 || v == 1 + d || v == 1 + dd)) {
+#pragma unroll
+      for (int o = 0; o < NO; ++o) qo[o][dd * NV + v] = 0.0;  // not read by visc_axis<d>
+      continue;
+    }
+    const double* base = dd < 0 ? sU + (lb * NV + v) * E + el : sQ + ((dd * NS + lb) * NV + v) * E + el;
+    double x[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) x[i] = base[i * ls * NV * E];
+#pragma unroll
+    for (int o = 0; o < NO; ++o) {
+      double s2;
+      if (o < NA) {
+        s2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) s2 = fma(L.Iint[A0 + o][i], x[i], s2);
+      } else if (dd < 0) {
+        s2 = interp_end<n>(L.Iend[1], x);
+      } else {
+        s2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < n; ++i) s2 = fma(L.Iend[1][i], x[i], s2);
+      }
+      if (dd < 0) uo[o][v] = s2;
+      else qo[o][dd * NV + v] = s2;
+    }
+    asm volatile("" ::: "memory");
+  }
+  const double wf = g.detJ * g.jinv[d];
+#pragma unroll
+  for (int o = 0; o < NA; ++o) {
+    double fc[NV], fv[NV];
+    Ph::template conv_axis<d>(ph, uo[o], wf, fc);
+    Ph::template visc_axis<d>(ph, uo[o], qo[o], wf, fv);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) sF[((t * NI + A0 + o) * NV + v) * E + el] = fc[v] + fv[v];
+  }
+  if constexpr (H == 1) {  // the x_d = +1 end: publish_F
+    const int64_t e = e0 + el;
+    if (e >= g.K) return;
+    const int ext = (2 * d + 1) * NL + t;
+    double* p1 = sP + d * NL * NV * E;
+    double uR[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) uR[v] = p1[(t * NV + v) * E + el];
+    double gv[NV], F[NV];
+    Ph::template visc_axis<d>(ph, uo[NA], qo[NA], 1.0, gv);
+    Ph::template conv_common_axis<d>(ph, uo[NA], uR, F);
+    const double wl = 0.5 + ph.beta;
+    const double sface = g.sface[d];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      F[v] = Ph::ldg_rn(F[v], __dmul_rn(wl, gv[v]), ph.eta, uo[NA][v], uR[v]);
+      b.Tg[((int64_t)ext * NV + v) * g.Kt + e] = F[v];
+      p1[(t * NV + v) * E + el] = sface * F[v];
+    }
+    if (b.Fexp) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) b.Fexp[((int64_t)ext * NV + v) * g.Kp + e] = F[v];
+    }
+  }
+}
+
 // visc_internal for the element pair (el0, el0 + 1): 16-byte shared-memory loads
 // (SDRT_TA_PAIR), the physics evaluated per element
 template <int D, int P, int EQ, int E, int d, int NI>
@@ -978,10 +1066,11 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     }
     constexpr bool LDMMA = SDRT_TA_DMMA != 0 && E == 8 && Ph::VISC && NV > 1;
     static_assert(!OSF || (!LDMMA && !LINE), "OSF runs on the per-point kernel-A items");
-    const int nA = (ph_ < D && !LDMMA && !LINE) ? npub : 0;
+    constexpr bool SLINE = OSF && SDRT_TA_SLINE == 1 && NV > 1 && NI < T::n;
+    constexpr bool HLINE = OSF && SDRT_TA_SLINE == 2 && NV > 1 && NI < T::n;  // publishes in its items
+    const int nA = (ph_ < D && !LDMMA && !LINE && !HLINE) ? npub : 0;
     constexpr bool PAIR = SDRT_TA_PAIR == 1 || (SDRT_TA_PAIR == 2 && NV == 1);
-    constexpr bool SLINE = OSF && SDRT_TA_SLINE != 0 && NV > 1 && NI < T::n;
-    const int nB = (ph_ < D && !LDMMA && !LINE) ? (SLINE ? NL * E : (PAIR ? NFI / 2 : NFI)) : 0;
+    const int nB = (ph_ < D && !LDMMA && !LINE) ? (HLINE ? 2 * NL * E : SLINE ? NL * E : (PAIR ? NFI / 2 : NFI)) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
     // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
     auto divergence = [&]() {
@@ -1064,6 +1153,19 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
           else if (ph_ == 1) publish_g<D, P, EQ, E, 1>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
           else if constexpr (D == 3) publish_g<D, P, EQ, E, 2>(g, L, ph, sU, sQ, b.Tg, e0, side, t, el);
         }
+      } else if constexpr (HLINE) {
+        // items 0 .. 2 NL E - 1 (no separate publish items): half h = first / second half of
+        // each line, warp-uniform (NL E is a multiple of 32)
+        const int el = item % E, t = (item / E) % NL, h = item / (NL * E);
+        double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
+        auto run = [&](auto dc) {
+          constexpr int d = decltype(dc)::value;
+          if (h == 0) visc_hline<D, P, EQ, E, d, NI, 0>(g, L, ph, sU, sQ, f1, b, sP, e0, t, el);
+          else visc_hline<D, P, EQ, E, d, NI, 1>(g, L, ph, sU, sQ, f1, b, sP, e0, t, el);
+        };
+        if (ph_ == 0) run(std::integral_constant<int, 0>{});
+        else if (ph_ == 1) run(std::integral_constant<int, 1>{});
+        else if constexpr (D == 3) run(std::integral_constant<int, 2>{});
       } else if constexpr (SLINE) {
         const int i2 = item - nA, el = i2 % E, t = i2 / E;
         double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
