@@ -84,8 +84,65 @@
 #ifndef SDRT_TA_LINE
 #define SDRT_TA_LINE 1
 #endif
+// half-line items (hex p = 3, N_V odd, 8-element tiles): row-pair swizzle of the gradient
+// tile sQ.  A warp's four x-lines (t = y + 4 z, y = 0..3) start 4 points = 20 rows of 64 B
+// apart: all in the same half of the 128-byte bank window (2-way conflict on every load of
+// direction 0).  Row r of point s is stored at r ^ ((s >> 2) & 1): adjacent y rows swap
+// halves, conflict-free in all three directions, no extra shared memory.  Bitwise the
+// unswizzled kernel (layout only).
+#ifndef SDRT_TA_QSWZ
+#define SDRT_TA_QSWZ 0
+#endif
+// half-line items: which warps take which half of the lines.  0: warps 0-3 the first
+// halves, 4-7 the second; 1: the half is bit 1 of the warp index, so the two warps of a
+// CTA that share a scheduler (w, w + 4) run the same code (instruction-cache reuse)
+#ifndef SDRT_TA_HMAP
+#define SDRT_TA_HMAP 0
+#endif
+// one-sided publication kernel A, divergence: the partial sums of R_int over the directions
+// accumulated by a global read-modify-write of the owning thread (0) or by
+// red.global.add.f64 onto the first direction's store (1, default: no load, no prefetch
+// registers, 126 -> 121 registers; the directions are separated by CTA barriers and each
+// address belongs to one CTA, so the sum order is fixed: deterministic; each direction's
+// fma chain is rounded before it is added, fl(R + fl(chain)), instead of one chain through
+// R, so not bitwise mode 0).  Measured on c4: kernel A 220 -> 203 us, 34.2 -> 36.15
+// GDOF-stage/s.
+#ifndef SDRT_TA_DRED
+#define SDRT_TA_DRED 1
+#endif
+// half-line items: 1 = software-pipelined component loads (the next needed component's n
+// shared-memory loads are issued before the current component's interpolation sums)
+#ifndef SDRT_TA_HPIPE
+#define SDRT_TA_HPIPE 0
+#endif
+// one-sided publication kernel A as a persistent kernel (kt_grad_p: MINB CTAs per SM, each
+// walking tiles blockIdx.x, + gridDim.x, ...): the next tile's stage input (TMA), neighbour
+// indices and neighbour traces are requested during the current tile's last divergence
+// phase, when the state and gradient tiles are dead, instead of at the next CTA's start
+// (the tile + neighbour-load latency is ~15 % of a one-tile CTA's life).  Same per-tile
+// arithmetic (bitwise the one-tile kernel).
+#ifndef SDRT_TA_PERSIST
+#define SDRT_TA_PERSIST 0
+#endif
 
 namespace sdrt {
+
+// swizzled sQ (SDRT_TA_QSWZ): offset (in doubles) added to the linear address of the i-th
+// load (point lb + i ls) of component v along d-line t; v, i compile-time at the call sites
+template <int d, int E>
+struct QSwz {
+  int f;
+  __device__ __forceinline__ explicit QSwz(int t) {
+    if constexpr (d == 0) f = (t & 1) * E;                      // s = y & 1, row parity (v + i) & 1
+    else if constexpr (d == 1) f = (t & 1) ? -E : E;            // s = i & 1, row parity (x + v) & 1
+    else f = ((t >> 2) & 1) ? ((t & 1) ? -E : E) : 0;           // s = y & 1, row parity (x + v) & 1
+  }
+  __device__ __forceinline__ int off(int v, int i) const {
+    if constexpr (d == 0) return ((v + i) & 1) ? -f : f;
+    else if constexpr (d == 1) return (i & 1) ? ((v & 1) ? -f : f) : 0;
+    else return (v & 1) ? -f : f;
+  }
+};
 
 // Optional per-phase cycle accounting (build with -DSDRT_PHASE_PROF; tools only):
 // thread 0 of every CTA adds the clock64() time of each phase after its barrier.
@@ -255,9 +312,11 @@ struct GradNb {
 
   // sNbR (OSF): the right neighbours' traces nb[.][1] are also stored to sNbR[d][t][v][el]
   // for publish_F (the same (d, t, v, el) entries)
+  template <bool SWZ = false>
   __device__ __forceinline__ void compute(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
                                           double* sQ, int64_t e0, double* sNbR = nullptr) const {
     constexpr int n = T::n, NL = T::NL, NS = T::NS;
+    static_assert(!SWZ || SDRT_TA_GQ != 0, "swizzled sQ: composite-operator gradient only");
     const double wl = 0.5 - ph.beta, wr = 0.5 + ph.beta;
 #pragma unroll
     for (int k = 0; k < CI; ++k) {
@@ -281,7 +340,12 @@ struct GradNb {
           q = fma(L.H1[dd][i], nb[k][1], q);
 #pragma unroll
           for (int j = 0; j < n; ++j) q = fma(L.Gq[dd][i][j], u[j], q);
-          sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el] = q;
+          if constexpr (SWZ) {  // SDRT_TA_QSWZ: row r of point s at r ^ ((s >> 2) & 1)
+            const int pt = lb + i * ls, row = (dd * NS + pt) * NV + v;
+            sQ[(row ^ ((pt >> 2) & 1)) * E + el] = q;
+          } else {
+            sQ[((dd * NS + (lb + i * ls)) * NV + v) * E + el] = q;
+          }
         }
       };
       if (d == 0) gq(std::integral_constant<int, 0>{});
@@ -664,7 +728,7 @@ __device__ __forceinline__ void visc_sline(const TensorGeom& g, const Line1D& L,
 // the end (publish_F's common flux).  Each item loads every component it needs once and
 // interpolates it to its two outputs from registers (half the loads of per-point items,
 // 2 x 16 live inputs).  Same arithmetic as visc_internal / publish_F (bitwise).
-template <int D, int P, int EQ, int E, int d, int NI, int H>
+template <int D, int P, int EQ, int E, int d, int NI, int H, bool SWZ = false>
 __device__ __forceinline__ void visc_hline(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const double* sU,
                                            const double* sQ, double* sF, const TensorBufs& b, double* sP,
                                            int64_t e0, int t, int el) {
@@ -676,19 +740,43 @@ __device__ __forceinline__ void visc_hline(const TensorGeom& g, const Line1D& L,
   constexpr int NA = H == 0 ? (NI + 1) / 2 : NI - A0;     // internal points of this item
   constexpr int NO = NA + H;                              // + the published end (H = 1)
   const int lb = lbase<D, P>(d, t), ls = lstr<D, P>(d);
+  static_assert(!SWZ || (D == 3 && n == 4 && (NV & 1) == 1 && E == 8), "swizzled sQ: hex p = 3, odd N_V, 8-element tiles");
+  const QSwz<d, E> qz(t);
   double uo[NO][NV], qo[NO][D * NV];
-#pragma unroll
-  for (int c = 0; c < NV + D * NV; ++c) {
+  constexpr int NC = NV + D * NV;
+  // component c = (dd, v): dd = -1 the state, else the gradient along dd; needed by visc_axis<d>?
+  auto needed = [](int c) {
     const int dd = c < NV ? -1 : (c - NV) / NV, v = c < NV ? c : (c - NV) % NV;
-    if (dd >= 0 && !(dd == d || v == 0 || v == 1 + d || v == 1 + dd)) {
+    return dd < 0 || dd == d || v == 0 || v == 1 + d || v == 1 + dd;
+  };
+  auto ld = [&](int c, double (&x)[n]) {  // the n line values of component c
+    const int dd = c < NV ? -1 : (c - NV) / NV, v = c < NV ? c : (c - NV) % NV;
+    const double* base = dd < 0 ? sU + (lb * NV + v) * E + el : sQ + ((dd * NS + lb) * NV + v) * E + el;
+    if constexpr (SWZ) {
+#pragma unroll
+      for (int i = 0; i < n; ++i) x[i] = base[i * ls * NV * E + (dd < 0 ? 0 : qz.off(v, i))];
+    } else {
+#pragma unroll
+      for (int i = 0; i < n; ++i) x[i] = base[i * ls * NV * E];
+    }
+  };
+  double x[n], xn[n];
+  if constexpr (SDRT_TA_HPIPE != 0) ld(0, x);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const int dd = c < NV ? -1 : (c - NV) / NV, v = c < NV ? c : (c - NV) % NV;
+    if (!needed(c)) {
 #pragma unroll
       for (int o = 0; o < NO; ++o) qo[o][dd * NV + v] = 0.0;  // not read by visc_axis<d>
       continue;
     }
-    const double* base = dd < 0 ? sU + (lb * NV + v) * E + el : sQ + ((dd * NS + lb) * NV + v) * E + el;
-    double x[n];
-#pragma unroll
-    for (int i = 0; i < n; ++i) x[i] = base[i * ls * NV * E];
+    if constexpr (SDRT_TA_HPIPE != 0) {  // the next needed component's loads before this one's sums
+      int c2 = c + 1;
+      while (c2 < NC && !needed(c2)) ++c2;
+      if (c2 < NC) ld(c2, xn);
+    } else {
+      ld(c, x);
+    }
 #pragma unroll
     for (int o = 0; o < NO; ++o) {
       double s2;
@@ -705,6 +793,10 @@ __device__ __forceinline__ void visc_hline(const TensorGeom& g, const Line1D& L,
       }
       if (dd < 0) uo[o][v] = s2;
       else qo[o][dd * NV + v] = s2;
+    }
+    if constexpr (SDRT_TA_HPIPE != 0) {
+#pragma unroll
+      for (int i = 0; i < n; ++i) x[i] = xn[i];
     }
     asm volatile("" ::: "memory");
   }
@@ -983,22 +1075,37 @@ __device__ __forceinline__ void visc_line_dmma(const TensorGeom& g, const Line1D
 // Kernel A body for the tile starting at element e0 (kt_grad: one tile per CTA; kt_fused:
 // the A jobs of the persistent schedule).  bar: the CTA's TMA mbarrier, already
 // initialised when init == false; par: the phase parity this use waits for.
-template <int D, int P, int EQ, int E, int NT, int NI, bool OSF>
+// PERS (kt_grad_p): the tile's TMA, neighbour indices and neighbour traces (gnp) were
+// requested by the caller / the previous tile; this tile requests those of tile e0n
+// (-1: none) into sNbN during its last divergence phase
+template <int D, int P, int EQ, int E, int NT, int NI, bool OSF, bool PERS = false>
 __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, const PhysDev& ph, const TensorBufs& b,
                                           const TileMaps& tm, int64_t e0, int (*sNb)[E], uint64_t* barp, bool init,
-                                          unsigned par) {
+                                          unsigned par, GradNb<D, P, EQ, E, NT, NI>* gnp = nullptr, int64_t e0n = -1,
+                                          int (*sNbN)[E] = nullptr) {
   PH_INIT
   using Ph = Phys<EQ, D>;
   using T = TDims<D, P>;
   constexpr int NV = Ph::NV, NL = T::NL, NS = T::NS;
   constexpr int NFB = NL * NI * NV * E;  // one internal-flux buffer
   constexpr bool DBUF = tensor_a_dbuf(D, NS, NL, NV, E, NI, OSF);
+  // half-line items on a swizzled gradient tile (see SDRT_TA_QSWZ)
+  constexpr bool QSWZ = SDRT_TA_QSWZ != 0 && SDRT_TA_GQ != 0 && OSF && SDRT_TA_SLINE == 2 && NV > 1 && NI < T::n &&
+                        D == 3 && T::n == 4 && (NV & 1) == 1 && E == 8 && SDRT_TA_GPAIR != 1;
   extern __shared__ __align__(128) double smem[];
   double* sU = smem;
   double* sQ = smem + NS * NV * E;
   double* sF = sQ + D * NS * NV * E;  // 2 x [NL][P][NV][E]
   // OSF: [D][NL][NV][E], the right neighbours' traces, then sface F at the x_d = +1 ends
   double* sP = sF + (DBUF ? 2 : 1) * NFB;
+  if constexpr (PERS) {
+    static_assert(OSF && !DBUF && Ph::NV > 1, "persistent kernel A: the one-sided publication path");
+    mbar_wait(barp, par);
+    __syncthreads();
+  PH(0, 1)
+    if constexpr (QSWZ) gnp->template compute<true>(g, L, ph, sU, sQ, e0, sP);
+    else gnp->compute(g, L, ph, sU, sQ, e0, sP);
+  } else {
   if (threadIdx.x == 0) {  // the stage-input tile by TMA
     if (init) {
       mbar_init(barp, 1);
@@ -1017,7 +1124,9 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     mbar_wait(barp, par);
     __syncthreads();
   PH(0, 1)
-    gn.compute(g, L, ph, sU, sQ, e0, OSF ? sP : nullptr);
+    if constexpr (QSWZ) gn.template compute<true>(g, L, ph, sU, sQ, e0, OSF ? sP : nullptr);
+    else gn.compute(g, L, ph, sU, sQ, e0, OSF ? sP : nullptr);
+  }
   }
   __syncthreads();
   PH(0, 2)
@@ -1050,8 +1159,9 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     // partial sums of R_int requested before the flux work (not in LSPLIT mode: there
     // the divergence threads do no flux work, and the prefetch registers would be live
     // across the line items in the register allocation)
-    double prev[LSPLIT ? 1 : CD][P + 1];
-    if (!LSPLIT && ph_ >= 2 && divthr) {
+    constexpr bool DRED = SDRT_TA_DRED == 2 || (SDRT_TA_DRED == 1 && OSF);  // 2: every kernel-A path
+    double prev[(LSPLIT || DRED) ? 1 : CD][(LSPLIT || DRED) ? 1 : P + 1];
+    if (!LSPLIT && !DRED && ph_ >= 2 && divthr) {
 #pragma unroll
       for (int k = 0; k < CD; ++k) {
         const int item = dtid + k * NDT;
@@ -1091,7 +1201,8 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
 #pragma unroll
         for (int i = 0; i <= P; ++i) {
           double acc = 0.0;
-          if constexpr (LSPLIT) {
+          if constexpr (DRED) {
+          } else if constexpr (LSPLIT) {
             if (ph_ >= 2) acc = dst[(int64_t)i * ls * NV * g.Kp];
           } else if (ph_ >= 2) {
             acc = prev[k][i];
@@ -1099,10 +1210,29 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
 #pragma unroll
           for (int a = 0; a < NI; ++a) acc = fma(L.Dfl[i][a + 1], f[a], acc);
           if constexpr (OSF) acc = fma(L.Dfl[i][NI + 1], fp, acc);
+          if constexpr (DRED) {
+            if (ph_ >= 2) {
+              asm volatile("red.global.add.f64 [%0], %1;" ::"l"(dst + (int64_t)i * ls * NV * g.Kp), "d"(acc) : "memory");
+              continue;
+            }
+          }
           dst[(int64_t)i * ls * NV * g.Kp] = acc;
         }
       }
     };
+    if constexpr (PERS) {
+      // last phase: the state and gradient tiles are dead (every thread fenced its reads
+      // against the async proxy before the barrier that ended phase D - 1)
+      if (ph_ == D && e0n >= 0) {
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(barp, NS * NV * E * 8);
+          tma_tile<NS * NV, E>(sU, &tm.uin, e0n, barp);
+        }
+        fill_nbrs<D, E>(g, sNbN, e0n);
+        __syncthreads();
+        gnp->load(g, ph, b.Tu, sNbN, e0n);
+      }
+    }
     if constexpr (!DBUF) {
       if (ph_ >= 1) divergence();
       __syncthreads();
@@ -1156,12 +1286,19 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
       } else if constexpr (HLINE) {
         // items 0 .. 2 NL E - 1 (no separate publish items): half h = first / second half of
         // each line, warp-uniform (NL E is a multiple of 32)
-        const int el = item % E, t = (item / E) % NL, h = item / (NL * E);
+        int el = item % E, t = (item / E) % NL, h = item / (NL * E);
+        if constexpr (SDRT_TA_HMAP != 0 && NL * E == 128 && NT == 256) {
+          // warps w and w + 4 (one scheduler) run the same half: h = bit 1 of the warp index
+          const int w = item >> 5, lane = item & 31;
+          h = (w >> 1) & 1;
+          t = 4 * ((w & 1) + 2 * (w >> 2)) + (lane >> 3);
+          el = lane & 7;
+        }
         double* f1 = sF + (DBUF ? (ph_ & 1) * NFB : 0);
         auto run = [&](auto dc) {
           constexpr int d = decltype(dc)::value;
-          if (h == 0) visc_hline<D, P, EQ, E, d, NI, 0>(g, L, ph, sU, sQ, f1, b, sP, e0, t, el);
-          else visc_hline<D, P, EQ, E, d, NI, 1>(g, L, ph, sU, sQ, f1, b, sP, e0, t, el);
+          if (h == 0) visc_hline<D, P, EQ, E, d, NI, 0, QSWZ>(g, L, ph, sU, sQ, f1, b, sP, e0, t, el);
+          else visc_hline<D, P, EQ, E, d, NI, 1, QSWZ>(g, L, ph, sU, sQ, f1, b, sP, e0, t, el);
         };
         if (ph_ == 0) run(std::integral_constant<int, 0>{});
         else if (ph_ == 1) run(std::integral_constant<int, 1>{});
@@ -1208,6 +1345,9 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     if constexpr (DBUF) {
       if (ph_ >= 1) divergence();
     }
+    if constexpr (PERS) {
+      if (ph_ == D - 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
     __syncthreads();
   PH(0, 3 + ph_)
   }
@@ -1221,6 +1361,43 @@ __global__ void __launch_bounds__(NT, MINB) kt_grad(TensorGeom g, Line1D L, Phys
   __shared__ __align__(8) uint64_t bar;
   const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
   grad_tile<D, P, EQ, E, NT, NI, OSF>(g, L, ph, b, tm, e0, sNb, &bar, true, 0);
+}
+
+// Persistent one-sided-publication kernel A (SDRT_TA_PERSIST): see the macro's comment
+template <int D, int P, int EQ, int E, int NT, int MINB, int NI>
+__global__ void __launch_bounds__(NT, MINB) kt_grad_p(TensorGeom g, Line1D L, PhysDev ph, TensorBufs b,
+                                                      const __grid_constant__ TileMaps tm, int ntiles) {
+  pdl_wait();
+  using T = TDims<D, P>;
+  constexpr int NV = Phys<EQ, D>::NV;
+  __shared__ int sNb[2][2 * D][E];
+  __shared__ __align__(8) uint64_t bar;
+  extern __shared__ __align__(128) double smem[];
+  auto tile_e0 = [&](int t) { return (int64_t)(g.tiles ? g.tiles[t] : t) * E; };
+  int tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  int64_t e0 = tile_e0(tile);
+  GradNb<D, P, EQ, E, NT, NI> gn;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, T::NS * NV * E * 8);
+    tma_tile<T::NS * NV, E>(smem, &tm.uin, e0, &bar);
+  }
+  fill_nbrs<D, E>(g, sNb[0], e0);
+  __syncthreads();
+  gn.load(g, ph, b.Tu, sNb[0], e0);
+  unsigned par = 0;
+  int buf = 0;
+#pragma unroll 1
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int next = tile + (int)gridDim.x;
+    const int64_t e0n = next < ntiles ? tile_e0(next) : -1;
+    grad_tile<D, P, EQ, E, NT, NI, true, true>(g, L, ph, b, tm, e0, sNb[buf], &bar, false, par, &gn, e0n, sNb[buf ^ 1]);
+    par ^= 1u;
+    buf ^= 1;
+    e0 = e0n;
+  }
 }
 
 // Kernel B: common fluxes at the line ends (Rusanov / upwind + the published viscous
@@ -1959,6 +2136,23 @@ static void run_stage_ni(const TensorGeom& g, const Line1D& L, const PhysDev& ph
       if (grid == 0) return;
       if constexpr (EQ == EQ_NS) {
         if (g.osf) {
+#if SDRT_TA_PERSIST
+          if constexpr (!tensor_a_dbuf(D, TDims<D, P>::NS, TDims<D, P>::NL, Phys<EQ, D>::NV, C::EA, NI, true)) {
+            auto kp = kt_grad_p<D, P, EQ, C::EA, C::NTA, C::MINB_A, NI>;
+            set_smem<D, P, EQ>((const void*)kp, C::smem_a(NI, true));
+            static int cap = 0;  // resident CTAs of this device
+            if (cap == 0) {
+              int nb = 0, dev = 0, nsm = 0;
+              cudaGetDevice(&dev);
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kp, C::NTA, C::smem_a(NI, true));
+              cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+              cap = nb * nsm > 0 ? nb * nsm : 1;
+            }
+            const unsigned gp = grid < (unsigned)cap ? grid : (unsigned)cap;
+            CUDA_LAUNCH_OK(launch_pdl(kp, gp, C::NTA, C::smem_a(NI, true), st, g, L, ph, b, maps_for(tma, b, false), (int)grid));
+            return;
+          }
+#endif
           auto ka = kt_grad<D, P, EQ, C::EA, C::NTA, C::MINB_A, NI, true>;
           set_smem<D, P, EQ>((const void*)ka, C::smem_a(NI, true));
           CUDA_LAUNCH_OK(launch_pdl(ka, grid, C::NTA, C::smem_a(NI, true), st, g, L, ph, b, maps_for(tma, b, false)));
