@@ -124,6 +124,18 @@
 #ifndef SDRT_TA_PERSIST
 #define SDRT_TA_PERSIST 0
 #endif
+// half-line items: warp-pair barriers.  Warps w and w + 4 hold the two halves of the same
+// four d-lines x 8 elements in every direction; with the divergence items of those lines
+// given to the same 64 threads, the flux -> divergence -> next flux hand-offs through the
+// internal-flux buffer are pair-local, so the direction loop synchronises on named
+// barriers of 64 threads (bar.sync 1 + pair) and the pairs drift apart (flux work of one
+// overlaps the divergence stores of another).  One CTA-wide barrier stays after the last
+// flux phase: a point's R_int entry is written by different pairs in different
+// directions, and the RED order of directions 1 and 2 (and the store before them) must be
+// fixed.  Same arithmetic per item and the same order per address (bitwise mode 0).
+#ifndef SDRT_TA_PAIRB
+#define SDRT_TA_PAIRB 0
+#endif
 
 namespace sdrt {
 
@@ -1183,13 +1195,29 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     const int nB = (ph_ < D && !LDMMA && !LINE) ? (HLINE ? 2 * NL * E : SLINE ? NL * E : (PAIR ? NFI / 2 : NFI)) : 0;
     // divergence of direction ph_-1 from buffer (ph_-1)&1 (single buffer when two do
     // not fit two CTAs per SM: then it runs before this phase's fluxes overwrite it)
+    constexpr bool PAIRB = SDRT_TA_PAIRB != 0 && HLINE && !PERS && !DBUF && NT == 256 && NL * E == 128;
+    const int pair = (threadIdx.x >> 5) & 3;  // PAIRB: warps pair, pair + 4
+    auto phase_sync = [&](bool cta) {
+      if constexpr (PAIRB) {
+        if (!cta) {
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
+          return;
+        }
+      }
+      __syncthreads();
+    };
     auto divergence = [&]() {
       const double* f0 = sF + (DBUF ? (dd & 1) * NFB : 0);
       if (!divthr) return;
 #pragma unroll
       for (int k = 0; k < CD; ++k) {
-        const int item = dtid + k * NDT;
-        const int el = item % E, r = item / E, v = r % NV, t = r / NV;
+        int item = dtid + k * NDT;
+        int el = item % E, r = item / E, v = r % NV, t = r / NV;
+        if constexpr (PAIRB) {  // the pair's own four lines: 4 NV E items over its 64 threads
+          const int j = ((int)(threadIdx.x >> 7) * 32 + (int)(threadIdx.x & 31)) + k * 64;
+          el = j % E, v = (j / E) % NV, t = 4 * pair + j / (E * NV);
+          item = j < 4 * NV * E ? 0 : NDI;
+        }
         if (item >= NDI || e0 + el >= g.K) continue;
         const int lb = lbase<D, P>(dd, t), ls = lstr<D, P>(dd);
         double f[NI];
@@ -1235,7 +1263,7 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     }
     if constexpr (!DBUF) {
       if (ph_ >= 1) divergence();
-      __syncthreads();
+      phase_sync(false);
     }
     if constexpr (LDMMA) {
       if (ph_ < D) {
@@ -1348,7 +1376,7 @@ __device__ __forceinline__ void grad_tile(const TensorGeom& g, const Line1D& L, 
     if constexpr (PERS) {
       if (ph_ == D - 1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    __syncthreads();
+    phase_sync(ph_ == D - 1);
   PH(0, 3 + ph_)
   }
 }
