@@ -136,6 +136,15 @@
 #ifndef SDRT_TA_PAIRB
 #define SDRT_TA_PAIRB 0
 #endif
+// kernel B walks the tiles in reverse launch order (CTA i takes tile grid - 1 - i): kernel
+// A runs first tile -> last, so kernel B starts on the tiles whose R_int and published
+// fluxes kernel A wrote last (still in the 126 MB L2) and ends on the first tiles, which
+// the next stage's kernel A reads first.  Tile order only: bitwise.  1 (default): the
+// one-sided publication kernel B only (c4, working set >> L2: 36.1 -> 36.5 GDOF-stage/s);
+// 2: the two-sided kernel B as well (measured slower on the L2-resident c3: 35.0 -> 34.5).
+#ifndef SDRT_TB_REV
+#define SDRT_TB_REV 1
+#endif
 
 namespace sdrt {
 
@@ -1452,7 +1461,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage(TensorGeom g, Line1D L, Phy
   double* sUn = sAcc + (stage_reads_acc(stage) ? NS * NV * E : 0);  // RK register u_n (RK4 stages 1, 2)
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar[2];
-  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  const int bx = SDRT_TB_REV == 2 ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[bx] : bx) * E;
   // every element-local input of the tile is requested up front by TMA: the stage
   // input (barrier 0), then R_int and the RK registers (barrier 1), waited for only
   // where they are used
@@ -1830,7 +1840,8 @@ __global__ void __launch_bounds__(NT, MINB) kt_stage_osf(TensorGeom g, Line1D L,
   pdl_wait();
   __shared__ int sNb[2 * D][E];
   __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  const int bx = SDRT_TB_REV != 0 ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[bx] : bx) * E;
   stage_osf_tile<D, P, EQ, E, NT, FEXP>(g, L, ph, b, stage, dt, tm, e0, sNb, &bar, true, 0);
 }
 
