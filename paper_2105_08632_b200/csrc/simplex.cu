@@ -123,6 +123,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #ifndef SDRT_SB_PF
 #define SDRT_SB_PF 1
 #endif
+#ifndef SDRT_SB_REV
+#define SDRT_SB_REV 0
+#endif
 #ifndef SDRT_SB_NT
 #define SDRT_SB_NT 160
 #endif
@@ -1227,7 +1230,9 @@ __global__ void __launch_bounds__(SDRT_SB_NT, SDRT_SB_MINB_OSF) ks_stage_osf(Geo
   double* sD = sAcc + Ly::U * E;  // D~ [next][NV][E]
   __shared__ int sNb[D + 2][E];
   __shared__ __align__(8) uint64_t bar;
-  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[blockIdx.x] : (int)blockIdx.x) * E;
+  // SDRT_SB_REV: reverse tile order (kernel A's last-written tiles first, see tensor.cu SDRT_TB_REV)
+  const int bx = SDRT_SB_REV ? (int)(gridDim.x - 1 - blockIdx.x) : (int)blockIdx.x;
+  const int64_t e0 = (int64_t)(g.tiles ? g.tiles[bx] : bx) * E;
   const bool need_in = stage == 0 || stage >= RK54_STAGE0;
   constexpr unsigned TB = S::nsol * NV * E * 8;
   if (threadIdx.x == 0) {
