@@ -145,6 +145,11 @@
 #ifndef SDRT_TB_REV
 #define SDRT_TB_REV 1
 #endif
+// one-sided kernel B: TMA loads with an L2 evict-first policy for R_int (1: read once, dead
+// afterwards) and also for the RK registers u_n and ACC (2: next read a whole stage later)
+#ifndef SDRT_TB_EF
+#define SDRT_TB_EF 0
+#endif
 
 namespace sdrt {
 
@@ -1727,10 +1732,11 @@ __device__ __forceinline__ void stage_osf_tile(const TensorGeom& g, const Line1D
     const unsigned bytes = TB * ((DIRECT ? 0 : 1) + (need_in ? 1 : 0) + (!DIRECT && stage_reads_un(stage) ? 1 : 0) +
                                  (stage_reads_acc(stage) ? 1 : 0));
     mbar_expect_tx(&bar, bytes);
-    if (!DIRECT) tma_tile<NS * NV, E>(sR, &tm.rv, e0, &bar);
+    constexpr bool EF = SDRT_TB_EF != 0;  // read-once streams: L2 evict-first
+    if (!DIRECT) tma_tile<NS * NV, E, EF>(sR, &tm.rv, e0, &bar);
     if (need_in) tma_tile<NS * NV, E>(sU, &tm.uin, e0, &bar);
-    if (!DIRECT && stage_reads_un(stage)) tma_tile<NS * NV, E>(sUn, &tm.un, e0, &bar);
-    if (stage_reads_acc(stage)) tma_tile<NS * NV, E>(sAcc, &tm.acc, e0, &bar);
+    if (!DIRECT && stage_reads_un(stage)) tma_tile<NS * NV, E, (SDRT_TB_EF > 1)>(sUn, &tm.un, e0, &bar);
+    if (stage_reads_acc(stage)) tma_tile<NS * NV, E, (SDRT_TB_EF > 1)>(sAcc, &tm.acc, e0, &bar);
   }
   fill_nbrs<D, E>(g, sNb, e0);
   __syncthreads();

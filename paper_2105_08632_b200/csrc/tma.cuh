@@ -39,6 +39,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// the same with an L2 evict-first policy: for tiles read once and dead afterwards (R_int)
+__device__ __forceinline__ void tma_load_2d_ef(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+      "[%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // rows per TMA box: the largest divisor of the row count that is <= 256
 __host__ __device__ constexpr int tma_box_rows(int rows) {
   int b = rows < 256 ? rows : 256;
@@ -47,11 +58,14 @@ __host__ __device__ constexpr int tma_box_rows(int rows) {
 }
 
 // whole tile [ROWS][E] of one array, issued by one thread, completing on bar
-template <int ROWS, int E>
+template <int ROWS, int E, bool EF = false>
 __device__ __forceinline__ void tma_tile(double* dst, const CUtensorMap* map, int64_t e0, uint64_t* bar) {
   constexpr int BR = tma_box_rows(ROWS);
 #pragma unroll
-  for (int r = 0; r < ROWS; r += BR) tma_load_2d(dst + r * E, map, (int)e0, r, bar);
+  for (int r = 0; r < ROWS; r += BR) {
+    if constexpr (EF) tma_load_2d_ef(dst + r * E, map, (int)e0, r, bar);
+    else tma_load_2d(dst + r * E, map, (int)e0, r, bar);
+  }
 }
 
 // host: descriptor of a [rows][Kp] fp64 array, boxes of E x tma_box_rows(rows)
